@@ -1,0 +1,334 @@
+"""Pins for the oracle's filter (window engine, pairwise criteria, argmin).
+
+Every expected value here comes from somewhere other than the oracle:
+closed forms for special windows (derived by hand from Eq. 5 / Eq. 8 and the
+readings R2-R3 in DESIGN.md), the paper's printed coefficients
+(tests/golden/paper_tables.txt) evaluated in 50-digit mpmath, an independent
+formula for the angle (atan2 of |a x b| and a.b instead of arccos/arcsin
+branches), the simplified closed form of the exp argument (n^(1+kappa/3)
+d1/(2 S1) instead of Eq. 8's bandwidth chain), hand-indexed windows (Fig. 1,
+S:68-75) and invariants.
+"""
+import itertools
+import math
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import oracle
+import vfsynth
+
+mp.mp.dps = 50
+KAPPA = mp.mpf("0.33")
+
+
+@pytest.fixture(scope="module")
+def T(paper_tables):
+    return {k: [mp.mpf(repr(v)) for v in d["values"]] for k, d in paper_tables.items()}
+
+
+def hornerm(a, z):
+    r = mp.mpf(0)
+    for c in reversed(a):
+        r = r * z + c
+    return r
+
+
+# ----------------------------------------------------------------- mpmath ref
+def mp_pair_angular(a, b, var, T):
+    a = [int(v) for v in a]
+    b = [int(v) for v in b]
+    nna, nnb = sum(v * v for v in a), sum(v * v for v in b)
+    if nna == 0 or nnb == 0:
+        return mp.mpf(0)
+    D = sum(x * y for x, y in zip(a, b))
+    if var == "exact":
+        cx = [a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]]
+        return mp.atan2(mp.sqrt(sum(v * v for v in cx)), D)      # the angle, independently
+    c = mp.mpf(D) / (mp.sqrt(nna) * mp.sqrt(nnb))
+    if 4 * D * D < nna * nnb:                                    # c < 0.5, exactly
+        return hornerm(T["ARCCOS"], c)
+    return hornerm(T["ARCSIN"], mp.sqrt(max(mp.mpf(0), 1 - c)))
+
+
+def mp_window(samples, crit, var, T):
+    s = [tuple(int(v) for v in x) for x in samples]
+    n = len(s)
+    Dm = [[mp.mpf(0)] * n for _ in range(n)]
+    d1 = [[sum(abs(p - q) for p, q in zip(s[i], s[j])) for j in range(n)] for i in range(n)]
+    S1 = sum(d1[i][j] for i in range(n) for j in range(i + 1, n))
+    for i in range(n):
+        for j in range(i + 1, n):
+            if crit == "angular":
+                d = mp_pair_angular(s[i], s[j], var, T)
+            elif S1 == 0:
+                d = mp.mpf(0)
+            elif crit == "exp":
+                z = mp.mpf(n) ** (1 + KAPPA / 3) * d1[i][j] / (2 * S1)
+                if var == "exact":
+                    e = mp.exp(-z)
+                elif var == "minimax":
+                    e = hornerm(T["EXP_NUM"], z) / hornerm(T["EXP_DEN"], z)
+                else:
+                    e = hornerm(T["EXP_P4"], z)
+                d = 1 - e
+            else:
+                q = mp.mpf(n - 1) * d1[i][j] / S1
+                sv = 1 - (1 - mp.exp(-1)) * q
+                if var == "exact":
+                    d = -sv * mp.log(sv)
+                else:
+                    d = -hornerm(T["ENT_NUM"], sv) / hornerm(T["ENT_DEN"], sv)
+            Dm[i][j] = Dm[j][i] = d
+    R = [mp.fsum(Dm[i][j] for j in range(n) if j != i) for i in range(n)]
+    return R
+
+
+CV = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp", "minimax"),
+      ("exp", "poly4"), ("log", "exact"), ("log", "minimax")]
+
+
+# ------------------------------------------------------- angular closed forms
+@pytest.mark.parametrize("pos", [0, 4, 8])
+def test_angular_spec_example(pos, T):
+    """eight (100,0,0) and one (0,100,0)."""
+    s = np.array([[100, 0, 0]] * 9, np.uint8)
+    s[pos] = [0, 100, 0]
+    k, R, _ = oracle.window(s, "angular", "exact")
+    inl = [i for i in range(9) if i != pos]
+    assert k == inl[0]
+    np.testing.assert_allclose(R[inl], math.pi / 2, rtol=1e-15)
+    assert R[pos] == pytest.approx(4 * math.pi, rel=1e-15)
+    k, R, _ = oracle.window(s, "angular", "minimax")
+    a0s, a0c = float(T["ARCSIN"][0]), float(T["ARCCOS"][0])
+    assert k == inl[0]
+    np.testing.assert_allclose(R[inl], 7 * a0s + a0c, rtol=1e-14)
+    assert R[pos] == pytest.approx(8 * a0c, rel=1e-14)
+
+
+@pytest.mark.parametrize("v", [1, 7, 100, 255])
+def test_angular_branch_point(v, T):
+    """(v,v,0) & (0,v,v): cos = 0.5 exactly; Eq. 6 applies for z >= 0.5, so the
+    minimax value is the ARCSIN row at tau = sqrt(0.5) (reading R5)."""
+    for a, b in [((v, v, 0), (0, v, v)), ((v, 0, v), (v, v, 0)), ((0, v, v), (v, 0, v))]:
+        de = oracle.pair_angular(a, b, "exact")
+        dm = oracle.pair_angular(a, b, "minimax")
+        assert de == pytest.approx(math.pi / 3, rel=1e-15)
+        assert dm == pytest.approx(float(hornerm(T["ARCSIN"], mp.sqrt(mp.mpf(1) / 2))), rel=1e-15)
+        assert abs(dm - float(hornerm(T["ARCCOS"], mp.mpf(1) / 2))) > 3e-5
+
+
+def test_angular_zero_vector_rule():
+    """a zero-norm vector has angle 0 to everything."""
+    for var in ("exact", "minimax"):
+        assert oracle.pair_angular((0, 0, 0), (10, 200, 3), var) == 0.0
+        assert oracle.pair_angular((0, 0, 0), (0, 0, 0), var) == 0.0
+    s = np.array([[0, 0, 0]] + [[50, 60, 70]] * 8, np.uint8)
+    k, R, _ = oracle.window(s, "angular", "exact")
+    assert R[0] == 0.0 and k == 0
+
+
+def test_angular_parallel_pairs_exact_zero():
+    for a, b in [((1, 2, 3), (2, 4, 6)), ((255, 255, 255), (1, 1, 1)), ((0, 5, 0), (0, 9, 0))]:
+        assert oracle.pair_angular(a, b, "exact") == 0.0
+
+
+def test_angular_random_pairs_vs_atan2(T):
+    rng = np.random.default_rng(1)
+    pts = rng.integers(0, 256, size=(3000, 2, 3))
+    # near-parallel and near-60-degree pairs too
+    base = rng.integers(1, 256, size=(500, 3))
+    pts = np.concatenate([pts, np.stack([base, np.clip(base + rng.integers(-1, 2, size=base.shape), 0, 255)], 1)])
+    for var in ("exact", "minimax"):
+        for a, b in pts:
+            got = oracle.pair_angular(a.astype(np.uint8), b.astype(np.uint8), var)
+            ref = mp_pair_angular(a, b, var, T)
+            assert abs(got - float(ref)) <= 1e-12 * abs(float(ref)) + 1e-15, (a, b, var, got, ref)
+
+
+# --------------------------------------------------- single-impulse windows
+def _impulse_window(n, pos, a, b):
+    s = np.array([a] * n, np.uint8)
+    s[pos] = b
+    return s
+
+
+@pytest.mark.parametrize("n", [9, 25])
+@pytest.mark.parametrize("pos,a,b", [(0, (10, 20, 30), (200, 5, 90)), (4, (0, 0, 0), (255, 255, 255)),
+                                     (8, (128, 128, 128), (129, 128, 128))])
+def test_single_impulse_closed_forms(n, pos, a, b, T):
+    """n-1 equal samples + one impulse, any colours: with d = |a-b|_1,
+    S1 = (n-1) d, so z* = n^(1+kappa/3) / (2 (n-1)) and q* = 1, s* = 1/e."""
+    s = _impulse_window(n, pos, a, b)
+    zs = mp.mpf(n) ** (1 + KAPPA / 3) / (2 * (n - 1))
+    E = lambda z: hornerm(T["EXP_NUM"], z) / hornerm(T["EXP_DEN"], z)
+    P4 = lambda z: hornerm(T["EXP_P4"], z)
+    ENTm = lambda s_: hornerm(T["ENT_NUM"], s_) / hornerm(T["ENT_DEN"], s_)
+    einv = mp.exp(-1)
+    cases = {
+        ("exp", "exact"): (1 - mp.exp(-zs), mp.mpf(0)),
+        ("exp", "minimax"): (1 - E(zs), 1 - E(mp.mpf(0))),
+        ("exp", "poly4"): (1 - P4(zs), 1 - P4(mp.mpf(0))),
+        ("log", "exact"): (einv, mp.mpf(0)),              # -s ln s at s = 1/e, and at s = 1
+        ("log", "minimax"): (-ENTm(einv), -ENTm(mp.mpf(1))),
+    }
+    inl = [i for i in range(n) if i != pos]
+    for (crit, var), (d_imp, d_same) in cases.items():
+        k, R, _ = oracle.window(s, crit, var)
+        r_in = (n - 2) * d_same + d_imp
+        r_imp = (n - 1) * d_imp
+        np.testing.assert_allclose(R[inl], float(r_in), rtol=1e-13)
+        assert R[pos] == pytest.approx(float(r_imp), rel=1e-13)
+        assert k == inl[0]
+
+
+def test_single_impulse_known_numbers():
+    """The survey's colour-independent constants for n=9."""
+    s = _impulse_window(9, 4, (10, 10, 10), (90, 10, 10))
+    _, R, _ = oracle.window(s, "exp", "exact")
+    assert R[0] == pytest.approx(0.5114387928, abs=1e-10)
+    assert R[4] == pytest.approx(4.0915103422, abs=1e-10)
+    _, R, _ = oracle.window(s, "log", "exact")
+    assert R[0] == pytest.approx(1 / math.e, rel=1e-14)
+    assert R[4] == pytest.approx(8 / math.e, rel=1e-14)
+
+
+# ----------------------------------------------------------- brute force
+@pytest.mark.parametrize("n", [9, 25])
+@pytest.mark.parametrize("crit,var", CV)
+def test_random_windows_vs_mpmath(n, crit, var, T):
+    rng = np.random.default_rng(100 + n)
+    n_win = 40 if n == 9 else 8
+    for t in range(n_win):
+        if t % 3 == 0:      # duplicates / palette -> ties, parallel vectors, zero vectors
+            s = rng.choice(np.array([0, 1, 2, 127, 128, 255], np.uint8), size=(n, 3))
+        elif t % 3 == 1:    # smooth region + impulses
+            s = np.clip(rng.integers(100, 104, size=(n, 3)), 0, 255).astype(np.uint8)
+            m = rng.random(n) < 0.2
+            s[m] = rng.integers(0, 256, size=(m.sum(), 3))
+        else:
+            s = rng.integers(0, 256, size=(n, 3)).astype(np.uint8)
+        k, R, Dm = oracle.window(s, crit, var)
+        Rm = mp_window(s, crit, var, T)
+        Rf = np.array([float(v) for v in Rm])
+        np.testing.assert_allclose(R, Rf, rtol=1e-12, atol=1e-14)
+        # argmin: lowest index among exact ties; near-ties may go either way
+        m = min(Rm)
+        cand = [i for i in range(n) if Rm[i] - m <= mp.mpf("1e-12") * max(abs(m), 1)]
+        assert k in cand
+        # (mathematically tied aggregates may differ by an ulp in double because
+        # each R_i is summed in its own order; the lowest-index rule is pinned on
+        # bit-tied windows in test_constant_image_unchanged / the SPEC example)
+        if len(cand) == 1:
+            assert k == cand[0]
+        assert np.array_equal(Dm, Dm.T)
+        assert np.all(np.diag(Dm) == 0)
+
+
+# ------------------------------------------------------------- invariants
+def _img(seed=3, H=40, W=48):
+    spec = vfsynth.ImageSpec("t", H, W, 1, (3,), 6, False, "uncorrelated", 0.15, seed=seed)
+    return vfsynth.make_image(spec, 0)
+
+
+@pytest.mark.parametrize("w", [3, 5])
+@pytest.mark.parametrize("crit,var", CV)
+def test_output_is_window_member(w, crit, var):
+    _, x = _img()
+    out, idx, agg = oracle.filter_image(x, w, crit, var, want_agg=True)
+    H, W = x.shape[:2]
+    for y in range(0, H, 3):
+        for xx in range(0, W, 5):
+            s = oracle.gather_window(x, w, y, xx)
+            assert np.array_equal(out[y, xx], s[idx[y, xx]])
+            assert agg[y, xx, idx[y, xx]] == agg[y, xx].min()
+
+
+@pytest.mark.parametrize("crit,var", CV)
+def test_constant_image_unchanged(crit, var):
+    x = np.full((12, 10, 3), 77, np.uint8)
+    x[..., 1] = 3
+    for w in (3, 5):
+        out, idx, _ = oracle.filter_image(x, w, crit, var)
+        assert np.array_equal(out, x)
+        assert np.all(idx == 0)    # all aggregates tie -> lowest index
+
+
+@pytest.mark.parametrize("crit,var", CV)
+def test_noise_free_flat_region_unchanged(crit, var):
+    c, _ = _img()
+    x = c.copy()
+    x[10:30, 10:30] = (40, 150, 220)
+    out, _, _ = oracle.filter_image(x, 3, crit, var)
+    assert np.array_equal(out[11:29, 11:29], x[11:29, 11:29])
+
+
+@pytest.mark.parametrize("crit,var", CV)
+def test_scale_invariance_bit_exact(crit, var):
+    """S:336 (angles are scale invariant); every criterion here depends on
+    the window only through scale-free ratios, and scaling by 2 is exact in
+    binary floating point, so the aggregates must be bit-identical."""
+    rng = np.random.default_rng(7)
+    x = rng.integers(0, 128, size=(14, 15, 3)).astype(np.uint8)
+    o1, i1, a1 = oracle.filter_image(x, 3, crit, var, want_agg=True)
+    o2, i2, a2 = oracle.filter_image(2 * x, 3, crit, var, want_agg=True)
+    assert np.array_equal(i1, i2)
+    assert np.array_equal(a1, a2)
+
+
+@pytest.mark.parametrize("n", [9, 25])
+def test_argument_bounds(n):
+    """Triangle inequality: sum_{k<l} d1 >= (n-1) d1_ij, so q <= 1 and
+    z <= z*_n; hence the EXP and ENT cutoffs are never reached and each D lies
+    below its single-impulse value."""
+    rng = np.random.default_rng(n)
+    zs = n ** (1 + 0.33 / 3) / (2 * (n - 1))
+    for _ in range(200):
+        s = rng.integers(0, 256, size=(n, 3)).astype(np.uint8)
+        s[rng.random(n) < 0.5] = s[0]
+        _, _, De = oracle.window(s, "exp", "exact")
+        _, _, Dl = oracle.window(s, "log", "exact")
+        assert De.max() <= 1 - math.exp(-zs) + 1e-15
+        assert Dl.max() <= 1 / math.e + 1e-15
+        assert De.min() >= 0 and Dl.min() >= 0
+
+
+# ----------------------------------------------------------- window engine
+def test_gather_window_indexing():
+    """Fig. 1 raster indexing and replicate padding."""
+    x = np.arange(5 * 5 * 3, dtype=np.uint8).reshape(5, 5, 3)
+    s = oracle.gather_window(x, 3, 1, 1)
+    assert np.array_equal(s[0], x[0, 0])          # index 1 (1-based) = top-left
+    assert np.array_equal(s[4], x[1, 1])          # centre C = (n+1)/2
+    assert np.array_equal(s.reshape(3, 3, 3), x[0:3, 0:3])
+    for w in (3, 5):
+        s = oracle.gather_window(x, w, 0, 0)
+        cnt = sum(np.array_equal(v, x[0, 0]) for v in s)
+        assert cnt == (w // 2 + 1) ** 2          # corner appears ceil(w/2)^2 times
+    s = oracle.gather_window(x, 3, 4, 2)
+    assert np.array_equal(s[6], x[4, 1]) and np.array_equal(s[7], x[4, 2])
+
+
+def test_invalid_arguments():
+    x = np.zeros((8, 8, 3), np.uint8)
+    for w in (2, 4, 1, 9):
+        with pytest.raises(ValueError):
+            oracle.filter_image(x, w, "angular", "exact")
+    with pytest.raises(ValueError):
+        oracle.filter_image(x, 3, "angular", "poly4")
+    with pytest.raises(ValueError):
+        oracle.filter_image(x, 3, "log", "poly4")
+    with pytest.raises(ValueError):
+        oracle.filter_image(x[:2], 3, "exp", "exact")
+
+
+@pytest.mark.parametrize("crit,var", CV)
+def test_filter_pixels_matches_filter_image(crit, var):
+    _, x = _img(seed=9, H=33, W=29)
+    out, idx, agg = oracle.filter_image(x, 5, crit, var, want_agg=True)
+    ys, xs = np.meshgrid(np.arange(0, 33, 4), np.arange(0, 29, 3), indexing="ij")
+    o, i, a = oracle.filter_pixels(x, 5, crit, var, ys.ravel(), xs.ravel())
+    assert np.array_equal(o, out[ys.ravel(), xs.ravel()])
+    assert np.array_equal(i, idx[ys.ravel(), xs.ravel()])
+    assert np.array_equal(a, agg[ys.ravel(), xs.ravel()])
