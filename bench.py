@@ -1,0 +1,378 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path (BASELINE.json metric: Mpixels/s per criterion,
+exact vs minimax, 3x3/5x5, % of the FP32 FMA roofline).
+
+One STEP = one synthetic image of the chosen config (default C2 = configs[1]:
+512x512, 3x3 window, 10% correlated impulse noise) filtered by all seven
+criterion x variant kernels (angular/exp/log x exact/minimax + exp poly4).
+Inputs are resident in HBM before the timed region; L2 is flushed (a 512 MiB
+write) between timed steps, outside the per-step CUDA-event windows.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+N > 1 runs under torch.distributed.run: each rank filters its own image
+(image id = rank), no collective on the data path (weak scaling); the
+reported time is the max over ranks.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+COMBOS = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp", "minimax"),
+          ("exp", "poly4"), ("log", "exact"), ("log", "minimax")]
+
+# Algorithmic FP32 flops per pair (SURVEY.md 8(d) D4 counting rules: FMA = 2,
+# add/sub/mul = 1; robustness overhead not counted).  Exact variants: the
+# method's arithmetic around the libm call plus the FP32 flops of CUDA's libm
+# routine itself as compiled for sm_100a.
+FLOPS_PER_PAIR = {
+    ("angular", "minimax"): 18, ("exp", "minimax"): 26, ("exp", "poly4"): 18, ("log", "minimax"): 26,
+    ("angular", "exact"): 10 + 22, ("exp", "exact"): 10 + 28, ("log", "exact"): 11 + 30,
+}
+NOMINAL_FP32_TFLOPS_AT_MAX = 2 * 128 * 148 * 1.965e9 / 1e12   # 74.4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ workload
+def workload(cfg):
+    import vfsynth
+    spec = vfsynth.config(cfg)
+    w = spec.window[-1] if cfg == "C3" else spec.window[0]
+    return spec, w
+
+
+def make_input(spec, rank):
+    """This rank's input: one image of the config (C3: the batch of 8 images;
+    C4: a 16-image slice of the 1024-image batch)."""
+    import numpy as np
+    import vfsynth
+    if spec.name == "C3":
+        return vfsynth.make_batch(spec)
+    if spec.name == "C4":
+        return vfsynth.make_batch(spec, ids=range(rank * 16, rank * 16 + 16))
+    return vfsynth.make_image(spec, rank % max(spec.batch, 1) if spec.batch > 1 else rank)[1][None]
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def ncu_traffic(key):
+    """Per-launch DRAM bytes of the kernel from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch", {}).get(key)
+    except Exception:
+        return None
+
+
+def cpu_oracle_rate(spec, w, x_np, budget_s=12.0, combos=COMBOS):
+    """The oracle as it stands on the host cores: run whole steps (all 7
+    combos over this image) until ~budget_s of CPU time; Mpix/s."""
+    import oracle
+    t0 = time.perf_counter()
+    steps = 0
+    pix = 0
+    while True:
+        for b in range(x_np.shape[0]):
+            for crit, var in combos:
+                oracle.filter_image(x_np[b], w, crit, var, want_index=False)
+                pix += x_np.shape[1] * x_np.shape[2]
+        steps += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return pix / dt / 1e6, steps, dt, oracle.max_threads()
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    spec, w = workload(args.config)
+    x = make_input(spec, 0)
+    if spec.name in ("C3", "C4", "C5"):
+        # bounded sample: a 512-row band of the first image keeps a step to seconds
+        x = x[:1, :512]
+    import oracle
+    oracle.build()
+    npix = x.shape[0] * x.shape[1] * x.shape[2]
+    for _ in range(args.warmup):
+        for crit, var in COMBOS:
+            oracle.filter_image(x[0], w, crit, var, want_index=False)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        for b in range(x.shape[0]):
+            for crit, var in COMBOS:
+                oracle.filter_image(x[b], w, crit, var, want_index=False)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = len(COMBOS) * npix / (ms / 1e3) / 1e6
+    line = {
+        "impl": "reference", "metric": "filtered Mpixels/s (7 criterion x variant filters per pixel)",
+        "value": value, "unit": "Mpix/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{spec.name}: {x.shape[1]}x{x.shape[2]} x{x.shape[0]}, {w}x{w}, all 7 "
+                               "criterion/variant filters (CPU oracle, bounded sample)" },
+        "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": oracle.max_threads(), "kind": "oracle",
+                         "sample": f"{args.steps} steps x 7 filters of {x.shape[1]}x{x.shape[2]}x{x.shape[0]} px"},
+        "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    import paper_1009_0959_b200 as vfb
+    vfb.load_library()
+    spec, w = workload(args.config)
+    x_np = make_input(spec, rank)
+    B, H, W = x_np.shape[:3]
+    npix = B * H * W
+    x = torch.from_numpy(x_np).to(dev)
+    outs = {c: torch.empty_like(x) for c in COMBOS}
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step(events=None):
+        for i, (crit, var) in enumerate(COMBOS):
+            if events is not None:
+                events[i].record(stream)
+            vfb.vf_filter_batch(x, w, crit, var, out=outs[(crit, var)], stream=stream)
+        if events is not None:
+            events[len(COMBOS)].record(stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region: K steps, per-step CUDA events, L2 flush between steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(COMBOS) + 1)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index if world == 1 else local) as clk:
+        t_wall0 = time.perf_counter()
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)            # outside the event windows
+            step(ev[k])
+        torch.cuda.synchronize(dev)
+        t_wall = time.perf_counter() - t_wall0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    per_kernel_ms = [[ev[k][i].elapsed_time(ev[k][i + 1]) for i in range(len(COMBOS))] for k in range(args.steps)]
+    step_ms = [sum(r) for r in per_kernel_ms]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    units = world * npix * len(COMBOS)               # pixel-filter evaluations per step, all ranks
+    value = units / (ms_per_step / 1e3) / 1e6        # Mpix/s
+
+    # ---- per-kernel breakdown + roofline of the dominant kernel
+    clocks = clk.summary()
+    n = w * w
+    pairs = n * (n - 1) // 2
+    kern = {}
+    for i, c in enumerate(COMBOS):
+        ms = statistics.mean(r[i] for r in per_kernel_ms)
+        mpix = npix / (ms / 1e3) / 1e6
+        tfl = FLOPS_PER_PAIR[c] * pairs * npix / (ms / 1e3) / 1e12
+        kern[f"{c[0]}/{c[1]}"] = {"ms": ms, "mpix_s": mpix, "alg_tflops": tfl,
+                                  "frac_fp32_at_max_clock": tfl / NOMINAL_FP32_TFLOPS_AT_MAX}
+        if clocks.get("sm_mhz"):
+            kern[f"{c[0]}/{c[1]}"]["frac_fp32_at_measured_clock"] = \
+                tfl / (NOMINAL_FP32_TFLOPS_AT_MAX * clocks["sm_mhz"] / 1965.0)
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    d = kern[dom]
+    roofline = {"bound": "alu", "kernel": f"vf_window_kernel<{w},{dom}>", "achieved": d["alg_tflops"],
+                "peak": NOMINAL_FP32_TFLOPS_AT_MAX, "unit": "TFLOP/s", "frac": d["alg_tflops"] / NOMINAL_FP32_TFLOPS_AT_MAX,
+                "peak_source": "derived: 2 flop x 128 FP32 lanes x 148 SM x 1.965 GHz (DESIGN.md 6.1)",
+                "traffic": ncu_traffic(f"{w}x{w}/{dom}"),
+                "algorithmic_flops_per_launch": FLOPS_PER_PAIR[tuple(dom.split("/"))] * pairs * npix}
+    mm = [k for k in kern if k.endswith("minimax") or k.endswith("poly4")]
+    best_mm = max(mm, key=lambda k: kern[k]["frac_fp32_at_max_clock"])
+
+    # ---- end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_in = torch.from_numpy(x_np).pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        ws = torch.empty(vfb.vf_host_workspace_bytes(B, H, W), dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            for crit, var in COMBOS:
+                vfb.vf_filter_host(h_in, w, crit, var, h_out, ws, stream=stream)
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        ksteps = max(3, min(args.steps, 20))
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(ksteps):
+            for crit, var in COMBOS:
+                vfb.vf_filter_host(h_in, w, crit, var, h_out, ws, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = e0.elapsed_time(e1) / ksteps
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": units / (e2e_ms / 1e3) / 1e6, "unit": "Mpix/s",
+               "h2d_bytes_per_step": len(COMBOS) * npix * 3, "d2h_bytes_per_step": len(COMBOS) * npix * 3,
+               "ms_per_step": e2e_ms, "api": "vf_filter_host (pinned host in/out, one call per filter)"}
+
+    # ---- fidelity: minimax vs exact (the paper's quality measure)
+    fid = {}
+    for crit, mmv in (("angular", "minimax"), ("exp", "minimax"), ("exp", "poly4"), ("log", "minimax")):
+        f = vfb.fidelity(outs[(crit, "exact")], outs[(crit, mmv)])
+        fid[f"{crit}/{mmv}"] = {"psnr_db": f["psnr_db"], "ncd": f["ncd"], "diff_frac": f["diff_frac"]}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        xs = x_np if spec.name in ("C1", "C2") else x_np[:1, :256]
+        v, steps_done, dt, cores = cpu_oracle_rate(spec, w, xs)
+        cpu = {"value": v, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
+               "sample": f"{steps_done} x (7 filters over {xs.shape[0]}x{xs.shape[1]}x{xs.shape[2]} px), {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "filtered Mpixels/s (7 criterion x variant filters per pixel; per-kernel Mpix/s and "
+                      "% of FP32 roofline in per_kernel)",
+            "value": value, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{spec.name}: {B}x{H}x{W} uint8 RGB, {w}x{w} window, "
+                                   f"{spec.noise} impulse noise, all 7 criterion/variant filters per step",
+                       "per_rank_pixels": npix, "l2": "flushed between steps (512 MiB write, untimed)",
+                       "parallelism": f"dp{world} (independent images per rank)"},
+            "roofline": roofline,
+            "best_minimax_kernel": {"kernel": best_mm, **kern[best_mm]},
+            "per_kernel": kern,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "fidelity_minimax_vs_exact": fid,
+            "gpu_launches": len(COMBOS) * args.steps,
+            "clocks": clocks,
+            "wall_s_timed_region": t_wall,
+            "peaks": {"hbm_gbs": measured_peaks().get("hbm_gbs"),
+                      "fp32_tflops_nominal_at_max_clock": NOMINAL_FP32_TFLOPS_AT_MAX},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

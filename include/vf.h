@@ -1,0 +1,137 @@
+/*
+ * vf.h -- C ABI of libvf.so: B200 (sm_100a) order-statistics vector filters
+ * with exact and minimax elementary functions.
+ *
+ * Paper: Celebi, Kingravi, Lukac, Celiker, "Cost-Effective Implementation of
+ * Order-Statistics Based Vector Filters Using Minimax Approximations",
+ * arXiv 1009.0959 (/root/reference/PAPER.md, cited P:<line>).
+ *
+ * OPERATION (every vf_filter* entry point)
+ *   For every output pixel (y, x) take the w x w window W(y, x) of the input
+ *   (w = `window`, n = w*w samples re-indexed in raster order k = dy*w + dx,
+ *   Fig. 1; replicate (clamp) padding at the image border),
+ *   compute the pairwise criterion D(i, j) for all i < j, the aggregates
+ *   R_i = sum_{j != i} D(i, j) and output x_{k*}, k* = argmin_i R_i
+ *   (Eq. 5), the lowest index winning bit-equal aggregates.
+ *   Criteria (readings R2-R5):
+ *     VF_ANGULAR  D = angle between x_i and x_j (Eq. 5); exact = libm
+ *                 arccos / Eq. 6 identity; minimax = Table 1 composite
+ *                 (ARCCOS row for cos < 0.5, ARCSIN row in tau = sqrt(1-cos)
+ *                 otherwise; Eqs. 6-7).  Zero vectors give 0.
+ *     VF_EXP      D = 1 - exp(-z), z = |x_i-x_j|_1 / h_W, h_W the window mean
+ *                 of Eq. 8's bandwidth h_i (kappa = 0.33);
+ *                 minimax = Table 3 rational (VF_MINIMAX) or Table 2
+ *                 p = 4 polynomial (VF_MINIMAX_POLY4).
+ *     VF_LOG      D = -ENT(s), ENT(s) = s ln s, s = 1 - (1 - 1/e) q,
+ *                 q = (n-1) |x_i-x_j|_1 / sum_{k<l} |x_k-x_l|_1;
+ *                 minimax = Table 4 rational.
+ *   Arithmetic: fp32 on the device, with exact integer geometry (dot
+ *   products, squared norms, L1 distances and the cos < 0.5 branch decision
+ *   are exact); aggregates agree with the double-precision oracle within
+ *   1e-5 relative (tests/test_gpu_parity.py).
+ *
+ * LAYOUT
+ *   Images are uint8 RGB, HWC, row-major, row stride 3*W bytes, batches
+ *   dense [B][H][W][3].  `index` (nullable) is uint8 [..][H][W] holding k*.
+ *   `aggregates` (nullable) is float [..][H][W][n] holding R_0..R_{n-1}.
+ *
+ * OWNERSHIP / EXECUTION
+ *   All buffers are owned by the caller.  Unless stated otherwise they are
+ *   DEVICE pointers (e.g. from PyTorch's caching allocator).  The library never
+ *   allocates, frees or synchronises; every call enqueues work on `stream`
+ *   (a cudaStream_t passed as void*, NULL = legacy default stream) and
+ *   returns immediately.  The library is stateless and thread-safe; the
+ *   only per-thread state is the text of the last error.
+ *
+ * ERRORS
+ *   Every entry point returns a vf_status.  VF_EINVAL: invalid argument
+ *   (window even or < 3, H or W < 1, window > min(H, W), B < 1, NULL
+ *   img/out, input and output ranges overlap, criterion/variant out of range,
+ *   VF_MINIMAX_POLY4 with a criterion other than VF_EXP, a row band that does
+ *   not cover the rows the output stripe reads).  VF_EUNSUPPORTED: an odd
+ *   window >= 7 (valid, not compiled).  VF_ECUDA: a CUDA launch/copy error
+ *   (details from vf_last_error()).  No exception crosses the ABI.  On error
+ *   nothing has been enqueued.
+ */
+#ifndef VF_H_
+#define VF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define VF_API __attribute__((visibility("default")))
+#else
+#define VF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { VF_ANGULAR = 0, VF_EXP = 1, VF_LOG = 2 } vf_criterion;
+typedef enum { VF_EXACT = 0, VF_MINIMAX = 1, VF_MINIMAX_POLY4 = 2 } vf_variant;
+typedef enum { VF_OK = 0, VF_EINVAL = -1, VF_EUNSUPPORTED = -2, VF_ECUDA = -3 } vf_status;
+
+/* Kernel selection for the angular criterion (both variants are window
+ * independent, so pairs may be shared between overlapping windows,
+ * SURVEY.md 8(f1)).  VF_ALGO_AUTO picks the fastest; results are identical
+ * within the parity tolerance either way. */
+typedef enum { VF_ALGO_AUTO = 0, VF_ALGO_WINDOW = 1, VF_ALGO_SHARED = 2 } vf_algo;
+
+/* One image.  img, out: device [H][W][3]; index: device [H][W] or NULL;
+ * aggregates: device [H][W][n] or NULL. */
+VF_API int vf_filter(const uint8_t *img, int H, int W, int window, int criterion, int variant,
+              uint8_t *out, uint8_t *index, float *aggregates, void *stream);
+
+/* Dense batch of B images of equal size: imgs, outs device [B][H][W][3];
+ * index [B][H][W]; aggregates [B][H][W][n]. */
+VF_API int vf_filter_batch(const uint8_t *imgs, int B, int H, int W, int window, int criterion,
+                    int variant, uint8_t *outs, uint8_t *index, float *aggregates, void *stream);
+
+/* Row stripe of one H x W image (the spatial partitioner's call).
+ * band: device pointer to global rows [band_row0, band_row0 + band_rows)
+ * (stride 3W).  Writes global output rows [out_row0, out_row0 + out_rows)
+ * to out (device [out_rows][W][3]; index [out_rows][W]; aggregates
+ * [out_rows][W][n]).  Border clamping uses the GLOBAL image rows [0, H); the
+ * band must contain every clamped row the stripe reads, i.e.
+ * band_row0 <= max(out_row0 - w/2, 0) and
+ * band_row0 + band_rows >= min(out_row0 + out_rows + w/2, H). */
+VF_API int vf_filter_rows(const uint8_t *band, int band_row0, int band_rows, int H, int W,
+                   int out_row0, int out_rows, int window, int criterion, int variant,
+                   uint8_t *out, uint8_t *index, float *aggregates, void *stream);
+
+/* As vf_filter_batch with an explicit kernel choice (vf_algo). */
+VF_API int vf_filter_batch_algo(const uint8_t *imgs, int B, int H, int W, int window, int criterion,
+                         int variant, int algo, uint8_t *outs, uint8_t *index,
+                         float *aggregates, void *stream);
+
+/* End-to-end call with HOST buffers: h_imgs and h_outs are host [B][H][W][3]
+ * (pinned memory gives asynchronous copies); d_workspace is a caller-owned
+ * device buffer of at least vf_host_workspace_bytes(B, H, W) bytes.  Enqueues
+ * H2D copy -> filter -> D2H copy on `stream`; the caller synchronises the
+ * stream before reading h_outs. */
+VF_API size_t vf_host_workspace_bytes(int B, int H, int W);
+VF_API int vf_filter_host(const uint8_t *h_imgs, int B, int H, int W, int window, int criterion,
+                   int variant, uint8_t *h_outs, void *d_workspace, size_t workspace_bytes,
+                   void *stream);
+
+/* Per-image fidelity statistics of two device image batches a, b
+ * ([B][H][W][3]); stats: device double [B][8] =
+ *   {pixels with a != b, sum |a-b| (all channels), sum (a-b)^2,
+ *    sum |a_Lab - b_Lab|_2, sum |a_Lab|_2, max |a-b|, 0, 0}
+ * (MAE/MSE/NCD of P:286-293; CIELAB via sRGB/D65).  Overwrites stats. */
+VF_API int vf_image_stats(const uint8_t *a, const uint8_t *b, int B, int H, int W, double *stats,
+                   void *stream);
+
+VF_API const char *vf_status_string(int status);
+/* Text of the last error on the calling thread ("" if none). */
+VF_API const char *vf_last_error(void);
+/* ABI version (major*100 + minor). */
+VF_API int vf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VF_H_ */

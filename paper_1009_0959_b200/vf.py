@@ -1,0 +1,222 @@
+"""Thin Python binding of libvf.so (include/vf.h): argument marshalling only.
+
+PyTorch provides device memory and streams; every step of the filter runs in
+the library's CUDA kernels.  There is no CPU fallback: if libvf.so is missing
+or no CUDA device is present, these functions raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libvf.so")
+
+VF_ANGULAR, VF_EXP, VF_LOG = 0, 1, 2
+VF_EXACT, VF_MINIMAX, VF_MINIMAX_POLY4 = 0, 1, 2
+VF_OK, VF_EINVAL, VF_EUNSUPPORTED, VF_ECUDA = 0, -1, -2, -3
+VF_ALGO_AUTO, VF_ALGO_WINDOW, VF_ALGO_SHARED = 0, 1, 2
+
+CRITERIA = {"angular": VF_ANGULAR, "exp": VF_EXP, "log": VF_LOG}
+VARIANTS = {"exact": VF_EXACT, "minimax": VF_MINIMAX, "poly4": VF_MINIMAX_POLY4}
+ALGOS = {"auto": VF_ALGO_AUTO, "window": VF_ALGO_WINDOW, "shared": VF_ALGO_SHARED}
+EXPORTS = ["vf_filter", "vf_filter_batch", "vf_filter_rows", "vf_filter_batch_algo",
+           "vf_host_workspace_bytes", "vf_filter_host", "vf_image_stats", "vf_status_string",
+           "vf_last_error", "vf_version"]
+
+
+class VFError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: status {status} ({msg})")
+        self.status = status
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libvf.so (does not need a GPU).  Raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not found: build it with `python -m paper_1009_0959_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(path)
+    P, I, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    L.vf_filter.argtypes = [P, I, I, I, I, I, P, P, P, P]
+    L.vf_filter_batch.argtypes = [P, I, I, I, I, I, I, P, P, P, P]
+    L.vf_filter_batch_algo.argtypes = [P, I, I, I, I, I, I, I, P, P, P, P]
+    L.vf_filter_rows.argtypes = [P, I, I, I, I, I, I, I, I, I, P, P, P, P]
+    L.vf_host_workspace_bytes.argtypes = [I, I, I]
+    L.vf_host_workspace_bytes.restype = S
+    L.vf_filter_host.argtypes = [P, I, I, I, I, I, I, P, P, S, P]
+    L.vf_image_stats.argtypes = [P, P, I, I, I, P, P]
+    L.vf_status_string.argtypes = [I]
+    L.vf_status_string.restype = ctypes.c_char_p
+    L.vf_last_error.argtypes = []
+    L.vf_last_error.restype = ctypes.c_char_p
+    L.vf_version.argtypes = []
+    for name in ("vf_filter", "vf_filter_batch", "vf_filter_batch_algo", "vf_filter_rows",
+                 "vf_filter_host", "vf_image_stats", "vf_version"):
+        getattr(L, name).restype = I
+    _lib = L
+    return L
+
+
+def _check(rc: int, where: str):
+    if rc != VF_OK:
+        L = load_library()
+        raise VFError(rc, where, L.vf_last_error().decode() or L.vf_status_string(rc).decode())
+
+
+def _crit(c) -> int:
+    return CRITERIA[c] if isinstance(c, str) else int(c)
+
+
+def _var(v) -> int:
+    return VARIANTS[v] if isinstance(v, str) else int(v)
+
+
+def _dev_u8(t: torch.Tensor, name: str):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.uint8 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous uint8 tensor")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _ptr_or_none(t):
+    return None if t is None else t.data_ptr()
+
+
+def vf_filter_batch_algo(imgs: torch.Tensor, window: int, criterion, variant, algo="auto",
+                         out: Optional[torch.Tensor] = None, index: Optional[torch.Tensor] = None,
+                         aggregates: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """imgs: CUDA uint8 [B, H, W, 3] (or [H, W, 3]).  Returns out (same shape)."""
+    L = load_library()
+    single = imgs.dim() == 3
+    x = imgs.unsqueeze(0) if single else imgs
+    if x.dim() != 4 or x.shape[-1] != 3:
+        raise ValueError("expected [B, H, W, 3] or [H, W, 3]")
+    B, H, W, _ = x.shape
+    n = window * window
+    if out is None:
+        out = torch.empty_like(imgs)
+    if index is not None and (index.dtype != torch.uint8 or index.numel() != B * H * W or not index.is_cuda):
+        raise ValueError("index must be CUDA uint8 with B*H*W elements")
+    if aggregates is not None and (aggregates.dtype != torch.float32 or aggregates.numel() != B * H * W * n
+                                   or not aggregates.is_cuda):
+        raise ValueError("aggregates must be CUDA float32 with B*H*W*n elements")
+    rc = L.vf_filter_batch_algo(_dev_u8(x, "imgs"), B, H, W, window, _crit(criterion), _var(variant),
+                                ALGOS[algo] if isinstance(algo, str) else int(algo),
+                                _dev_u8(out, "out"), _ptr_or_none(index), _ptr_or_none(aggregates),
+                                _stream(stream))
+    _check(rc, "vf_filter_batch_algo")
+    return out
+
+
+def vf_filter_batch(imgs, window, criterion, variant, out=None, index=None, aggregates=None, stream=None):
+    return vf_filter_batch_algo(imgs, window, criterion, variant, "auto", out, index, aggregates, stream)
+
+
+def vf_filter(img, window, criterion, variant, out=None, index=None, aggregates=None, stream=None):
+    if img.dim() != 3:
+        raise ValueError("vf_filter expects [H, W, 3]")
+    return vf_filter_batch_algo(img, window, criterion, variant, "auto", out, index, aggregates, stream)
+
+
+def vf_filter_rows(band: torch.Tensor, band_row0: int, H: int, out_row0: int, out_rows: int, window: int,
+                   criterion, variant, out: Optional[torch.Tensor] = None, index=None, aggregates=None,
+                   stream=None) -> torch.Tensor:
+    """band: CUDA uint8 [band_rows, W, 3] holding global rows [band_row0, ...)."""
+    L = load_library()
+    band_rows, W, _ = band.shape
+    if out is None:
+        out = torch.empty((out_rows, W, 3), dtype=torch.uint8, device=band.device)
+    rc = L.vf_filter_rows(_dev_u8(band, "band"), band_row0, band_rows, H, W, out_row0, out_rows, window,
+                          _crit(criterion), _var(variant), _dev_u8(out, "out"), _ptr_or_none(index),
+                          _ptr_or_none(aggregates), _stream(stream))
+    _check(rc, "vf_filter_rows")
+    return out
+
+
+def vf_host_workspace_bytes(B: int, H: int, W: int) -> int:
+    return int(load_library().vf_host_workspace_bytes(B, H, W))
+
+
+def vf_filter_host(h_imgs: torch.Tensor, window: int, criterion, variant, h_out: torch.Tensor,
+                   workspace: torch.Tensor, stream=None) -> torch.Tensor:
+    """End-to-end call on HOST tensors (pinned for async copies): enqueues
+    H2D -> filter -> D2H on the stream; synchronise before reading h_out."""
+    L = load_library()
+    x = h_imgs.unsqueeze(0) if h_imgs.dim() == 3 else h_imgs
+    B, H, W, _ = x.shape
+    for t, nm in ((x, "h_imgs"), (h_out, "h_out")):
+        if t.is_cuda or t.dtype != torch.uint8 or not t.is_contiguous():
+            raise ValueError(f"{nm} must be a contiguous uint8 host tensor")
+    if not workspace.is_cuda:
+        raise ValueError("workspace must be a CUDA tensor")
+    rc = L.vf_filter_host(x.data_ptr(), B, H, W, window, _crit(criterion), _var(variant), h_out.data_ptr(),
+                          workspace.data_ptr(), workspace.numel() * workspace.element_size(), _stream(stream))
+    _check(rc, "vf_filter_host")
+    return h_out
+
+
+def vf_image_stats(a: torch.Tensor, b: torch.Tensor, stats: Optional[torch.Tensor] = None,
+                   stream=None) -> torch.Tensor:
+    """Per-image [B, 8] float64 statistics (see include/vf.h)."""
+    L = load_library()
+    x = a.unsqueeze(0) if a.dim() == 3 else a
+    B, H, W, _ = x.shape
+    if stats is None:
+        stats = torch.empty((B, 8), dtype=torch.float64, device=a.device)
+    rc = L.vf_image_stats(_dev_u8(a, "a"), _dev_u8(b, "b"), B, H, W, stats.data_ptr(), _stream(stream))
+    _check(rc, "vf_image_stats")
+    return stats
+
+
+def vf_status_string(status: int) -> str:
+    return load_library().vf_status_string(status).decode()
+
+
+def vf_last_error() -> str:
+    return load_library().vf_last_error().decode()
+
+
+def vf_version() -> int:
+    return int(load_library().vf_version())
+
+
+# --------------------------------------------------------------- conveniences
+def filter(img: torch.Tensor, window: int = 3, criterion="angular", variant="minimax", algo="auto",
+           want_index: bool = False, want_agg: bool = False, stream=None):
+    """Filter a CUDA uint8 image [H, W, 3] or batch [B, H, W, 3].
+    Returns (out, index | None, aggregates | None)."""
+    shape = img.shape[:-1]
+    n = window * window
+    idx = torch.empty(shape, dtype=torch.uint8, device=img.device) if want_index else None
+    agg = torch.empty(tuple(shape) + (n,), dtype=torch.float32, device=img.device) if want_agg else None
+    out = vf_filter_batch_algo(img, window, criterion, variant, algo, None, idx, agg, stream)
+    return out, idx, agg
+
+
+def fidelity(a: torch.Tensor, b: torch.Tensor) -> dict:
+    """PSNR / NCD / MAE / MSE / fraction of differing pixels of b against a
+    (the paper's quality measures), per batch, from vf_image_stats."""
+    import math
+    s = vf_image_stats(a, b).double().sum(0).cpu().tolist()
+    x = a.unsqueeze(0) if a.dim() == 3 else a
+    npix = x.shape[0] * x.shape[1] * x.shape[2]
+    mse = s[2] / (3 * npix)
+    return dict(diff_frac=s[0] / npix, mae=s[1] / (3 * npix), mse=mse,
+                psnr_db=(math.inf if mse == 0 else 10 * math.log10(255.0 ** 2 / mse)),
+                ncd=(s[3] / s[4] if s[4] > 0 else float("nan")), max_abs=s[5])

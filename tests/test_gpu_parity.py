@@ -1,0 +1,262 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs, with the acceptance rule of tests/parity.py (aggregates
+within 1e-5 relative, selected index exact unless the oracle's candidates are
+within 1e-5 relative, output = the window sample at the selected index)."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle
+import vfsynth
+from tests.parity import check_parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1009_0959_b200 as vfb  # noqa: E402
+
+CV = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp", "minimax"),
+      ("exp", "poly4"), ("log", "exact"), ("log", "minimax")]
+
+
+def gpu_full(img_np, w, crit, var, algo="auto"):
+    x = torch.from_numpy(np.ascontiguousarray(img_np)).cuda()
+    out, idx, agg = vfb.filter(x, w, crit, var, algo=algo, want_index=True, want_agg=True)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), idx.cpu().numpy(), agg.cpu().numpy()
+
+
+def full_parity(img_np, w, crit, var, algo="auto"):
+    g_out, g_idx, g_agg = gpu_full(img_np, w, crit, var, algo)
+    _, o_idx, o_agg = oracle.filter_image(img_np, w, crit, var, want_agg=True)
+    rep = check_parity(img_np, w, g_out, g_idx, g_agg, o_idx, o_agg)
+    assert rep["ok"], rep
+    return rep
+
+
+# ------------------------------------------------------------- config images
+@pytest.mark.parametrize("var", ["exact", "minimax"])
+def test_c1_angular(var):
+    _, x = vfsynth.make_image(vfsynth.config("C1"), 0)
+    full_parity(x, 3, "angular", var)
+
+
+@pytest.mark.parametrize("crit,var", CV)
+def test_c2_all_criteria(crit, var):
+    _, x = vfsynth.make_image(vfsynth.config("C2"), 0)
+    full_parity(x, 3, crit, var)
+
+
+@pytest.mark.parametrize("crit,var", CV)
+def test_5x5_midsize(crit, var):
+    spec = dataclasses.replace(vfsynth.config("C3"), H=203, W=301)   # several tiles + ragged tail
+    _, x = vfsynth.make_image(spec, 0)
+    full_parity(x, 5, crit, var)
+
+
+# ------------------------------------------------------------- edge cases
+RAGGED = [(3, 3), (5, 5), (3, 37), (37, 3), (9, 200), (41, 33), (8, 32), (17, 65)]
+
+
+@pytest.mark.parametrize("crit,var", CV)
+@pytest.mark.parametrize("w", [3, 5])
+def test_ragged_sizes(crit, var, w):
+    for H, W in RAGGED:
+        if w > min(H, W):
+            continue
+        x = vfsynth.random_image(11 + H, H, W)
+        full_parity(x, w, crit, var)
+
+
+@pytest.mark.parametrize("crit,var", CV)
+@pytest.mark.parametrize("w", [3, 5])
+def test_palette_ties_zero_vectors_branch_points(crit, var, w):
+    """Few channel levels: duplicate samples (exact ties), parallel vectors,
+    black pixels (zero-vector rule S:342) and cos = 0.5 pairs."""
+    x = vfsynth.small_palette_image(5, 67, 71)
+    full_parity(x, w, crit, var)
+    x2 = vfsynth.small_palette_image(6, 40, 50, levels=(0, 0, 0, 60, 120))   # many black pixels
+    full_parity(x2, w, crit, var)
+
+
+@pytest.mark.parametrize("crit,var", CV)
+def test_constant_and_black_images(crit, var):
+    for val in [(0, 0, 0), (255, 255, 255), (12, 200, 7)]:
+        x = np.empty((19, 45, 3), np.uint8)
+        x[...] = val
+        for w in (3, 5):
+            g_out, g_idx, g_agg = gpu_full(x, w, crit, var)
+            assert np.array_equal(g_out, x)
+            assert np.all(g_idx == 0)
+            full_parity(x, w, crit, var)
+
+
+@pytest.mark.parametrize("crit,var", CV)
+def test_branch_point_image(crit, var):
+    """Every pixel is one of (v,v,0), (0,v,v), (v,0,v): all cross pairs sit
+    exactly on cos = 0.5, where the two Table 1 rows differ by 3.1e-5."""
+    rng = np.random.default_rng(3)
+    v = rng.integers(1, 256, size=(30, 40))
+    k = rng.integers(0, 3, size=(30, 40))
+    x = np.zeros((30, 40, 3), np.uint8)
+    for c in range(3):
+        x[..., c] = np.where((k == c) | (k == (c + 1) % 3), v, 0)
+    full_parity(x, 3, crit, var)
+    full_parity(x, 5, crit, var)
+
+
+# ------------------------------------------------------------- batch / rows / host API
+@pytest.mark.parametrize("crit,var", [("angular", "minimax"), ("exp", "minimax"), ("log", "exact")])
+def test_batch_matches_per_image(crit, var):
+    spec = dataclasses.replace(vfsynth.config("C4"), H=64, W=96, batch=3)
+    xb = vfsynth.make_batch(spec)
+    xt = torch.from_numpy(xb).cuda()
+    out, idx, agg = vfb.filter(xt, 3, crit, var, want_index=True, want_agg=True)
+    torch.cuda.synchronize()
+    for b in range(3):
+        _, o_idx, o_agg = oracle.filter_image(xb[b], 3, crit, var, want_agg=True)
+        rep = check_parity(xb[b], 3, out[b].cpu().numpy(), idx[b].cpu().numpy(), agg[b].cpu().numpy(),
+                           o_idx, o_agg)
+        assert rep["ok"], (b, rep)
+
+
+@pytest.mark.parametrize("w", [3, 5])
+@pytest.mark.parametrize("crit,var", [("angular", "minimax"), ("angular", "exact"), ("log", "minimax")])
+def test_row_stripes_equal_full_image(w, crit, var):
+    """Stripes with w//2 halo rows, clamped at the global border, reproduce the
+    full-image result bit-exactly (the per-pixel computation does not depend
+    on the partition)."""
+    x = vfsynth.random_image(21, 53, 70)
+    H, W = x.shape[:2]
+    full, fidx, fagg = gpu_full(x, w, crit, var)
+    r = w // 2
+    for k in (1, 2, 3, 4, 7):
+        bounds = np.linspace(0, H, k + 1).astype(int)
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            lo, hi = max(0, a - r), min(H, b + r)
+            band = torch.from_numpy(np.ascontiguousarray(x[lo:hi])).cuda()
+            idx = torch.empty((b - a, W), dtype=torch.uint8, device="cuda")
+            agg = torch.empty((b - a, W, w * w), dtype=torch.float32, device="cuda")
+            out = vfb.vf_filter_rows(band, lo, H, a, b - a, w, crit, var, index=idx, aggregates=agg)
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().numpy(), full[a:b])
+            assert np.array_equal(idx.cpu().numpy(), fidx[a:b])
+            assert np.array_equal(agg.cpu().numpy(), fagg[a:b])
+
+
+def test_rows_invalid_band_rejected():
+    x = torch.zeros((20, 30, 3), dtype=torch.uint8, device="cuda")
+    with pytest.raises(vfb.VFError) as e:
+        vfb.vf_filter_rows(x[2:10].contiguous(), 2, 40, 5, 5, 5, "angular", "minimax")   # needs rows 3..11
+    assert e.value.status == -1
+
+
+def test_host_api_matches_device_api():
+    _, x = vfsynth.make_image(vfsynth.config("C2"), 0)
+    h = torch.from_numpy(x).pin_memory()
+    ho = torch.empty_like(h).pin_memory()
+    ws = torch.empty(vfb.vf_host_workspace_bytes(1, 512, 512), dtype=torch.uint8, device="cuda")
+    for crit, var in CV:
+        vfb.vf_filter_host(h, 3, crit, var, ho, ws)
+        torch.cuda.synchronize()
+        d, _, _ = gpu_full(x, 3, crit, var)
+        assert np.array_equal(ho.numpy(), d), (crit, var)
+
+
+def test_invalid_arguments_return_status():
+    x = torch.zeros((16, 16, 3), dtype=torch.uint8, device="cuda")
+    for w, c, v, st in [(4, "angular", "exact", -1), (7, "angular", "exact", -2), (3, "angular", "poly4", -1),
+                        (3, 5, 0, -1), (3, 0, 9, -1), (17, "exp", "exact", -1)]:
+        with pytest.raises(vfb.VFError) as e:
+            vfb.filter(x, w, c, v)
+        assert e.value.status == st, (w, c, v)
+    with pytest.raises(vfb.VFError):
+        vfb.vf_filter_batch_algo(x, 3, "angular", "exact", out=x)    # aliasing
+
+
+# ------------------------------------------------------------- stats kernel
+def test_image_stats_against_numpy_metrics():
+    from oracle import metrics
+    rng = np.random.default_rng(0)
+    a = rng.integers(0, 256, size=(2, 33, 47, 3)).astype(np.uint8)
+    b = a.copy()
+    m = rng.random(a.shape) < 0.1
+    b[m] = rng.integers(0, 256, size=m.sum())
+    s = vfb.vf_image_stats(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+    for i in range(2):
+        npix = 33 * 47
+        assert s[i, 0] == (a[i] != b[i]).any(-1).sum()
+        assert s[i, 1] / (3 * npix) == pytest.approx(metrics.mae(a[i], b[i]), rel=1e-12)
+        assert s[i, 2] / (3 * npix) == pytest.approx(metrics.mse(a[i], b[i]), rel=1e-12)
+        assert s[i, 3] / s[i, 4] == pytest.approx(metrics.ncd(a[i], b[i]), rel=1e-9)
+        assert s[i, 5] == np.abs(a[i].astype(int) - b[i]).max()
+
+
+# ------------------------------------------------------------- full-size configs (sampled)
+def _sample_pixels(H, W, n, seed):
+    rng = np.random.default_rng(seed)
+    ys = rng.integers(0, H, size=n)
+    xs = rng.integers(0, W, size=n)
+    # all four borders too
+    by = np.concatenate([np.zeros(W, int), np.full(W, H - 1), np.arange(H), np.arange(H)])
+    bx = np.concatenate([np.arange(W), np.arange(W), np.zeros(H, int), np.full(H, W - 1)])
+    sel = np.random.default_rng(seed + 1).permutation(by.shape[0])[:4000]
+    return np.concatenate([ys, by[sel]]), np.concatenate([xs, bx[sel]])
+
+
+def sampled_parity(img_np, w, crit, var, g_out, g_idx, g_agg, nsample=20000, seed=0):
+    H, W = img_np.shape[:2]
+    ys, xs = _sample_pixels(H, W, nsample, seed)
+    _, o_idx, o_agg = oracle.filter_pixels(img_np, w, crit, var, ys, xs)
+    rep = check_parity(img_np, w, g_out[ys, xs], g_idx[ys, xs], g_agg[ys, xs], o_idx, o_agg, ys=ys, xs=xs)
+    assert rep["ok"], rep
+    return rep
+
+
+@pytest.mark.parametrize("crit,var", CV)
+def test_c3_full_size_sampled(crit, var):
+    """C3: 8 x 2048 x 2048, 5x5, the bench's launch configuration (whole batch
+    in one call); sampled pixels of images 0 and 7 against the oracle."""
+    spec = vfsynth.config("C3")
+    xb = vfsynth.make_batch(spec, ids=range(8))
+    xt = torch.from_numpy(xb).cuda()
+    out, idx, agg = vfb.filter(xt, 5, crit, var, want_index=True, want_agg=True)
+    torch.cuda.synchronize()
+    for b in (0, 7):
+        sampled_parity(xb[b], 5, crit, var, out[b].cpu().numpy(), idx[b].cpu().numpy(), agg[b].cpu().numpy(),
+                       nsample=4000, seed=b)
+
+
+@pytest.mark.parametrize("w", [3, 5])
+def test_c5_full_size_sampled(w):
+    """C5: one 4320 x 7680 image, minimax angular."""
+    _, x = vfsynth.make_image(vfsynth.config("C5"), 0)
+    xt = torch.from_numpy(x).cuda()
+    out, idx, agg = vfb.filter(xt, w, "angular", "minimax", want_index=True, want_agg=True)
+    torch.cuda.synchronize()
+    sampled_parity(x, w, "angular", "minimax", out.cpu().numpy(), idx.cpu().numpy(), agg.cpu().numpy(),
+                   nsample=20000 if w == 3 else 5000)
+
+
+@pytest.mark.parametrize("crit,var", CV)
+def test_c4_full_batch_sampled(crit, var):
+    """C4: 1024 x 512 x 768 in one batched call; sampled pixels of 3 images."""
+    spec = vfsynth.config("C4")
+    ids = [0, 511, 1023]
+    xb = vfsynth.make_batch(spec, ids=ids)
+    full = torch.empty((1024, 512, 768, 3), dtype=torch.uint8, device="cuda")
+    full.random_(0, 256, generator=torch.Generator(device="cuda").manual_seed(1))
+    for j, b in enumerate(ids):
+        full[b] = torch.from_numpy(xb[j]).cuda()
+    out, idx, _ = vfb.filter(full, 3, crit, var, want_index=True)
+    torch.cuda.synchronize()
+    for j, b in enumerate(ids):
+        sub = full[b:b + 1]
+        o2, i2, a2 = vfb.filter(sub.contiguous(), 3, crit, var, want_index=True, want_agg=True)
+        assert torch.equal(o2[0], out[b]) and torch.equal(i2[0], idx[b])
+        sampled_parity(xb[j], 3, crit, var, o2[0].cpu().numpy(), i2[0].cpu().numpy(), a2[0].cpu().numpy(),
+                       nsample=5000, seed=b)
