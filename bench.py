@@ -77,7 +77,9 @@ def make_input(spec, rank):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi sampler (B200_PROFILING.md clocks line), started before the
+    warm-up; samples are time-stamped on arrival so the ones taken inside the
+    timed region can be selected."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -87,22 +89,25 @@ class ClockSampler:
         self.proc = None
         self.lines = []
 
-    def __enter__(self):
+    def start(self, wait_s: float = 5.0):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < wait_s:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
-    def __exit__(self, *a):
+    def stop(self):
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -110,25 +115,36 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
-        sm, mx, reasons = [], None, set()
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-            for nm, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
+    def summary(self, t0: float, t1: float):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+        def parse(sel):
+            sm, mx, reasons, pw = [], None, set(), []
+            for _, ln in sel:
+                f = [x.strip() for x in ln.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx = float(f[2])
+                    pw.append(float(f[3]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, f[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            return sm, mx, reasons, pw
+
+        timed = [l for l in self.lines if t0 - 0.06 <= l[0] <= t1 + 0.06]
+        window = "timed"
+        sm, mx, reasons, pw = parse(timed)
+        if len(sm) < 3:     # timed region shorter than a few sampling periods
+            window = "timed+warmup (timed region %.3f s)" % (t1 - t0)
+            sm, mx, reasons, pw = parse([l for l in self.lines if l[0] <= t1 + 0.06][-40:])
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "window": window}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": window, "power_w_max": max(pw) if pw else None}
 
 
 # ------------------------------------------------------------------ helpers
@@ -247,8 +263,15 @@ def main():
         if events is not None:
             events[len(COMBOS)].record(stream)
 
-    for _ in range(max(args.warmup, 3)):
+    clk = ClockSampler(dev.index).start()
+    # warm-up: at least W (>= 3) steps and at least 1 s of load, so clocks settle
+    tw = time.perf_counter()
+    nw = 0
+    while nw < max(args.warmup, 3) or time.perf_counter() - tw < 1.0:
         step()
+        nw += 1
+        if nw % 50 == 0:
+            torch.cuda.synchronize(dev)
     torch.cuda.synchronize(dev)
 
     # ---- timed region: K steps, per-step CUDA events, L2 flush between steps
@@ -256,13 +279,14 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(dev.index if world == 1 else local) as clk:
-        t_wall0 = time.perf_counter()
-        for k in range(args.steps):
-            flush.fill_(k & 0xFF)            # outside the event windows
-            step(ev[k])
-        torch.cuda.synchronize(dev)
-        t_wall = time.perf_counter() - t_wall0
+    t_wall0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)            # outside the event windows
+        step(ev[k])
+    torch.cuda.synchronize(dev)
+    t_wall1 = time.perf_counter()
+    t_wall = t_wall1 - t_wall0
+    clk.stop()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -278,7 +302,7 @@ def main():
     value = units / (ms_per_step / 1e3) / 1e6        # Mpix/s
 
     # ---- per-kernel breakdown + roofline of the dominant kernel
-    clocks = clk.summary()
+    clocks = clk.summary(t_wall0, t_wall1)
     n = w * w
     pairs = n * (n - 1) // 2
     kern = {}

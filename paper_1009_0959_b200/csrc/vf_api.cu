@@ -39,24 +39,24 @@ typedef void (*KernelFn)(const Launch);
 template <int WIN>
 KernelFn window_kernel(int crit, int var) {
   using namespace vf;
-  if (crit == ANGULAR) return var == EXACT ? vf_window_kernel<WIN, ANGULAR, EXACT> : vf_window_kernel<WIN, ANGULAR, MINIMAX>;
+  if (crit == ANGULAR) return var == EXACT ? vf_angular_window_kernel<WIN, EXACT> : vf_angular_window_kernel<WIN, MINIMAX>;
   if (crit == EXPC) {
-    if (var == EXACT) return vf_window_kernel<WIN, EXPC, EXACT>;
-    if (var == MINIMAX) return vf_window_kernel<WIN, EXPC, MINIMAX>;
-    return vf_window_kernel<WIN, EXPC, POLY4>;
+    if (var == EXACT) return vf_el_kernel<WIN, EXPC, EXACT>;
+    if (var == MINIMAX) return vf_el_kernel<WIN, EXPC, MINIMAX>;
+    return vf_el_kernel<WIN, EXPC, POLY4>;
   }
-  return var == EXACT ? vf_window_kernel<WIN, LOGC, EXACT> : vf_window_kernel<WIN, LOGC, MINIMAX>;
+  return var == EXACT ? vf_el_kernel<WIN, LOGC, EXACT> : vf_el_kernel<WIN, LOGC, MINIMAX>;
 }
 
 int validate(int B, int H, int W, int window, int crit, int var) {
   if (window < 3 || window % 2 == 0) return fail(VF_EINVAL, "window must be odd and >= 3%s (got %lld)", "", window);
-  if (window > 5) return fail(VF_EUNSUPPORTED, "window %s%lld is valid but not compiled (3 and 5 are)", "", window);
   if (B < 1) return fail(VF_EINVAL, "batch must be >= 1%s (got %lld)", "", B);
   if (H < 1 || W < 1) return fail(VF_EINVAL, "image size must be positive%s", "");
   if (window > H || window > W) return fail(VF_EINVAL, "window larger than the image (S:64)%s", "");
   if (crit < 0 || crit > 2) return fail(VF_EINVAL, "criterion out of range%s (%lld)", "", crit);
   if (var < 0 || var > 2) return fail(VF_EINVAL, "variant out of range%s (%lld)", "", var);
   if (var == VF_MINIMAX_POLY4 && crit != VF_EXP) return fail(VF_EINVAL, "VF_MINIMAX_POLY4 is only defined for VF_EXP%s", "");
+  if (window > 5) return fail(VF_EUNSUPPORTED, "window %s%lld is valid but not compiled (3 and 5 are)", "", window);
   return VF_OK;
 }
 

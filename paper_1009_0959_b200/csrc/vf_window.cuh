@@ -1,14 +1,14 @@
-// vf_window.cuh -- the per-window kernel: one thread = one output pixel, all
+// vf_window.cuh -- per-window kernels: one thread = one output pixel, all
 // n(n-1)/2 pairs of its window evaluated in registers (SURVEY.md 8(a) rows
 // a1-a8 fused in one launch).
 //
-//   a1  stage the block's tile + halo (uint8 HWC -> fp32 in smem) with
-//       replicate clamping against the GLOBAL image rows (stripes), Fig. 1 /
-//       S:78;
-//   a2  per-pixel precompute once per staged pixel: (r, g, b, |x|^2) and, for
-//       the angular criterion, (|x|, 1/|x|);
-//   a3  exp/log: window statistic S1 = sum_{i<j} |x_i - x_j|_1 and the scale
-//       c_E = n^(1+kappa/3) / (2 S1) (= 1/h_W, Eq. 8) or c_L = (1-1/e)(n-1)/S1;
+//   a1  stage the block's tile + halo (uint8 HWC -> smem) with replicate
+//       clamping against the GLOBAL image rows (stripes), Fig. 1 / S:78;
+//   a2  per-pixel precompute once per staged pixel: packed RGB0 (exp/log), or
+//       (r, g, b, |x|^2) and (|x|, 1/|x|) (angular);
+//   a3  exp/log: window statistic S1 = sum_{i<j} |x_i - x_j|_1 (integer, one
+//       VABSDIFF4 per pair) and the scale c_E = n^(1+kappa/3) / (2 S1)
+//       (= 1/h_W, Eq. 8) or c_L = (1-1/e)(n-1)/S1;
 //   a4  pair geometry; a5 criterion (libm or minimax Horner, Tables 1-4);
 //   a6  symmetric accumulation R_i += D, R_j += D (each pair computed once);
 //   a7  argmin, strict '<' in increasing k (lowest index on ties);
@@ -35,128 +35,29 @@ struct Launch {
   float kscale;        // exp: n^(1+kappa/3)/2 ; log: (1-1/e)(n-1)
 };
 
-template <int WIN, int CRIT, int VAR>
-__global__ void __launch_bounds__(TX * TY) vf_window_kernel(const Launch L) {
-  constexpr int R = WIN / 2;
-  constexpr int N = WIN * WIN;
-  constexpr int SW = TX + 2 * R;
-  constexpr int SH = TY + 2 * R;
-  __shared__ float4 s_px[SH * SW];                        // r, g, b, |x|^2
-  __shared__ float2 s_nm[CRIT == ANGULAR ? SH * SW : 1];  // |x|, 1/|x|
+// Pointer to the input pixel of global (clamped) coordinates (gy, gx).
+__device__ __forceinline__ const uint8_t* pixel_ptr(const Launch& L, const uint8_t* in, int gy, int gx) {
+  gy = clampi(gy, 0, L.H - 1) - L.band_row0;
+  gx = clampi(gx, 0, L.W - 1);
+  return in + ((long long)gy * L.W + gx) * 3;
+}
 
-  const int b = blockIdx.z;
-  const int x0 = blockIdx.x * TX;
-  const int y0 = L.out_row0 + blockIdx.y * TY;           // global row of tile row 0
-  const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
-
-  // ---- a1 + a2: stage tile + halo ------------------------------------------
-  const int tid = threadIdx.y * TX + threadIdx.x;
-  for (int p = tid; p < SH * SW; p += TX * TY) {
-    const int sy = p / SW, sx = p - sy * SW;
-    const int gy = clampi(y0 + sy - R, 0, L.H - 1) - L.band_row0;
-    const int gx = clampi(x0 + sx - R, 0, L.W - 1);
-    const uint8_t* q = in + ((long long)gy * L.W + gx) * 3;
-    const float r = q[0], g = q[1], bl = q[2];
-    const float nn = fmaf(r, r, fmaf(g, g, bl * bl));    // exact integer < 2^18
-    s_px[p] = make_float4(r, g, bl, nn);
-    if (CRIT == ANGULAR) {
-      const float nrm = sqrtf(nn);
-      s_nm[p] = make_float2(nrm, nn > 0.0f ? 1.0f / nrm : 0.0f);
-    }
-  }
-  __syncthreads();
-
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int ox = x0 + tx, oy = y0 + ty;
-  if (ox >= L.W || oy >= L.out_row0 + L.out_rows) return;
-
-  float xr[N], xg[N], xb[N], xn[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    const float4 v = s_px[(ty + k / WIN) * SW + tx + k % WIN];
-    xr[k] = v.x; xg[k] = v.y; xb[k] = v.z; xn[k] = CRIT == ANGULAR ? v.w : 0.0f;
-  }
-  float Ra[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) Ra[k] = 0.0f;
-
-  if (CRIT == ANGULAR) {
-    float xm[N], xi[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      const float2 v = s_nm[(ty + k / WIN) * SW + tx + k % WIN];
-      xm[k] = v.x; xi[k] = v.y;
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-#pragma unroll
-      for (int j = i + 1; j < N; ++j) {
-        const float d = angular_pair<VAR>(xr[i], xg[i], xb[i], xn[i], xm[i], xi[i],
-                                          xr[j], xg[j], xb[j], xn[j], xm[j], xi[j]);
-        Ra[i] += d;
-        Ra[j] += d;
-      }
-    }
-    if (VAR != EXACT) {
-      // zero-vector fix-up: every pair touching a zero vector
-      // contributed the ARCSIN row's a0 instead of 0.
-      int zc = 0;
-#pragma unroll
-      for (int k = 0; k < N; ++k) zc += (xn[k] == 0.0f);
-      if (zc) {
-        const float corr = (float)zc * coef::ASIN().a0;
-#pragma unroll
-        for (int k = 0; k < N; ++k) Ra[k] = (xn[k] == 0.0f) ? 0.0f : Ra[k] - corr;
-      }
-    }
-  } else {
-    // ---- a3: window statistic S1 ------------------------------------------
-    constexpr bool KEEP = (N <= 9);
-    float d1k[KEEP ? N * (N - 1) / 2 : 1];
-    float S1 = 0.0f;
-#pragma unroll
-    for (int i = 0, p = 0; i < N; ++i) {
-#pragma unroll
-      for (int j = i + 1; j < N; ++j, ++p) {
-        // (written as max - min so that, for 5x5, the compiler does not keep
-        // all 300 distances live until pass 2: recomputing is cheaper than spilling)
-        const float d = KEEP ? l1(xr[i], xg[i], xb[i], xr[j], xg[j], xb[j])
-                             : l1_maxmin(xr[i], xg[i], xb[i], xr[j], xg[j], xb[j]);
-        if (KEEP) d1k[p] = d;
-        S1 += d;                                          // exact: S1 < 2^18
-      }
-    }
-    if (S1 > 0.0f) {                                      // flat window: all D = 0
-      const float sc = L.kscale / S1;                     // c_E or c_L
-#pragma unroll
-      for (int i = 0, p = 0; i < N; ++i) {
-#pragma unroll
-        for (int j = i + 1; j < N; ++j, ++p) {
-          const float d = KEEP ? d1k[p] : l1(xr[i], xg[i], xb[i], xr[j], xg[j], xb[j]);
-          const float v = CRIT == EXPC ? exp_crit<VAR>(sc * d) : log_crit<VAR>(sc * d);
-          Ra[i] += v;
-          Ra[j] += v;
-        }
-      }
-    }
-  }
-
-  // ---- a7: argmin, lowest index on ties ---------------------------------------
+// a7 + a8: argmin (lowest index on ties) and store.
+template <int N>
+__device__ __forceinline__ void argmin_store(const Launch& L, int b, int ox, int oy, const float (&Ra)[N],
+                                             const uint32_t (&pk)[N]) {
   int best = 0;
   float bv = Ra[0];
 #pragma unroll
   for (int k = 1; k < N; ++k) {
     if (Ra[k] < bv) { bv = Ra[k]; best = k; }
   }
-  // ---- a8: store -----------------------------------------------------------------
-  float orr = xr[0], og = xg[0], ob = xb[0];
+  uint32_t o = pk[0];
 #pragma unroll
-  for (int k = 1; k < N; ++k) {
-    if (best == k) { orr = xr[k]; og = xg[k]; ob = xb[k]; }
-  }
+  for (int k = 1; k < N; ++k) o = (best == k) ? pk[k] : o;
   const long long po = (long long)(oy - L.out_row0) * L.W + ox;
-  uint8_t* o = L.out + (long long)b * L.out_stride + po * 3;
-  o[0] = (uint8_t)orr; o[1] = (uint8_t)og; o[2] = (uint8_t)ob;
+  uint8_t* op = L.out + (long long)b * L.out_stride + po * 3;
+  op[0] = (uint8_t)(o & 0xff); op[1] = (uint8_t)((o >> 8) & 0xff); op[2] = (uint8_t)((o >> 16) & 0xff);
   const long long npix_img = (long long)L.out_rows * L.W;
   if (L.idx) L.idx[b * npix_img + po] = (uint8_t)best;
   if (L.agg) {
@@ -164,6 +65,146 @@ __global__ void __launch_bounds__(TX * TY) vf_window_kernel(const Launch L) {
 #pragma unroll
     for (int k = 0; k < N; ++k) a[k] = Ra[k];
   }
+}
+
+// ============================================================================
+// exp / log criteria (readings R2, R3): everything derives from the integer L1
+// distances, so a sample is one packed RGB0 word and the L1 distance of a pair
+// is one VABSDIFF4.  Pass 1 forms S1 exactly in integers; pass 2 recomputes
+// each distance already biased into a float (2^23 + d1) and turns it into the
+// scaled argument with one FFMA.
+// ============================================================================
+template <int WIN, int CRIT, int VAR>
+__global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
+  constexpr int R = WIN / 2;
+  constexpr int N = WIN * WIN;
+  constexpr int SW = TX + 2 * R;
+  constexpr int SH = TY + 2 * R;
+  __shared__ uint32_t s_pk[SH * SW];
+
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * TX;
+  const int y0 = L.out_row0 + blockIdx.y * TY;
+  const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  for (int p = tid; p < SH * SW; p += TX * TY) {          // a1 + a2
+    const int sy = p / SW, sx = p - sy * SW;
+    const uint8_t* q = pixel_ptr(L, in, y0 + sy - R, x0 + sx - R);
+    s_pk[p] = pack_rgb(q[0], q[1], q[2]);
+  }
+  __syncthreads();
+
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int ox = x0 + tx, oy = y0 + ty;
+  if (ox >= L.W || oy >= L.out_row0 + L.out_rows) return;
+
+  uint32_t pk[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) pk[k] = s_pk[(ty + k / WIN) * SW + tx + k % WIN];
+
+  // a3: S1 = sum_{i<j} d1_ij, exact, in 4 independent integer chains
+  uint32_t acc[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int i = 0, p = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = i + 1; j < N; ++j, ++p) acc[p & 3] = sad4(pk[i], pk[j], acc[p & 3]);
+  }
+  const uint32_t S1 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+
+  float Ra[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) Ra[k] = 0.0f;
+  if (S1 != 0u) {                                          // flat window: all D = 0 (R18)
+    const float sc = L.kscale / (float)S1;                 // c_E = 1/h_W, or c_L
+    const float bias = -sc * F2P23;                        // exact
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = i + 1; j < N; ++j) {
+        const float fb = __uint_as_float(sad4(pk[i], pk[j], F2P23_BITS));   // 2^23 + d1
+        const float zu = fmaf(sc, fb, bias);                                 // c * d1
+        const float v = CRIT == EXPC ? exp_crit<VAR>(zu) : log_crit<VAR>(zu);
+        Ra[i] += v;
+        Ra[j] += v;
+      }
+    }
+  }
+  argmin_store<N>(L, b, ox, oy, Ra, pk);
+}
+
+// ============================================================================
+// angular criterion, per-window (VF_ALGO_WINDOW).  See vf_shared.cuh for the
+// cross-window pair-sharing kernel used by default.
+// ============================================================================
+template <int WIN, int VAR>
+__global__ void __launch_bounds__(TX * TY) vf_angular_window_kernel(const Launch L) {
+  constexpr int R = WIN / 2;
+  constexpr int N = WIN * WIN;
+  constexpr int SW = TX + 2 * R;
+  constexpr int SH = TY + 2 * R;
+  __shared__ float4 s_px[SH * SW];                        // r, g, b, |x|^2
+  __shared__ float2 s_nm[SH * SW];                        // |x|, 1/|x|
+  __shared__ uint32_t s_pk[SH * SW];                      // packed RGB0 (output)
+
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * TX;
+  const int y0 = L.out_row0 + blockIdx.y * TY;
+  const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  for (int p = tid; p < SH * SW; p += TX * TY) {
+    const int sy = p / SW, sx = p - sy * SW;
+    const uint8_t* q = pixel_ptr(L, in, y0 + sy - R, x0 + sx - R);
+    const float r = q[0], g = q[1], bl = q[2];
+    const float nn = fmaf(r, r, fmaf(g, g, bl * bl));    // exact integer < 2^18
+    s_px[p] = make_float4(r, g, bl, nn);
+    const float nrm = sqrtf(nn);
+    s_nm[p] = make_float2(nrm, nn > 0.0f ? 1.0f / nrm : 0.0f);
+    s_pk[p] = pack_rgb(q[0], q[1], q[2]);
+  }
+  __syncthreads();
+
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int ox = x0 + tx, oy = y0 + ty;
+  if (ox >= L.W || oy >= L.out_row0 + L.out_rows) return;
+
+  float xr[N], xg[N], xb[N], xn[N], xm[N], xi[N];
+  uint32_t pk[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const int a = (ty + k / WIN) * SW + tx + k % WIN;
+    const float4 v = s_px[a];
+    xr[k] = v.x; xg[k] = v.y; xb[k] = v.z; xn[k] = v.w;
+    const float2 u = s_nm[a];
+    xm[k] = u.x; xi[k] = u.y;
+  }
+  float Ra[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) Ra[k] = 0.0f;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = i + 1; j < N; ++j) {
+      const float d = angular_pair<VAR>(xr[i], xg[i], xb[i], xn[i], xm[i], xi[i],
+                                        xr[j], xg[j], xb[j], xn[j], xm[j], xi[j]);
+      Ra[i] += d;
+      Ra[j] += d;
+    }
+  }
+  if (VAR != EXACT) {
+    // zero-vector fix-up: every pair touching a zero vector
+    // contributed the ARCSIN row's a0 instead of 0.
+    int zc = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) zc += (xn[k] == 0.0f);
+    if (zc) {
+      const float corr = (float)zc * coef::ASIN().a0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) Ra[k] = (xn[k] == 0.0f) ? 0.0f : Ra[k] - corr;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) pk[k] = s_pk[(ty + k / WIN) * SW + tx + k % WIN];
+  argmin_store<N>(L, b, ox, oy, Ra, pk);
 }
 
 }  // namespace vf
