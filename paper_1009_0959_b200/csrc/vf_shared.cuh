@@ -1,13 +1,246 @@
-// vf_shared.cuh -- cross-window pair sharing for the angular criterion
-// (SURVEY.md 8(f1)).  Placeholder: not yet applicable (returns -100 so the
-// per-window kernel runs).
+// vf_shared.cuh -- angular criterion with cross-window pair sharing
+// (SURVEY.md 8(f1)).
+//
+// The angular distance A(x_p, x_q) of Eq. 5 depends only on the two pixels,
+// not on the window, so each image pair within Chebyshev distance 2r = w - 1
+// is evaluated ONCE per block and read by every window that contains it:
+// 12 (3x3) or 40 (5x5) evaluations per pixel instead of 36 or 300.  The
+// aggregates R_i = sum_{j != i} A(x_i, x_j) are then formed per window from the
+// stored pair values, exactly as in Eq. 5, so results agree with the
+// per-window kernel and the oracle within the parity tolerance.
+//
+// Block = 256 threads over a 32 x PH region P of input pixels (PH = 24, i.e.
+// 3 pixels per thread); the output tile is the interior (32-2r) x (PH-2r).
+//   stage   P (uint8 HWC, replicate-clamped) -> smem: packed RGB0, |x|^2, |x|
+//   phase A for every pair offset delta in the half plane (dy > 0, or dy = 0
+//           and dx > 0), |dy|,|dx| <= 2r, and every p in P:
+//           M[delta][p] = A(x_p, x_{p+delta}) (minimax: Table 1 ARCSIN row in
+//           tau; exact: Eq. 6 with libm asinf).  Pairs that may have cos < 0.5
+//           or a zero vector (a conservative test, <~1.5% of pairs) are flagged
+//           and re-evaluated exactly afterwards (exact 4D^2 < P predicate,
+//           ARCCOS row / acosf, zero-vector rule S:342).
+//   phase C for each output window and each pair i < j of it:
+//           v = M[o_j - o_i][c + o_i];  R_i += v;  R_j += v
+//   then argmin (lowest index on ties) and store.
+// For 5x5 the 40 offsets are processed in 4 groups of 10 so M fits in 30 KB.
 #pragma once
 #include <cuda_runtime.h>
+
+#include <utility>
 
 #include "vf_window.cuh"
 
 namespace vf {
 
-inline int launch_shared(const Launch&, int, int, int, cudaStream_t) { return -100; }
+namespace shared {
+
+constexpr int PW = 32;              // region width  (= warp width)
+constexpr int PH = 24;              // region height (3 pixels per thread)
+constexpr int NP = PW * PH;         // 768
+constexpr int PAD = 5 * PW;         // reads past the region stay in bounds
+constexpr int NTHR = 256;
+constexpr int PPT = NP / NTHR;      // pixels per thread (3)
+
+__host__ __device__ constexpr int n_delta(int r) { return 4 * r * (2 * r + 1); }
+// offset index d -> (dy, dx): d < 2r: (0, d+1); else dy = 1 + (d-2r)/(4r+1), dx = -2r + (d-2r)%(4r+1)
+__host__ __device__ constexpr int delta_dy(int r, int d) { return d < 2 * r ? 0 : 1 + (d - 2 * r) / (4 * r + 1); }
+__host__ __device__ constexpr int delta_dx(int r, int d) { return d < 2 * r ? d + 1 : -2 * r + (d - 2 * r) % (4 * r + 1); }
+__host__ __device__ constexpr int delta_index(int r, int dy, int dx) {
+  return dy == 0 ? dx - 1 : 2 * r + (dy - 1) * (4 * r + 1) + (dx + 2 * r);
+}
+
+}  // namespace shared
+
+// Exact re-evaluation of a flagged pair (rare path); returns true and the
+// value when it differs from the tau-branch value computed in phase A.
+template <int VAR>
+__device__ __noinline__ bool angular_fixup(uint32_t pa, float nna, float nrma, uint32_t pb, float nnb, float nrmb,
+                                           float* val) {
+  if (nna == 0.0f || nnb == 0.0f) { *val = 0.0f; return true; }
+  const float ra = (float)(pa & 0xff), ga = (float)((pa >> 8) & 0xff), ba = (float)(pa >> 16);
+  const float rb = (float)(pb & 0xff), gb = (float)((pb >> 8) & 0xff), bb = (float)(pb >> 16);
+  const AngGeo g = angular_geo(ra, ga, ba, nna, nrma, rb, gb, bb, nnb, nrmb);
+  if (!g.acos_branch) return false;                                       // phase A value stands
+  const float c = g.D / __fmul_rn(nrma, nrmb);                            // cos < 0.5
+  *val = (VAR == EXACT) ? acosf(c) : horner4(coef::ACOS(), c);
+  return true;
+}
+
+// Per-block shared-memory state of the pair-sharing kernel.
+template <int GD>
+struct SharedSmem {
+  uint32_t pk[shared::NP + shared::PAD];
+  float2 nm[shared::NP + shared::PAD];   // (|x|^2, |x|)
+  float M[GD][shared::NP];
+};
+
+// One group of GD offsets: phase A (pair maps) + rare fix-ups + phase C.
+// G is a template parameter so that every register index stays static.
+template <int WIN, int VAR, int GD, int OPT, int G>
+__device__ __forceinline__ void shared_group(SharedSmem<GD>& sm, const uint32_t (&my_pk)[shared::PPT],
+                                             const float (&my_nn)[shared::PPT], const float (&my_nrm)[shared::PPT],
+                                             const float (&my_nrmk)[shared::PPT], float (&Ra)[OPT][WIN * WIN],
+                                             int tid) {
+  using namespace shared;
+  constexpr int R = WIN / 2;
+  constexpr int N = WIN * WIN;
+  constexpr int TW = PW - 2 * R;
+  constexpr int TH = PH - 2 * R;
+  const int tx = tid & 31, ty = tid >> 5;
+  __syncthreads();   // staging done (G = 0) / previous phase C done with M
+  // ---- phase A: pair maps for offsets [G*GD, G*GD + GD) ------------------------------
+  uint64_t flags = 0;
+#pragma unroll
+  for (int dl = 0; dl < GD; ++dl) {
+    const int d = G * GD + dl;
+    const int off = delta_dy(R, d) * PW + delta_dx(R, d);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const int p = tid + NTHR * k;
+      const int q = p + off;                                  // in bounds (PAD); garbage if outside P
+      const uint32_t qk = sm.pk[q];
+      const float2 qn = sm.nm[q];
+      const float D = __uint_as_float(__dp4a(my_pk[k], qk, F2P23_BITS)) - F2P23;   // exact dot
+      const float Ph = __fmul_rn(my_nn[k], qn.x);
+      const float Pl = fmaf(my_nn[k], qn.x, -Ph);
+      const float X = __fadd_rn(fmaf(-D, D, Ph), Pl);         // |x_p x x_q|^2
+      const float s = __fmul_rn(my_nrm[k], qn.y);
+      const bool rare = !(D > __fmul_rn(my_nrmk[k], qn.y));   // maybe cos < 0.5, or a zero vector
+      const float w = fmaf(s, D, Ph);
+      const float tau = __fmul_rn(X, rsqrt_approx(fmaf(X, w, 1e-30f)));
+      float v;
+      if (VAR == EXACT)
+        v = 2.0f * asinf(tau * 0.70710678118654752f);
+      else
+        v = horner4(coef::ASIN(), tau);
+      sm.M[dl][p] = v;
+      // (offsets reaching below the region read the zero padding: never flag those)
+      const bool valid = (k < PPT - 1) || (q < NP);
+      flags |= (rare && valid) ? (1ull << (dl * PPT + k)) : 0ull;
+    }
+  }
+  // rare pairs: exact branch decision (re-evaluated, then overwritten)
+  while (flags) {
+    const int bit = __ffsll((long long)flags) - 1;
+    flags &= flags - 1;
+    const int dl = bit / PPT, k = bit - dl * PPT;
+    const int d = G * GD + dl;
+    const int p = tid + NTHR * k;
+    const int q = p + delta_dy(R, d) * PW + delta_dx(R, d);
+    const float2 pn = sm.nm[p], qn = sm.nm[q];
+    float v;
+    if (angular_fixup<VAR>(sm.pk[p], pn.x, pn.y, sm.pk[q], qn.x, qn.y, &v)) sm.M[dl][p] = v;
+  }
+  __syncthreads();
+  // ---- phase C: accumulate the window aggregates ------------------------------------
+#pragma unroll
+  for (int k = 0; k < OPT; ++k) {
+    const int oy = ty + 8 * k;
+    if ((TH % 8 == 0 || oy < TH) && tx < TW) {
+      const int base = oy * PW + tx;                          // P index of window sample (0,0)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int j = i + 1; j < N; ++j) {
+          const int d = delta_index(R, j / WIN - i / WIN, j % WIN - i % WIN);
+          if (d / GD == G) {
+            const float v = sm.M[d - G * GD][base + (i / WIN) * PW + (i % WIN)];
+            Ra[k][i] += v;
+            Ra[k][j] += v;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int WIN, int VAR, int GD, int OPT, int... Gs>
+__device__ __forceinline__ void shared_groups(std::integer_sequence<int, Gs...>, SharedSmem<GD>& sm,
+                                              const uint32_t (&my_pk)[shared::PPT], const float (&my_nn)[shared::PPT],
+                                              const float (&my_nrm)[shared::PPT], const float (&my_nrmk)[shared::PPT],
+                                              float (&Ra)[OPT][WIN * WIN], int tid) {
+  (shared_group<WIN, VAR, GD, OPT, Gs>(sm, my_pk, my_nn, my_nrm, my_nrmk, Ra, tid), ...);
+}
+
+template <int WIN, int VAR>
+__global__ void __launch_bounds__(shared::NTHR) vf_angular_shared_kernel(const Launch L) {
+  using namespace shared;
+  constexpr int R = WIN / 2;
+  constexpr int N = WIN * WIN;
+  constexpr int TW = PW - 2 * R;            // output tile width
+  constexpr int TH = PH - 2 * R;            // output tile height
+  constexpr int ND = n_delta(R);            // 12 or 40
+  constexpr int GD = (WIN == 3) ? 12 : 10;  // offsets per group
+  constexpr int NG = ND / GD;
+  constexpr int OPT = (TH + 7) / 8;         // outputs per thread (rows ty, ty+8, ty+16)
+  static_assert(ND % GD == 0, "groups must tile the offsets");
+  __shared__ SharedSmem<GD> sm;
+
+  const int b = blockIdx.z;
+  const int ox0 = blockIdx.x * TW;                        // output tile origin (global)
+  const int oy0 = L.out_row0 + blockIdx.y * TH;
+  const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;
+
+  // ---- stage P ----------------------------------------------------------------
+  uint32_t my_pk[PPT];
+  float my_nn[PPT], my_nrm[PPT], my_nrmk[PPT];
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int p = tid + NTHR * k;
+    const int py = p >> 5, px = p & 31;
+    const uint8_t* q = pixel_ptr(L, in, oy0 - R + py, ox0 - R + px);
+    const uint32_t r = q[0], g = q[1], bl = q[2];
+    const float nn = (float)(r * r + g * g + bl * bl);          // exact
+    const float nrm = sqrtf(nn);
+    my_pk[k] = pack_rgb(r, g, bl);
+    my_nn[k] = nn;
+    my_nrm[k] = nrm;
+    my_nrmk[k] = nrm * 0.50048828125f;                          // 0.5 (1 + 2^-10): conservative cut
+    sm.pk[p] = my_pk[k];
+    sm.nm[p] = make_float2(nn, nrm);
+  }
+  if (tid < PAD) { sm.pk[NP + tid] = 0u; sm.nm[NP + tid] = make_float2(0.0f, 0.0f); }
+
+  float Ra[OPT][N];
+#pragma unroll
+  for (int k = 0; k < OPT; ++k)
+#pragma unroll
+    for (int i = 0; i < N; ++i) Ra[k][i] = 0.0f;
+
+  shared_groups<WIN, VAR, GD, OPT>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, my_nrmk, Ra,
+                                   tid);
+
+  // ---- argmin + store ------------------------------------------------------------------
+#pragma unroll
+  for (int k = 0; k < OPT; ++k) {
+    const int oy = ty + 8 * k;
+    const int gy = oy0 + oy, gx = ox0 + tx;
+    if ((TH % 8 == 0 || oy < TH) && tx < TW && gx < L.W && gy < L.out_row0 + L.out_rows) {
+      uint32_t pk[N];
+      const int base = oy * PW + tx;
+#pragma unroll
+      for (int i = 0; i < N; ++i) pk[i] = sm.pk[base + (i / WIN) * PW + (i % WIN)];
+      argmin_store<N>(L, b, gx, gy, Ra[k], pk);
+    }
+  }
+}
+
+inline int launch_shared(const Launch& L, int B, int window, int var, cudaStream_t st) {
+  using namespace shared;
+  const int R = window / 2;
+  const int TW = PW - 2 * R, TH = PH - 2 * R;
+  dim3 grid((L.W + TW - 1) / TW, (L.out_rows + TH - 1) / TH, B);
+  if (grid.y > 65535 || grid.z > 65535) return (int)cudaErrorInvalidConfiguration;
+  if (window == 3) {
+    if (var == EXACT) vf_angular_shared_kernel<3, EXACT><<<grid, NTHR, 0, st>>>(L);
+    else vf_angular_shared_kernel<3, MINIMAX><<<grid, NTHR, 0, st>>>(L);
+  } else {
+    if (var == EXACT) vf_angular_shared_kernel<5, EXACT><<<grid, NTHR, 0, st>>>(L);
+    else vf_angular_shared_kernel<5, MINIMAX><<<grid, NTHR, 0, st>>>(L);
+  }
+  return (int)cudaGetLastError();
+}
 
 }  // namespace vf

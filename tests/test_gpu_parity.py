@@ -30,11 +30,15 @@ def gpu_full(img_np, w, crit, var, algo="auto"):
     return out.cpu().numpy(), idx.cpu().numpy(), agg.cpu().numpy()
 
 
-def full_parity(img_np, w, crit, var, algo="auto"):
-    g_out, g_idx, g_agg = gpu_full(img_np, w, crit, var, algo)
+def full_parity(img_np, w, crit, var, algo=None):
+    """Both angular kernels (per-window and pair-sharing) are checked unless
+    `algo` is given; exp/log have one kernel."""
+    algos = ([algo] if algo else ["window", "shared"]) if crit == "angular" else ["auto"]
     _, o_idx, o_agg = oracle.filter_image(img_np, w, crit, var, want_agg=True)
-    rep = check_parity(img_np, w, g_out, g_idx, g_agg, o_idx, o_agg)
-    assert rep["ok"], rep
+    for a in algos:
+        g_out, g_idx, g_agg = gpu_full(img_np, w, crit, var, a)
+        rep = check_parity(img_np, w, g_out, g_idx, g_agg, o_idx, o_agg)
+        assert rep["ok"], (a, rep)
     return rep
 
 
