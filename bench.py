@@ -226,12 +226,15 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+KERNEL_NAMES = {"angular": "vf_angular_shared_kernel<{w},{v}>", "exp": "vf_el_kernel<{w},exp,{v}>",
+                "log": "vf_el_kernel<{w},log,{v}>"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -251,17 +254,14 @@ def main():
     B, H, W = x_np.shape[:3]
     npix = B * H * W
     x = torch.from_numpy(x_np).to(dev)
-    outs = {c: torch.empty_like(x) for c in COMBOS}
+    outs = [torch.empty_like(x) for _ in COMBOS]
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    # the step: one plan = one CUDA graph whose 7 filter kernels are independent nodes
+    plan = vfb.Plan(x, outs, w, COMBOS)
 
-    def step(events=None):
-        for i, (crit, var) in enumerate(COMBOS):
-            if events is not None:
-                events[i].record(stream)
-            vfb.vf_filter_batch(x, w, crit, var, out=outs[(crit, var)], stream=stream)
-        if events is not None:
-            events[len(COMBOS)].record(stream)
+    def step():
+        plan.launch(stream)
 
     clk = ClockSampler(dev.index).start()
     # warm-up: at least W (>= 3) steps and at least 1 s of load, so clocks settle
@@ -275,23 +275,23 @@ def main():
     torch.cuda.synchronize(dev)
 
     # ---- timed region: K steps, per-step CUDA events, L2 flush between steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(COMBOS) + 1)] for _ in range(args.steps)]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     t_wall0 = time.perf_counter()
     for k in range(args.steps):
         flush.fill_(k & 0xFF)            # outside the event windows
-        step(ev[k])
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
     torch.cuda.synchronize(dev)
     t_wall1 = time.perf_counter()
     t_wall = t_wall1 - t_wall0
-    clk.stop()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    per_kernel_ms = [[ev[k][i].elapsed_time(ev[k][i + 1]) for i in range(len(COMBOS))] for k in range(args.steps)]
-    step_ms = [sum(r) for r in per_kernel_ms]
+    step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -301,64 +301,85 @@ def main():
     units = world * npix * len(COMBOS)               # pixel-filter evaluations per step, all ranks
     value = units / (ms_per_step / 1e3) / 1e6        # Mpix/s
 
-    # ---- per-kernel breakdown + roofline of the dominant kernel
+    # ---- per-kernel breakdown: each filter launched alone (same L2 flush),
+    # CUDA events on the launching stream; gives the roofline of each kernel
+    kreps = max(3, min(args.steps, 20))
+    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in COMBOS]
+           for _ in range(kreps)]
+    t_k0 = time.perf_counter()
+    for r in range(kreps):
+        for i, (crit, var) in enumerate(COMBOS):
+            flush.fill_((r + i) & 0xFF)
+            kev[r][i][0].record(stream)
+            vfb.vf_filter_batch(x, w, crit, var, out=outs[i], stream=stream)
+            kev[r][i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    t_k1 = time.perf_counter()
+    clk.stop()
     clocks = clk.summary(t_wall0, t_wall1)
     n = w * w
     pairs = n * (n - 1) // 2
     kern = {}
     for i, c in enumerate(COMBOS):
-        ms = statistics.mean(r[i] for r in per_kernel_ms)
+        ms = statistics.mean(kev[r][i][0].elapsed_time(kev[r][i][1]) for r in range(kreps))
         mpix = npix / (ms / 1e3) / 1e6
         tfl = FLOPS_PER_PAIR[c] * pairs * npix / (ms / 1e3) / 1e12
-        kern[f"{c[0]}/{c[1]}"] = {"ms": ms, "mpix_s": mpix, "alg_tflops": tfl,
-                                  "frac_fp32_at_max_clock": tfl / NOMINAL_FP32_TFLOPS_AT_MAX}
+        kern[f"{c[0]}/{c[1]}"] = {"kernel": KERNEL_NAMES[c[0]].format(w=w, v=c[1]), "ms": ms, "mpix_s": mpix,
+                                  "alg_tflops": tfl, "frac_fp32_at_max_clock": tfl / NOMINAL_FP32_TFLOPS_AT_MAX}
         if clocks.get("sm_mhz"):
             kern[f"{c[0]}/{c[1]}"]["frac_fp32_at_measured_clock"] = \
                 tfl / (NOMINAL_FP32_TFLOPS_AT_MAX * clocks["sm_mhz"] / 1965.0)
     dom = max(kern, key=lambda k: kern[k]["ms"])
     d = kern[dom]
-    roofline = {"bound": "alu", "kernel": f"vf_window_kernel<{w},{dom}>", "achieved": d["alg_tflops"],
+    roofline = {"bound": "alu", "kernel": d["kernel"], "achieved": d["alg_tflops"],
                 "peak": NOMINAL_FP32_TFLOPS_AT_MAX, "unit": "TFLOP/s", "frac": d["alg_tflops"] / NOMINAL_FP32_TFLOPS_AT_MAX,
-                "peak_source": "derived: 2 flop x 128 FP32 lanes x 148 SM x 1.965 GHz (DESIGN.md 6.1)",
-                "traffic": ncu_traffic(f"{w}x{w}/{dom}"),
-                "algorithmic_flops_per_launch": FLOPS_PER_PAIR[tuple(dom.split("/"))] * pairs * npix}
+                "peak_source": "derived: 2 flop x 128 FP32 lanes x 148 SM x 1.965 GHz (DESIGN.md 6.1); "
+                               "tools/fp32_peak.cu measures 68.9 TFLOP/s of FFMA",
+                "traffic": ncu_traffic(f"{spec.name}/{dom}"),
+                "algorithmic_flops_per_launch": FLOPS_PER_PAIR[tuple(dom.split("/"))] * pairs * npix,
+                "timing": "kernel launched alone, CUDA events on its stream, L2 flushed before each launch"}
     mm = [k for k in kern if k.endswith("minimax") or k.endswith("poly4")]
     best_mm = max(mm, key=lambda k: kern[k]["frac_fp32_at_max_clock"])
 
-    # ---- end to end through the C ABI with host buffers
+    # ---- end to end through the C ABI with HOST buffers: a plan whose graph is
+    # H2D(input) -> 7 filter kernels -> 7 x D2H(output), pinned host memory
     e2e = None
     if not args.no_e2e:
         h_in = torch.from_numpy(x_np).pin_memory()
-        h_out = torch.empty_like(h_in).pin_memory()
-        ws = torch.empty(vfb.vf_host_workspace_bytes(B, H, W), dtype=torch.uint8, device=dev)
-        for _ in range(2):
-            for crit, var in COMBOS:
-                vfb.vf_filter_host(h_in, w, crit, var, h_out, ws, stream=stream)
+        h_outs = [torch.empty_like(h_in).pin_memory() for _ in COMBOS]
+        d_in2 = torch.empty_like(x)
+        d_outs2 = [torch.empty_like(x) for _ in COMBOS]
+        hplan = vfb.Plan(d_in2, d_outs2, w, COMBOS, h_in=h_in, h_outs=h_outs)
+        for _ in range(3):
+            hplan.launch(stream)
         torch.cuda.synchronize(dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
         ksteps = max(3, min(args.steps, 20))
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ksteps)]
         if world > 1:
             dist.barrier()
-        e0.record(stream)
-        for _ in range(ksteps):
-            for crit, var in COMBOS:
-                vfb.vf_filter_host(h_in, w, crit, var, h_out, ws, stream=stream)
-        e1.record(stream)
+        for k in range(ksteps):
+            flush.fill_(k & 0xFF)
+            eev[k][0].record(stream)
+            hplan.launch(stream)
+            eev[k][1].record(stream)
         torch.cuda.synchronize(dev)
-        e2e_ms = e0.elapsed_time(e1) / ksteps
+        e2e_ms = sum(a.elapsed_time(b) for a, b in eev) / ksteps
         if world > 1:
             t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
+        same = all(torch.equal(h_outs[i], outs[i].cpu()) for i in range(len(COMBOS)))
         e2e = {"value": units / (e2e_ms / 1e3) / 1e6, "unit": "Mpix/s",
-               "h2d_bytes_per_step": len(COMBOS) * npix * 3, "d2h_bytes_per_step": len(COMBOS) * npix * 3,
-               "ms_per_step": e2e_ms, "api": "vf_filter_host (pinned host in/out, one call per filter)"}
+               "h2d_bytes_per_step": npix * 3, "d2h_bytes_per_step": len(COMBOS) * npix * 3,
+               "ms_per_step": e2e_ms, "outputs_match_device_path": same,
+               "api": "vf_plan_create(h_in, h_outs) + vf_plan_launch: graph H2D -> 7 kernels -> 7 D2H"}
+        hplan.close()
 
     # ---- fidelity: minimax vs exact (the paper's quality measure)
+    oi = {c: outs[i] for i, c in enumerate(COMBOS)}
     fid = {}
     for crit, mmv in (("angular", "minimax"), ("exp", "minimax"), ("exp", "poly4"), ("log", "minimax")):
-        f = vfb.fidelity(outs[(crit, "exact")], outs[(crit, mmv)])
+        f = vfb.fidelity(oi[(crit, "exact")], oi[(crit, mmv)])
         fid[f"{crit}/{mmv}"] = {"psnr_db": f["psnr_db"], "ncd": f["ncd"], "diff_frac": f["diff_frac"]}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
@@ -379,9 +400,10 @@ def main():
             "config": {"workload": f"{spec.name}: {B}x{H}x{W} uint8 RGB, {w}x{w} window, "
                                    f"{spec.noise} impulse noise, all 7 criterion/variant filters per step",
                        "per_rank_pixels": npix, "l2": "flushed between steps (512 MiB write, untimed)",
+                       "step": "vf_plan_launch: one CUDA graph, 7 independent filter kernels",
                        "parallelism": f"dp{world} (independent images per rank)"},
             "roofline": roofline,
-            "best_minimax_kernel": {"kernel": best_mm, **kern[best_mm]},
+            "best_minimax_kernel": {"name": best_mm, **kern[best_mm]},
             "per_kernel": kern,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -393,6 +415,7 @@ def main():
                       "fp32_tflops_nominal_at_max_clock": NOMINAL_FP32_TFLOPS_AT_MAX},
         }
         print(json.dumps(line), flush=True)
+    plan.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

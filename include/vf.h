@@ -116,6 +116,22 @@ VF_API int vf_filter_host(const uint8_t *h_imgs, int B, int H, int W, int window
                    int variant, uint8_t *h_outs, void *d_workspace, size_t workspace_bytes,
                    void *stream);
 
+/* PLAN (executor): n filters of the same input, built once as an
+ * instantiated CUDA graph whose n kernel nodes are independent (they run
+ * concurrently, so small images fill the GPU), optionally preceded by an H2D
+ * copy node (h_in != NULL: host [B][H][W][3] -> d_in) and followed by n D2H
+ * copy nodes (h_outs != NULL: d_outs[i] -> h_outs[i]).  All pointers are fixed
+ * at creation (device buffers d_in, d_outs[i] of [B][H][W][3]; host buffers
+ * should be pinned) and must stay valid while the plan is used.
+ * vf_plan_launch enqueues the whole graph on `stream`.  criteria[i],
+ * variants[i] as in vf_filter; n in [1, 64]. */
+typedef struct vf_plan_s *vf_plan;
+VF_API int vf_plan_create(vf_plan *plan, int B, int H, int W, int window, int n, const int *criteria,
+                          const int *variants, const uint8_t *d_in, uint8_t *const *d_outs,
+                          const uint8_t *h_in, uint8_t *const *h_outs);
+VF_API int vf_plan_launch(vf_plan plan, void *stream);
+VF_API int vf_plan_destroy(vf_plan plan);
+
 /* Per-image fidelity statistics of two device image batches a, b
  * ([B][H][W][3]); stats: device double [B][8] =
  *   {pixels with a != b, sum |a-b| (all channels), sum (a-b)^2,
@@ -127,7 +143,7 @@ VF_API int vf_image_stats(const uint8_t *a, const uint8_t *b, int B, int H, int 
 VF_API const char *vf_status_string(int status);
 /* Text of the last error on the calling thread ("" if none). */
 VF_API const char *vf_last_error(void);
-/* ABI version (major*100 + minor). */
+/* ABI version (major*100 + minor): 101. */
 VF_API int vf_version(void);
 
 #ifdef __cplusplus

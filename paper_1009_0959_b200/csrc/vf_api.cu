@@ -1,12 +1,15 @@
 // vf_api.cu -- C ABI of libvf.so (declared in include/vf.h): argument
-// validation, kernel dispatch, error reporting.  Host code only launches;
-// every step of the filter runs in the kernels of vf_window.cuh /
+// validation, kernel selection, launches, the plan executor (an instantiated
+// CUDA graph of parallel filter kernels) and error reporting.  Host code only
+// launches; every step of the filter runs in the kernels of vf_window.cuh /
 // vf_shared.cuh.
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <new>
+#include <vector>
 
 #include "../../include/vf.h"
 #include "vf_shared.cuh"
@@ -17,8 +20,8 @@ namespace {
 
 thread_local char g_err[512] = "";
 
-int fail(int code, const char* fmt, const char* a = "", long long v = 0) {
-  std::snprintf(g_err, sizeof(g_err), fmt, a, v);
+int fail(int code, const char* msg, long long v = 0) {
+  std::snprintf(g_err, sizeof(g_err), msg, v);
   return code;
 }
 
@@ -34,29 +37,38 @@ bool overlap(const void* a, size_t na, const void* b, size_t nb) {
 }
 
 using vf::Launch;
-typedef void (*KernelFn)(const Launch);
+
+// One kernel launch, fully described (function, geometry, parameters), so that
+// it can be launched on a stream or added to a graph as a kernel node.
+struct KernelDesc {
+  const void* fn;
+  dim3 grid, block;
+  Launch L;
+};
 
 template <int WIN>
-KernelFn window_kernel(int crit, int var) {
+const void* window_kernel(int crit, int var) {
   using namespace vf;
-  if (crit == ANGULAR) return var == EXACT ? vf_angular_window_kernel<WIN, EXACT> : vf_angular_window_kernel<WIN, MINIMAX>;
+  if (crit == ANGULAR)
+    return var == EXACT ? (const void*)vf_angular_window_kernel<WIN, EXACT>
+                        : (const void*)vf_angular_window_kernel<WIN, MINIMAX>;
   if (crit == EXPC) {
-    if (var == EXACT) return vf_el_kernel<WIN, EXPC, EXACT>;
-    if (var == MINIMAX) return vf_el_kernel<WIN, EXPC, MINIMAX>;
-    return vf_el_kernel<WIN, EXPC, POLY4>;
+    if (var == EXACT) return (const void*)vf_el_kernel<WIN, EXPC, EXACT>;
+    if (var == MINIMAX) return (const void*)vf_el_kernel<WIN, EXPC, MINIMAX>;
+    return (const void*)vf_el_kernel<WIN, EXPC, POLY4>;
   }
-  return var == EXACT ? vf_el_kernel<WIN, LOGC, EXACT> : vf_el_kernel<WIN, LOGC, MINIMAX>;
+  return var == EXACT ? (const void*)vf_el_kernel<WIN, LOGC, EXACT> : (const void*)vf_el_kernel<WIN, LOGC, MINIMAX>;
 }
 
 int validate(int B, int H, int W, int window, int crit, int var) {
-  if (window < 3 || window % 2 == 0) return fail(VF_EINVAL, "window must be odd and >= 3%s (got %lld)", "", window);
-  if (B < 1) return fail(VF_EINVAL, "batch must be >= 1%s (got %lld)", "", B);
-  if (H < 1 || W < 1) return fail(VF_EINVAL, "image size must be positive%s", "");
-  if (window > H || window > W) return fail(VF_EINVAL, "window larger than the image (S:64)%s", "");
-  if (crit < 0 || crit > 2) return fail(VF_EINVAL, "criterion out of range%s (%lld)", "", crit);
-  if (var < 0 || var > 2) return fail(VF_EINVAL, "variant out of range%s (%lld)", "", var);
-  if (var == VF_MINIMAX_POLY4 && crit != VF_EXP) return fail(VF_EINVAL, "VF_MINIMAX_POLY4 is only defined for VF_EXP%s", "");
-  if (window > 5) return fail(VF_EUNSUPPORTED, "window %s%lld is valid but not compiled (3 and 5 are)", "", window);
+  if (window < 3 || window % 2 == 0) return fail(VF_EINVAL, "window must be odd and >= 3 (got %lld)", window);
+  if (B < 1) return fail(VF_EINVAL, "batch must be >= 1 (got %lld)", B);
+  if (H < 1 || W < 1) return fail(VF_EINVAL, "image size must be positive");
+  if (window > H || window > W) return fail(VF_EINVAL, "window larger than the image (S:64)");
+  if (crit < 0 || crit > 2) return fail(VF_EINVAL, "criterion out of range (%lld)", crit);
+  if (var < 0 || var > 2) return fail(VF_EINVAL, "variant out of range (%lld)", var);
+  if (var == VF_MINIMAX_POLY4 && crit != VF_EXP) return fail(VF_EINVAL, "VF_MINIMAX_POLY4 is only defined for VF_EXP");
+  if (window > 5) return fail(VF_EUNSUPPORTED, "window %lld is valid but not compiled (3 and 5 are)", window);
   return VF_OK;
 }
 
@@ -67,59 +79,80 @@ float kscale(int crit, int window) {
   return 0.0f;
 }
 
-int launch(const uint8_t* in, long long in_stride, int band_row0, int band_rows, int B, int H, int W,
-           int out_row0, int out_rows, int window, int crit, int var, int algo, uint8_t* out,
-           long long out_stride, uint8_t* index, float* agg, cudaStream_t st) {
-  Launch L;
+int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_row0, int band_rows, int B, int H, int W,
+             int out_row0, int out_rows, int window, int crit, int var, int algo, uint8_t* out, long long out_stride,
+             uint8_t* index, float* agg) {
+  Launch& L = kd->L;
   L.in = in; L.out = out; L.idx = index; L.agg = agg;
   L.in_stride = in_stride; L.out_stride = out_stride;
   L.H = H; L.W = W; L.band_row0 = band_row0; L.band_rows = band_rows;
   L.out_row0 = out_row0; L.out_rows = out_rows;
   L.kscale = kscale(crit, window);
-
   if (crit == VF_ANGULAR && algo != VF_ALGO_WINDOW) {
-    const int rc = vf::launch_shared(L, B, window, var, st);
-    if (rc != -100) {   // -100: shared kernel not applicable, fall through
-      if (rc != 0) return cuda_fail((cudaError_t)rc, "vf_shared_kernel launch");
-      return VF_OK;
-    }
+    kd->fn = vf::shared_kernel_fn(window, var);
+    kd->grid = vf::shared_grid(L, B, window);
+    kd->block = dim3(vf::shared::NTHR);
+  } else {
+    kd->fn = window == 3 ? window_kernel<3>(crit, var) : window_kernel<5>(crit, var);
+    kd->grid = dim3((W + vf::TX - 1) / vf::TX, (out_rows + vf::TY - 1) / vf::TY, B);
+    kd->block = dim3(vf::TX, vf::TY);
   }
-  KernelFn k = window == 3 ? window_kernel<3>(crit, var) : window_kernel<5>(crit, var);
-  dim3 grid((W + vf::TX - 1) / vf::TX, (out_rows + vf::TY - 1) / vf::TY, B);
-  dim3 block(vf::TX, vf::TY);
-  if (grid.y > 65535 || grid.z > 65535) return fail(VF_EINVAL, "grid too large%s", "");
-  k<<<grid, block, 0, st>>>(L);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "vf_window_kernel launch");
+  if (kd->grid.y > 65535 || kd->grid.z > 65535)
+    return fail(VF_EINVAL, "grid too large (%lld blocks in y or z)",
+                (long long)(kd->grid.y > kd->grid.z ? kd->grid.y : kd->grid.z));
   return VF_OK;
+}
+
+int launch_desc(KernelDesc& kd, cudaStream_t st) {
+  void* args[] = {&kd.L};
+  cudaError_t e = cudaLaunchKernel(kd.fn, kd.grid, kd.block, args, 0, st);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return VF_OK;
+}
+
+int launch(const uint8_t* in, long long in_stride, int band_row0, int band_rows, int B, int H, int W, int out_row0,
+           int out_rows, int window, int crit, int var, int algo, uint8_t* out, long long out_stride, uint8_t* index,
+           float* agg, cudaStream_t st) {
+  KernelDesc kd;
+  int rc = describe(&kd, in, in_stride, band_row0, band_rows, B, H, W, out_row0, out_rows, window, crit, var, algo,
+                    out, out_stride, index, agg);
+  if (rc) return rc;
+  return launch_desc(kd, st);
 }
 
 }  // namespace
 
+// ---- plan: an instantiated CUDA graph ---------------------------------------------
+struct vf_plan_s {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int nkernels = 0;
+};
+
 extern "C" {
 
-int vf_filter_batch_algo(const uint8_t* imgs, int B, int H, int W, int window, int criterion, int variant,
-                         int algo, uint8_t* outs, uint8_t* index, float* aggregates, void* stream) {
+int vf_filter_batch_algo(const uint8_t* imgs, int B, int H, int W, int window, int criterion, int variant, int algo,
+                         uint8_t* outs, uint8_t* index, float* aggregates, void* stream) {
   g_err[0] = 0;
   int rc = validate(B, H, W, window, criterion, variant);
   if (rc) return rc;
-  if (!imgs || !outs) return fail(VF_EINVAL, "NULL image or output pointer%s", "");
-  if (algo < 0 || algo > 2) return fail(VF_EINVAL, "algo out of range%s", "");
+  if (!imgs || !outs) return fail(VF_EINVAL, "NULL image or output pointer");
+  if (algo < 0 || algo > 2) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
   const size_t bytes = (size_t)B * H * W * 3;
-  if (overlap(imgs, bytes, outs, bytes)) return fail(VF_EINVAL, "input and output overlap%s", "");
+  if (overlap(imgs, bytes, outs, bytes)) return fail(VF_EINVAL, "input and output overlap");
   const long long stride = (long long)H * W * 3;
-  return launch(imgs, stride, 0, H, B, H, W, 0, H, window, criterion, variant, algo, outs, stride, index,
-                aggregates, (cudaStream_t)stream);
+  return launch(imgs, stride, 0, H, B, H, W, 0, H, window, criterion, variant, algo, outs, stride, index, aggregates,
+                (cudaStream_t)stream);
 }
 
-int vf_filter_batch(const uint8_t* imgs, int B, int H, int W, int window, int criterion, int variant,
-                    uint8_t* outs, uint8_t* index, float* aggregates, void* stream) {
+int vf_filter_batch(const uint8_t* imgs, int B, int H, int W, int window, int criterion, int variant, uint8_t* outs,
+                    uint8_t* index, float* aggregates, void* stream) {
   return vf_filter_batch_algo(imgs, B, H, W, window, criterion, variant, VF_ALGO_AUTO, outs, index, aggregates,
                               stream);
 }
 
-int vf_filter(const uint8_t* img, int H, int W, int window, int criterion, int variant, uint8_t* out,
-              uint8_t* index, float* aggregates, void* stream) {
+int vf_filter(const uint8_t* img, int H, int W, int window, int criterion, int variant, uint8_t* out, uint8_t* index,
+              float* aggregates, void* stream) {
   return vf_filter_batch_algo(img, 1, H, W, window, criterion, variant, VF_ALGO_AUTO, out, index, aggregates,
                               stream);
 }
@@ -130,19 +163,18 @@ int vf_filter_rows(const uint8_t* band, int band_row0, int band_rows, int H, int
   g_err[0] = 0;
   int rc = validate(1, H, W, window, criterion, variant);
   if (rc) return rc;
-  if (!band || !out) return fail(VF_EINVAL, "NULL band or output pointer%s", "");
-  if (out_rows < 1 || out_row0 < 0 || out_row0 + out_rows > H)
-    return fail(VF_EINVAL, "output rows outside the image%s", "");
+  if (!band || !out) return fail(VF_EINVAL, "NULL band or output pointer");
+  if (out_rows < 1 || out_row0 < 0 || out_row0 + out_rows > H) return fail(VF_EINVAL, "output rows outside the image");
   const int r = window / 2;
   const int need_lo = out_row0 - r < 0 ? 0 : out_row0 - r;
   const int need_hi = out_row0 + out_rows + r > H ? H : out_row0 + out_rows + r;
   if (band_rows < 1 || band_row0 < 0 || band_row0 > need_lo || band_row0 + band_rows < need_hi ||
       band_row0 + band_rows > H)
-    return fail(VF_EINVAL, "row band does not cover the rows the stripe reads%s", "");
+    return fail(VF_EINVAL, "row band does not cover the rows the stripe reads");
   if (overlap(band, (size_t)band_rows * W * 3, out, (size_t)out_rows * W * 3))
-    return fail(VF_EINVAL, "input and output overlap%s", "");
-  return launch(band, 0, band_row0, band_rows, 1, H, W, out_row0, out_rows, window, criterion, variant,
-                VF_ALGO_AUTO, out, 0, index, aggregates, (cudaStream_t)stream);
+    return fail(VF_EINVAL, "input and output overlap");
+  return launch(band, 0, band_row0, band_rows, 1, H, W, out_row0, out_rows, window, criterion, variant, VF_ALGO_AUTO,
+                out, 0, index, aggregates, (cudaStream_t)stream);
 }
 
 size_t vf_host_workspace_bytes(int B, int H, int W) {
@@ -151,14 +183,14 @@ size_t vf_host_workspace_bytes(int B, int H, int W) {
   return 2 * ((img + 255) / 256 * 256);
 }
 
-int vf_filter_host(const uint8_t* h_imgs, int B, int H, int W, int window, int criterion, int variant,
-                   uint8_t* h_outs, void* d_workspace, size_t workspace_bytes, void* stream) {
+int vf_filter_host(const uint8_t* h_imgs, int B, int H, int W, int window, int criterion, int variant, uint8_t* h_outs,
+                   void* d_workspace, size_t workspace_bytes, void* stream) {
   g_err[0] = 0;
   int rc = validate(B, H, W, window, criterion, variant);
   if (rc) return rc;
-  if (!h_imgs || !h_outs || !d_workspace) return fail(VF_EINVAL, "NULL pointer%s", "");
+  if (!h_imgs || !h_outs || !d_workspace) return fail(VF_EINVAL, "NULL pointer");
   const size_t need = vf_host_workspace_bytes(B, H, W);
-  if (workspace_bytes < need) return fail(VF_EINVAL, "workspace too small (need %s%lld bytes)", "", (long long)need);
+  if (workspace_bytes < need) return fail(VF_EINVAL, "workspace too small (need %lld bytes)", (long long)need);
   const size_t img = (size_t)B * H * W * 3;
   uint8_t* d_in = (uint8_t*)d_workspace;
   uint8_t* d_out = d_in + (img + 255) / 256 * 256;
@@ -174,10 +206,83 @@ int vf_filter_host(const uint8_t* h_imgs, int B, int H, int W, int window, int c
   return VF_OK;
 }
 
+int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const int* criteria, const int* variants,
+                   const uint8_t* d_in, uint8_t* const* d_outs, const uint8_t* h_in, uint8_t* const* h_outs) {
+  g_err[0] = 0;
+  if (!plan) return fail(VF_EINVAL, "NULL plan pointer");
+  *plan = nullptr;
+  if (n < 1 || n > 64) return fail(VF_EINVAL, "number of filters must be in [1, 64] (got %lld)", n);
+  if (!criteria || !variants || !d_in || !d_outs) return fail(VF_EINVAL, "NULL argument");
+  const size_t bytes = (size_t)B * H * W * 3;
+  for (int i = 0; i < n; ++i) {
+    int rc = validate(B, H, W, window, criteria[i], variants[i]);
+    if (rc) return rc;
+    if (!d_outs[i]) return fail(VF_EINVAL, "NULL output %lld", i);
+    if (overlap(d_in, bytes, d_outs[i], bytes)) return fail(VF_EINVAL, "input and output %lld overlap", i);
+    for (int j = 0; j < i; ++j)
+      if (overlap(d_outs[j], bytes, d_outs[i], bytes)) return fail(VF_EINVAL, "outputs %lld overlap", i);
+    if (h_outs && !h_outs[i]) return fail(VF_EINVAL, "NULL host output %lld", i);
+  }
+  vf_plan_s* p = new (std::nothrow) vf_plan_s();
+  if (!p) return fail(VF_ECUDA, "out of host memory");
+  cudaError_t e = cudaGraphCreate(&p->graph, 0);
+  if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaGraphCreate"); }
+  auto bail = [&](int rc) { cudaGraphDestroy(p->graph); delete p; return rc; };
+  cudaGraphNode_t h2d = nullptr;
+  if (h_in) {
+    e = cudaGraphAddMemcpyNode1D(&h2d, p->graph, nullptr, 0, (void*)d_in, h_in, bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (H2D)"));
+  }
+  const long long stride = (long long)H * W * 3;
+  for (int i = 0; i < n; ++i) {
+    KernelDesc kd;
+    int rc = describe(&kd, d_in, stride, 0, H, B, H, W, 0, H, window, criteria[i], variants[i], VF_ALGO_AUTO,
+                      d_outs[i], stride, nullptr, nullptr);
+    if (rc) return bail(rc);
+    void* args[] = {&kd.L};
+    cudaKernelNodeParams kp = {};
+    kp.func = (void*)kd.fn;
+    kp.gridDim = kd.grid;
+    kp.blockDim = kd.block;
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = args;
+    cudaGraphNode_t kn;
+    e = cudaGraphAddKernelNode(&kn, p->graph, h2d ? &h2d : nullptr, h2d ? 1 : 0, &kp);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddKernelNode"));
+    if (h_outs) {
+      cudaGraphNode_t d2h;
+      e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, &kn, 1, h_outs[i], d_outs[i], bytes, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (D2H)"));
+    }
+  }
+  e = cudaGraphInstantiate(&p->exec, p->graph, 0);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphInstantiate"));
+  p->nkernels = n;
+  *plan = p;
+  return VF_OK;
+}
+
+int vf_plan_launch(vf_plan plan, void* stream) {
+  g_err[0] = 0;
+  if (!plan || !plan->exec) return fail(VF_EINVAL, "invalid plan");
+  cudaError_t e = cudaGraphLaunch(plan->exec, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
+  return VF_OK;
+}
+
+int vf_plan_destroy(vf_plan plan) {
+  g_err[0] = 0;
+  if (!plan) return VF_OK;
+  if (plan->exec) cudaGraphExecDestroy(plan->exec);
+  if (plan->graph) cudaGraphDestroy(plan->graph);
+  delete plan;
+  return VF_OK;
+}
+
 int vf_image_stats(const uint8_t* a, const uint8_t* b, int B, int H, int W, double* stats, void* stream) {
   g_err[0] = 0;
-  if (!a || !b || !stats) return fail(VF_EINVAL, "NULL pointer%s", "");
-  if (B < 1 || H < 1 || W < 1) return fail(VF_EINVAL, "bad size%s", "");
+  if (!a || !b || !stats) return fail(VF_EINVAL, "NULL pointer");
+  if (B < 1 || H < 1 || W < 1) return fail(VF_EINVAL, "bad size");
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(double) * 8 * (size_t)B, st);
   if (e != cudaSuccess) return cuda_fail(e, "stats memset");
@@ -202,6 +307,6 @@ const char* vf_status_string(int status) {
 
 const char* vf_last_error(void) { return g_err; }
 
-int vf_version(void) { return 100; }
+int vf_version(void) { return 101; }
 
 }  // extern "C"

@@ -227,20 +227,18 @@ __global__ void __launch_bounds__(shared::NTHR) vf_angular_shared_kernel(const L
   }
 }
 
-inline int launch_shared(const Launch& L, int B, int window, int var, cudaStream_t st) {
+// Kernel + grid of the pair-sharing kernel for a launch (see vf_api.cu).
+inline const void* shared_kernel_fn(int window, int var) {
+  if (window == 3) return var == EXACT ? (const void*)vf_angular_shared_kernel<3, EXACT>
+                                       : (const void*)vf_angular_shared_kernel<3, MINIMAX>;
+  return var == EXACT ? (const void*)vf_angular_shared_kernel<5, EXACT> : (const void*)vf_angular_shared_kernel<5, MINIMAX>;
+}
+
+inline dim3 shared_grid(const Launch& L, int B, int window) {
   using namespace shared;
   const int R = window / 2;
   const int TW = PW - 2 * R, TH = PH - 2 * R;
-  dim3 grid((L.W + TW - 1) / TW, (L.out_rows + TH - 1) / TH, B);
-  if (grid.y > 65535 || grid.z > 65535) return (int)cudaErrorInvalidConfiguration;
-  if (window == 3) {
-    if (var == EXACT) vf_angular_shared_kernel<3, EXACT><<<grid, NTHR, 0, st>>>(L);
-    else vf_angular_shared_kernel<3, MINIMAX><<<grid, NTHR, 0, st>>>(L);
-  } else {
-    if (var == EXACT) vf_angular_shared_kernel<5, EXACT><<<grid, NTHR, 0, st>>>(L);
-    else vf_angular_shared_kernel<5, MINIMAX><<<grid, NTHR, 0, st>>>(L);
-  }
-  return (int)cudaGetLastError();
+  return dim3((L.W + TW - 1) / TW, (L.out_rows + TH - 1) / TH, B);
 }
 
 }  // namespace vf

@@ -24,8 +24,8 @@ CRITERIA = {"angular": VF_ANGULAR, "exp": VF_EXP, "log": VF_LOG}
 VARIANTS = {"exact": VF_EXACT, "minimax": VF_MINIMAX, "poly4": VF_MINIMAX_POLY4}
 ALGOS = {"auto": VF_ALGO_AUTO, "window": VF_ALGO_WINDOW, "shared": VF_ALGO_SHARED}
 EXPORTS = ["vf_filter", "vf_filter_batch", "vf_filter_rows", "vf_filter_batch_algo",
-           "vf_host_workspace_bytes", "vf_filter_host", "vf_image_stats", "vf_status_string",
-           "vf_last_error", "vf_version"]
+           "vf_host_workspace_bytes", "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_destroy",
+           "vf_image_stats", "vf_status_string", "vf_last_error", "vf_version"]
 
 
 class VFError(RuntimeError):
@@ -54,6 +54,9 @@ def load_library(path: str = LIB_PATH):
     L.vf_host_workspace_bytes.argtypes = [I, I, I]
     L.vf_host_workspace_bytes.restype = S
     L.vf_filter_host.argtypes = [P, I, I, I, I, I, I, P, P, S, P]
+    L.vf_plan_create.argtypes = [ctypes.POINTER(P), I, I, I, I, I, P, P, P, P, P, P]
+    L.vf_plan_launch.argtypes = [P, P]
+    L.vf_plan_destroy.argtypes = [P]
     L.vf_image_stats.argtypes = [P, P, I, I, I, P, P]
     L.vf_status_string.argtypes = [I]
     L.vf_status_string.restype = ctypes.c_char_p
@@ -61,7 +64,8 @@ def load_library(path: str = LIB_PATH):
     L.vf_last_error.restype = ctypes.c_char_p
     L.vf_version.argtypes = []
     for name in ("vf_filter", "vf_filter_batch", "vf_filter_batch_algo", "vf_filter_rows",
-                 "vf_filter_host", "vf_image_stats", "vf_version"):
+                 "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_destroy", "vf_image_stats",
+                 "vf_version"):
         getattr(L, name).restype = I
     _lib = L
     return L
@@ -171,6 +175,55 @@ def vf_filter_host(h_imgs: torch.Tensor, window: int, criterion, variant, h_out:
     return h_out
 
 
+class Plan:
+    """vf_plan_* (include/vf.h): several filters of one input as ONE CUDA graph
+    with independent (concurrent) kernel nodes, optionally with the H2D copy
+    of a host input and the D2H copies of the outputs inside the graph.
+
+    d_in: CUDA uint8 [B, H, W, 3]; d_outs: list of CUDA tensors like d_in;
+    combos: list of (criterion, variant); h_in / h_outs: pinned host tensors
+    (optional).  Buffers are bound at creation; call launch() per step."""
+
+    def __init__(self, d_in: torch.Tensor, d_outs, window: int, combos, h_in: Optional[torch.Tensor] = None,
+                 h_outs=None):
+        L = load_library()
+        x = d_in.unsqueeze(0) if d_in.dim() == 3 else d_in
+        B, H, W, _ = x.shape
+        n = len(combos)
+        if len(d_outs) != n or (h_outs is not None and len(h_outs) != n):
+            raise ValueError("one output per filter")
+        for t in d_outs:
+            _dev_u8(t, "d_outs[i]")
+            if t.numel() != x.numel():
+                raise ValueError("outputs must match the input size")
+        if h_in is not None and (h_in.is_cuda or h_in.dtype != torch.uint8 or h_in.numel() != x.numel()):
+            raise ValueError("h_in must be a host uint8 tensor like d_in")
+        self._keep = (d_in, list(d_outs), h_in, None if h_outs is None else list(h_outs))
+        crit = (ctypes.c_int * n)(*[_crit(c) for c, _ in combos])
+        var = (ctypes.c_int * n)(*[_var(v) for _, v in combos])
+        douts = (ctypes.c_void_p * n)(*[t.data_ptr() for t in d_outs])
+        houts = None if h_outs is None else (ctypes.c_void_p * n)(*[t.data_ptr() for t in h_outs])
+        self._h = ctypes.c_void_p()
+        rc = L.vf_plan_create(ctypes.byref(self._h), B, H, W, window, n, crit, var, _dev_u8(x, "d_in"), douts,
+                              None if h_in is None else h_in.data_ptr(), houts)
+        _check(rc, "vf_plan_create")
+        self.n = n
+
+    def launch(self, stream=None):
+        _check(load_library().vf_plan_launch(self._h, _stream(stream)), "vf_plan_launch")
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load_library().vf_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def vf_image_stats(a: torch.Tensor, b: torch.Tensor, stats: Optional[torch.Tensor] = None,
                    stream=None) -> torch.Tensor:
     """Per-image [B, 8] float64 statistics (see include/vf.h)."""
@@ -190,6 +243,10 @@ def vf_status_string(status: int) -> str:
 
 def vf_last_error() -> str:
     return load_library().vf_last_error().decode()
+
+
+def vf_plan_create(*a, **k) -> "Plan":
+    return Plan(*a, **k)
 
 
 def vf_version() -> int:

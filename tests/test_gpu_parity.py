@@ -264,3 +264,57 @@ def test_c4_full_batch_sampled(crit, var):
         assert torch.equal(o2[0], out[b]) and torch.equal(i2[0], idx[b])
         sampled_parity(xb[j], 3, crit, var, o2[0].cpu().numpy(), i2[0].cpu().numpy(), a2[0].cpu().numpy(),
                        nsample=5000, seed=b)
+
+
+# ------------------------------------------------------------- plan (CUDA-graph executor)
+@pytest.mark.parametrize("w", [3, 5])
+def test_plan_matches_individual_filters(w):
+    """A plan runs the 7 filters as independent graph nodes; outputs must be
+    bit-identical to launching each filter alone, on every replay."""
+    _, x = vfsynth.make_image(vfsynth.config("C2"), 0)
+    xt = torch.from_numpy(x).cuda()
+    outs = [torch.empty_like(xt) for _ in CV]
+    plan = vfb.Plan(xt, outs, w, CV)
+    for rep in range(3):
+        for o in outs:
+            o.zero_()
+        plan.launch()
+        torch.cuda.synchronize()
+        for (crit, var), o in zip(CV, outs):
+            ref, _, _ = vfb.filter(xt, w, crit, var)
+            assert torch.equal(o, ref), (rep, crit, var)
+    plan.close()
+
+
+def test_host_plan_copies_inside_graph():
+    spec = dataclasses.replace(vfsynth.config("C4"), H=96, W=128, batch=2)
+    xb = vfsynth.make_batch(spec)
+    h_in = torch.from_numpy(xb).pin_memory()
+    h_outs = [torch.zeros_like(h_in).pin_memory() for _ in CV]
+    d_in = torch.empty(h_in.shape, dtype=torch.uint8, device="cuda")
+    d_outs = [torch.empty_like(d_in) for _ in CV]
+    plan = vfb.Plan(d_in, d_outs, 3, CV, h_in=h_in, h_outs=h_outs)
+    plan.launch()
+    torch.cuda.synchronize()
+    xt = torch.from_numpy(xb).cuda()
+    for (crit, var), ho in zip(CV, h_outs):
+        ref, _, _ = vfb.filter(xt, 3, crit, var)
+        assert torch.equal(ho, ref.cpu()), (crit, var)
+    # new host data is picked up by the next launch (pointers are bound, not data)
+    h_in.copy_(torch.from_numpy(xb[::-1].copy()))
+    plan.launch()
+    torch.cuda.synchronize()
+    ref, _, _ = vfb.filter(xt.flip(0).contiguous(), 3, *CV[1])
+    assert torch.equal(h_outs[1], ref.cpu())
+    plan.close()
+
+
+def test_plan_rejects_bad_arguments():
+    x = torch.zeros((16, 16, 3), dtype=torch.uint8, device="cuda")
+    with pytest.raises(vfb.VFError):
+        vfb.Plan(x, [x], 3, [("angular", "minimax")])                   # output aliases input
+    o = torch.empty_like(x)
+    with pytest.raises(vfb.VFError):
+        vfb.Plan(x, [o, o], 3, [("angular", "minimax"), ("exp", "exact")])   # outputs overlap
+    with pytest.raises(vfb.VFError):
+        vfb.Plan(x, [o], 3, [("log", "poly4")])

@@ -69,7 +69,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_status_strings_and_version(lib):
     from paper_1009_0959_b200 import vf
-    assert vf.vf_version() == 100
+    assert vf.vf_version() == 101
     assert vf.vf_status_string(0) == "VF_OK"
     assert "invalid" in vf.vf_status_string(-1)
     assert "compiled" in vf.vf_status_string(-2)
@@ -96,3 +96,15 @@ def test_invalid_arguments_rejected_before_any_device_work(lib):
     # stripe band that misses a halo row
     assert lib.vf_filter_rows(p, 5, 8, 40, 16, 5, 5, 3, 0, 1, q, None, None, None) == -1
     assert lib.vf_host_workspace_bytes(1, 10, 10) >= 600
+    # plans validate every filter before creating anything
+    h = ctypes.c_void_p()
+    crit = (ctypes.c_int * 2)(0, 1)
+    var = (ctypes.c_int * 2)(1, 2)
+    outs = (ctypes.c_void_p * 2)(1 << 40, 1 << 41)
+    assert lib.vf_plan_create(ctypes.byref(h), 1, 16, 16, 3, 2, crit, (ctypes.c_int * 2)(1, 3), p, outs, None,
+                              None) == -1
+    assert lib.vf_plan_create(ctypes.byref(h), 1, 16, 16, 3, 0, crit, var, p, outs, None, None) == -1
+    assert lib.vf_plan_create(ctypes.byref(h), 1, 16, 16, 4, 2, crit, var, p, outs, None, None) == -1
+    assert h.value is None
+    assert lib.vf_plan_launch(None, None) == -1
+    assert lib.vf_plan_destroy(None) == 0
