@@ -94,7 +94,8 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
     kd->block = dim3(vf::shared::NTHR);
   } else {
     kd->fn = window == 3 ? window_kernel<3>(crit, var) : window_kernel<5>(crit, var);
-    kd->grid = dim3((W + vf::TX - 1) / vf::TX, (out_rows + vf::TY - 1) / vf::TY, B);
+    const int th = crit == VF_ANGULAR ? vf::TY : vf::TY * vf::el_opt(window);
+    kd->grid = dim3((W + vf::TX - 1) / vf::TX, (out_rows + th - 1) / th, B);
     kd->block = dim3(vf::TX, vf::TY);
   }
   if (kd->grid.y > 65535 || kd->grid.z > 65535)

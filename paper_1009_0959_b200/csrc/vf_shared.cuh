@@ -16,9 +16,10 @@
 //           and dx > 0), |dy|,|dx| <= 2r, and every p in P:
 //           M[delta][p] = A(x_p, x_{p+delta}) (minimax: Table 1 ARCSIN row in
 //           tau; exact: Eq. 6 with libm asinf).  Pairs that may have cos < 0.5
-//           or a zero vector (a conservative test, <~1.5% of pairs) are flagged
+//           (a conservative test on tau, ~1% of pairs) are flagged
 //           and re-evaluated exactly afterwards (exact 4D^2 < P predicate,
-//           ARCCOS row / acosf, zero-vector rule S:342).
+//           ARCCOS row / acosf).  Zero vectors are fixed by a
+//           block-uniform slow path in the (rare) blocks that contain one.
 //   phase C for each output window and each pair i < j of it:
 //           v = M[o_j - o_i][c + o_i];  R_i += v;  R_j += v
 //   then argmin (lowest index on ties) and store.
@@ -79,17 +80,19 @@ struct SharedSmem {
 template <int WIN, int VAR, int GD, int OPT, int G>
 __device__ __forceinline__ void shared_group(SharedSmem<GD>& sm, const uint32_t (&my_pk)[shared::PPT],
                                              const float (&my_nn)[shared::PPT], const float (&my_nrm)[shared::PPT],
-                                             const float (&my_nrmk)[shared::PPT], float (&Ra)[OPT][WIN * WIN],
-                                             int tid) {
+                                             float (&Ra)[OPT][WIN * WIN], int tid, bool blk_zero) {
   using namespace shared;
   constexpr int R = WIN / 2;
   constexpr int N = WIN * WIN;
   constexpr int TW = PW - 2 * R;
   constexpr int TH = PH - 2 * R;
   const int tx = tid & 31, ty = tid >> 5;
-  __syncthreads();   // staging done (G = 0) / previous phase C done with M
+  if (G > 0) __syncthreads();   // previous phase C done with M (G = 0: the staging barrier)
   // ---- phase A: pair maps for offsets [G*GD, G*GD + GD) ------------------------------
-  uint64_t flags = 0;
+  constexpr int NFW = (GD * PPT + 31) / 32;                 // flag words
+  uint32_t flags[NFW];
+#pragma unroll
+  for (int f = 0; f < NFW; ++f) flags[f] = 0u;
 #pragma unroll
   for (int dl = 0; dl < GD; ++dl) {
     const int d = G * GD + dl;
@@ -105,31 +108,56 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD>& sm, const uint32_t 
       const float Pl = fmaf(my_nn[k], qn.x, -Ph);
       const float X = __fadd_rn(fmaf(-D, D, Ph), Pl);         // |x_p x x_q|^2
       const float s = __fmul_rn(my_nrm[k], qn.y);
-      const bool rare = !(D > __fmul_rn(my_nrmk[k], qn.y));   // maybe cos < 0.5, or a zero vector
       const float w = fmaf(s, D, Ph);
-      const float tau = __fmul_rn(X, rsqrt_approx(fmaf(X, w, 1e-30f)));
+      const float tau = __fmul_rn(X, rsqrt_approx(fmaf(X, w, 1e-30f)));   // sqrt(1 - cos)
       float v;
       if (VAR == EXACT)
         v = 2.0f * asinf(tau * 0.70710678118654752f);
       else
         v = horner4(coef::ASIN(), tau);
       sm.M[dl][p] = v;
-      // (offsets reaching below the region read the zero padding: never flag those)
+      // cos < 0.5 <=> tau > 1/sqrt2: flag a superset (margin 2^-10 >> the
+      // ~5e-7 relative error of tau) for the exact decision below.  Offsets
+      // reaching below the region read the zero padding: never flag those.
+      const bool rare = tau > 0.70641626f;                    // (1/sqrt2) (1 - 2^-10)
       const bool valid = (k < PPT - 1) || (q < NP);
-      flags |= (rare && valid) ? (1ull << (dl * PPT + k)) : 0ull;
+      const int bit = dl * PPT + k;                           // compile-time after unrolling
+      if (rare && valid) flags[bit / 32] |= 1u << (bit % 32);
     }
   }
   // rare pairs: exact branch decision (re-evaluated, then overwritten)
-  while (flags) {
-    const int bit = __ffsll((long long)flags) - 1;
-    flags &= flags - 1;
-    const int dl = bit / PPT, k = bit - dl * PPT;
-    const int d = G * GD + dl;
-    const int p = tid + NTHR * k;
-    const int q = p + delta_dy(R, d) * PW + delta_dx(R, d);
-    const float2 pn = sm.nm[p], qn = sm.nm[q];
-    float v;
-    if (angular_fixup<VAR>(sm.pk[p], pn.x, pn.y, sm.pk[q], qn.x, qn.y, &v)) sm.M[dl][p] = v;
+#pragma unroll
+  for (int f = 0; f < NFW; ++f) {
+    while (flags[f]) {
+      const int bit = 32 * f + __ffs(flags[f]) - 1;
+      flags[f] &= flags[f] - 1;
+      const int dl = bit / PPT, k = bit - dl * PPT;
+      const int d = G * GD + dl;
+      const int p = tid + NTHR * k;
+      const int q = p + delta_dy(R, d) * PW + delta_dx(R, d);
+      const float2 pn = sm.nm[p], qn = sm.nm[q];
+      float v;
+      if (angular_fixup<VAR>(sm.pk[p], pn.x, pn.y, sm.pk[q], qn.x, qn.y, &v)) sm.M[dl][p] = v;
+    }
+  }
+  // zero vectors: block-uniform slow path, only in blocks that hold
+  // a black pixel.  Every pair touching a zero pixel is set to 0, including
+  // the entries other threads wrote with the zero pixel on the q side.
+  if (blk_zero) {
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      if (my_nn[k] == 0.0f) {
+        const int p = tid + NTHR * k;
+#pragma unroll
+        for (int dl = 0; dl < GD; ++dl) {
+          const int d = G * GD + dl;
+          const int off = delta_dy(R, d) * PW + delta_dx(R, d);
+          sm.M[dl][p] = 0.0f;
+          if (p - off >= 0) sm.M[dl][p - off] = 0.0f;
+        }
+      }
+    }
   }
   __syncthreads();
   // ---- phase C: accumulate the window aggregates ------------------------------------
@@ -157,13 +185,13 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD>& sm, const uint32_t 
 template <int WIN, int VAR, int GD, int OPT, int... Gs>
 __device__ __forceinline__ void shared_groups(std::integer_sequence<int, Gs...>, SharedSmem<GD>& sm,
                                               const uint32_t (&my_pk)[shared::PPT], const float (&my_nn)[shared::PPT],
-                                              const float (&my_nrm)[shared::PPT], const float (&my_nrmk)[shared::PPT],
-                                              float (&Ra)[OPT][WIN * WIN], int tid) {
-  (shared_group<WIN, VAR, GD, OPT, Gs>(sm, my_pk, my_nn, my_nrm, my_nrmk, Ra, tid), ...);
+                                              const float (&my_nrm)[shared::PPT], float (&Ra)[OPT][WIN * WIN], int tid,
+                                              bool blk_zero) {
+  (shared_group<WIN, VAR, GD, OPT, Gs>(sm, my_pk, my_nn, my_nrm, Ra, tid, blk_zero), ...);
 }
 
 template <int WIN, int VAR>
-__global__ void __launch_bounds__(shared::NTHR) vf_angular_shared_kernel(const Launch L) {
+__global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_shared_kernel(const Launch L) {
   using namespace shared;
   constexpr int R = WIN / 2;
   constexpr int N = WIN * WIN;
@@ -185,7 +213,8 @@ __global__ void __launch_bounds__(shared::NTHR) vf_angular_shared_kernel(const L
 
   // ---- stage P ----------------------------------------------------------------
   uint32_t my_pk[PPT];
-  float my_nn[PPT], my_nrm[PPT], my_nrmk[PPT];
+  float my_nn[PPT], my_nrm[PPT];
+  bool has_zero = false;
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     const int p = tid + NTHR * k;
@@ -197,11 +226,12 @@ __global__ void __launch_bounds__(shared::NTHR) vf_angular_shared_kernel(const L
     my_pk[k] = pack_rgb(r, g, bl);
     my_nn[k] = nn;
     my_nrm[k] = nrm;
-    my_nrmk[k] = nrm * 0.50048828125f;                          // 0.5 (1 + 2^-10): conservative cut
+    has_zero |= (nn == 0.0f);
     sm.pk[p] = my_pk[k];
     sm.nm[p] = make_float2(nn, nrm);
   }
   if (tid < PAD) { sm.pk[NP + tid] = 0u; sm.nm[NP + tid] = make_float2(0.0f, 0.0f); }
+  const bool blk_zero = __syncthreads_or(has_zero) != 0;       // staging barrier
 
   float Ra[OPT][N];
 #pragma unroll
@@ -209,8 +239,8 @@ __global__ void __launch_bounds__(shared::NTHR) vf_angular_shared_kernel(const L
 #pragma unroll
     for (int i = 0; i < N; ++i) Ra[k][i] = 0.0f;
 
-  shared_groups<WIN, VAR, GD, OPT>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, my_nrmk, Ra,
-                                   tid);
+  shared_groups<WIN, VAR, GD, OPT>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, Ra, tid,
+                                   blk_zero);
 
   // ---- argmin + store ------------------------------------------------------------------
 #pragma unroll

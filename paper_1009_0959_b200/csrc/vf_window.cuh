@@ -22,6 +22,7 @@ namespace vf {
 
 constexpr int TX = 32;   // output tile width  (one warp per tile row)
 constexpr int TY = 8;    // output tile height (8 warps per block)
+__host__ __device__ constexpr int el_opt(int win) { return win == 3 ? 2 : 1; }  // exp/log: output rows per thread
 
 struct Launch {
   const uint8_t* in;   // global row band_row0 of image 0
@@ -78,58 +79,73 @@ template <int WIN, int CRIT, int VAR>
 __global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
   constexpr int R = WIN / 2;
   constexpr int N = WIN * WIN;
+  constexpr int OPT = el_opt(WIN);             // output rows per thread (consecutive)
+  constexpr int TYE = TY * OPT;                // output tile height
   constexpr int SW = TX + 2 * R;
-  constexpr int SH = TY + 2 * R;
+  constexpr int SH = TYE + 2 * R;
+  constexpr int LR = OPT + 2 * R;              // sample rows a thread reads
   __shared__ uint32_t s_pk[SH * SW];
 
   const int b = blockIdx.z;
   const int x0 = blockIdx.x * TX;
-  const int y0 = L.out_row0 + blockIdx.y * TY;
+  const int y0 = L.out_row0 + blockIdx.y * TYE;
   const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
-  const int tid = threadIdx.y * TX + threadIdx.x;
-  for (int p = tid; p < SH * SW; p += TX * TY) {          // a1 + a2
-    const int sy = p / SW, sx = p - sy * SW;
-    const uint8_t* q = pixel_ptr(L, in, y0 + sy - R, x0 + sx - R);
-    s_pk[p] = pack_rgb(q[0], q[1], q[2]);
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  // a1 + a2: stage (rows per warp, columns per lane: no index division)
+  for (int row = ty; row < SH; row += TY) {
+    const int gy = clampi(y0 - R + row, 0, L.H - 1) - L.band_row0;
+    const uint8_t* rp = in + (long long)gy * L.W * 3;
+#pragma unroll
+    for (int col = tx; col < SW; col += TX) {
+      const uint8_t* q = rp + clampi(x0 - R + col, 0, L.W - 1) * 3;
+      s_pk[row * SW + col] = pack_rgb(q[0], q[1], q[2]);
+    }
   }
   __syncthreads();
 
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int ox = x0 + tx, oy = y0 + ty;
-  if (ox >= L.W || oy >= L.out_row0 + L.out_rows) return;
+  const int ox = x0 + tx;
+  const int oyb = y0 + OPT * ty;
+  if (ox >= L.W || oyb >= L.out_row0 + L.out_rows) return;
 
-  uint32_t pk[N];
+  uint32_t pk[LR * WIN];
 #pragma unroll
-  for (int k = 0; k < N; ++k) pk[k] = s_pk[(ty + k / WIN) * SW + tx + k % WIN];
+  for (int k = 0; k < LR * WIN; ++k) pk[k] = s_pk[(OPT * ty + k / WIN) * SW + tx + k % WIN];
 
-  // a3: S1 = sum_{i<j} d1_ij, exact, in 4 independent integer chains
-  uint32_t acc[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-  for (int i = 0, p = 0; i < N; ++i) {
+  for (int o = 0; o < OPT; ++o) {
+    if (o > 0 && oyb + o >= L.out_row0 + L.out_rows) break;
+    uint32_t w[N];
 #pragma unroll
-    for (int j = i + 1; j < N; ++j, ++p) acc[p & 3] = sad4(pk[i], pk[j], acc[p & 3]);
-  }
-  const uint32_t S1 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    for (int k = 0; k < N; ++k) w[k] = pk[o * WIN + k];
+    // a3: S1 = sum_{i<j} d1_ij, exact, in 4 independent integer chains
+    uint32_t acc[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i = 0, p = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = i + 1; j < N; ++j, ++p) acc[p & 3] = sad4(w[i], w[j], acc[p & 3]);
+    }
+    const uint32_t S1 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 
-  float Ra[N];
+    float Ra[N];
 #pragma unroll
-  for (int k = 0; k < N; ++k) Ra[k] = 0.0f;
-  if (S1 != 0u) {                                          // flat window: all D = 0 (R18)
-    const float sc = L.kscale / (float)S1;                 // c_E = 1/h_W, or c_L
-    const float bias = -sc * F2P23;                        // exact
+    for (int k = 0; k < N; ++k) Ra[k] = 0.0f;
+    if (S1 != 0u) {                                          // flat window: all D = 0 (R18)
+      const float sc = L.kscale * rcp_approx((float)S1);     // c_E = 1/h_W, or c_L (<= 1 ulp + rounding)
+      const float bias = -sc * F2P23;                        // exact
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
+      for (int i = 0; i < N; ++i) {
 #pragma unroll
-      for (int j = i + 1; j < N; ++j) {
-        const float fb = __uint_as_float(sad4(pk[i], pk[j], F2P23_BITS));   // 2^23 + d1
-        const float zu = fmaf(sc, fb, bias);                                 // c * d1
-        const float v = CRIT == EXPC ? exp_crit<VAR>(zu) : log_crit<VAR>(zu);
-        Ra[i] += v;
-        Ra[j] += v;
+        for (int j = i + 1; j < N; ++j) {
+          const float fb = __uint_as_float(sad4(w[i], w[j], F2P23_BITS));   // 2^23 + d1
+          const float zu = fmaf(sc, fb, bias);                               // c * d1
+          const float v = CRIT == EXPC ? exp_crit<VAR>(zu) : log_crit<VAR>(zu);
+          Ra[i] += v;
+          Ra[j] += v;
+        }
       }
     }
+    argmin_store<N>(L, b, ox, oyb + o, Ra, w);
   }
-  argmin_store<N>(L, b, ox, oy, Ra, pk);
 }
 
 // ============================================================================
