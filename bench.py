@@ -38,7 +38,7 @@ COMBOS = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp"
 # routine itself as compiled for sm_100a.
 FLOPS_PER_PAIR = {
     ("angular", "minimax"): 18, ("exp", "minimax"): 26, ("exp", "poly4"): 18, ("log", "minimax"): 26,
-    ("angular", "exact"): 10 + 22, ("exp", "exact"): 10 + 28, ("log", "exact"): 11 + 30,
+    ("angular", "exact"): 10 + 23, ("exp", "exact"): 10 + 24, ("log", "exact"): 11 + 28,
 }
 NOMINAL_FP32_TFLOPS_AT_MAX = 2 * 128 * 148 * 1.965e9 / 1e12   # 74.4
 

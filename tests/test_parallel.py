@@ -1,0 +1,144 @@
+"""Multi-process (gloo, CPU) tests of the partitioner's host logic: partitions,
+halo bands, the stats all_gather and the stripe gather.  The per-rank compute
+is the CPU oracle (tests may use it), so results must equal the single-process
+oracle bit-exactly for every world size."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1009_0959_b200 import parallel as par
+
+
+def test_shard_range_partitions():
+    for n in [0, 1, 5, 8, 17, 1024]:
+        for world in [1, 2, 3, 4, 8]:
+            parts = [par.shard_range(n, world, r) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            for (a, b), (c, d) in zip(parts, parts[1:]):
+                assert b == c
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_stripe_bounds_halo_and_clamp():
+    H = 4320
+    for w in (3, 5):
+        r = w // 2
+        for world in (1, 2, 4, 8):
+            rows = []
+            for rank in range(world):
+                o0, on, b0, bn = par.stripe_bounds(H, world, rank, w)
+                rows.extend(range(o0, o0 + on))
+                assert b0 == max(0, o0 - r) and b0 + bn == min(H, o0 + on + r)
+            assert rows == list(range(H))
+
+
+# ---------------------------------------------------------------- multi-process
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_filter_batch(imgs, window, crit, var):
+    import oracle
+    x = imgs.numpy()
+    return torch.from_numpy(np.stack([oracle.filter_image(x[b], window, crit, var, want_index=False)[0]
+                                      for b in range(x.shape[0])]))
+
+
+def _numpy_stats(a, b):
+    from oracle import metrics
+    a, b = a.numpy(), b.numpy()
+    out = np.zeros((a.shape[0], 8))
+    for i in range(a.shape[0]):
+        ai, bi = a[i].astype(np.int64), b[i].astype(np.int64)
+        out[i, 0] = (ai != bi).any(-1).sum()
+        out[i, 1] = np.abs(ai - bi).sum()
+        out[i, 2] = ((ai - bi) ** 2).sum()
+        la, lb = metrics.rgb_to_lab(a[i]), metrics.rgb_to_lab(b[i])
+        out[i, 3] = np.linalg.norm(la - lb, axis=-1).sum()
+        out[i, 4] = np.linalg.norm(la, axis=-1).sum()
+        out[i, 5] = np.abs(ai - bi).max()
+    return torch.from_numpy(out)
+
+
+def _oracle_filter_rows(band, band_row0, H, out_row0, out_rows, window, crit, var):
+    """Stripe filter from the band only: rows outside the band are garbage
+    (255) in the scratch image, so a wrong halo shows up as a mismatch."""
+    import oracle
+    b = band.numpy()
+    W = b.shape[1]
+    scratch = np.full((H, W, 3), 255, np.uint8)
+    scratch[band_row0:band_row0 + b.shape[0]] = b
+    ys, xs = np.meshgrid(np.arange(out_row0, out_row0 + out_rows), np.arange(W), indexing="ij")
+    o, _, _ = oracle.filter_pixels(scratch, window, crit, var, ys.ravel(), xs.ravel(), want_agg=False)
+    return torch.from_numpy(o.reshape(out_rows, W, 3))
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import vfsynth
+        # ---- batch sharding (C4-like, small)
+        spec = vfsynth.ImageSpec("t", 24, 40, 5, (3,), 4, False, "uncorrelated", None,
+                                 p_choices=(0.05, 0.3), seed=99)
+        B = spec.batch
+        lo, hi = par.shard_range(B, world, rank)
+        local = torch.from_numpy(vfsynth.make_batch(spec, ids=range(lo, hi)))
+        combos = [("angular", "exact"), ("angular", "minimax"), ("log", "minimax")]
+        outs, stats = par.run_batch_sharded(local, B, 3, combos, filter_fn=_oracle_filter_batch,
+                                            stats_fn=_numpy_stats)
+        # ---- stripes (C5-like, small): band generated locally, row-addressable
+        spec5 = vfsynth.ImageSpec("t5", 37, 29, 1, (3, 5), 4, False, "correlated", 0.15, seed=7)
+        res = {}
+        for w in (3, 5):
+            o0, on, b0, bn = par.stripe_bounds(spec5.H, world, rank, w)
+            band = torch.from_numpy(vfsynth.make_image(spec5, 0, b0, b0 + bn)[1])
+            stripe, full = par.run_stripes(band, spec5.H, w, "angular", "minimax", filter_fn=_oracle_filter_rows)
+            res[w] = full.numpy()
+        q.put((rank, {k: v.numpy() for k, v in stats.items()}, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multiprocess_batch_and_stripes(world):
+    import oracle
+    import vfsynth
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # single-process references
+    spec = vfsynth.ImageSpec("t", 24, 40, 5, (3,), 4, False, "uncorrelated", None, p_choices=(0.05, 0.3), seed=99)
+    full_b = torch.from_numpy(vfsynth.make_batch(spec))
+    combos = [("angular", "exact"), ("angular", "minimax"), ("log", "minimax")]
+    ref_out = {c: _oracle_filter_batch(full_b, 3, *c) for c in combos}
+    ref_stats = {c: _numpy_stats(ref_out[combos[0]], ref_out[c]).numpy() for c in combos}
+    spec5 = vfsynth.ImageSpec("t5", 37, 29, 1, (3, 5), 4, False, "correlated", 0.15, seed=7)
+    img5 = vfsynth.make_image(spec5, 0)[1]
+    for rank, stats, res in results:
+        for c in combos:
+            assert np.array_equal(stats[c], ref_stats[c]), (rank, c)
+        for w in (3, 5):
+            ref = oracle.filter_image(img5, w, "angular", "minimax", want_index=False)[0]
+            assert np.array_equal(res[w], ref), (rank, w)
+    # a filter against itself: no differing pixel, zero error (column 4 is the NCD denominator)
+    z = ref_stats[("angular", "exact")]
+    assert np.all(z[:, [0, 1, 2, 3, 5]] == 0) and np.all(z[:, 4] > 0)
