@@ -222,7 +222,8 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
     const uint8_t* q = pixel_ptr(L, in, oy0 - R + py, ox0 - R + px);
     const uint32_t r = q[0], g = q[1], bl = q[2];
     const float nn = (float)(r * r + g * g + bl * bl);          // exact
-    const float nrm = sqrtf(nn);
+    float nrm;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(nrm) : "f"(nn));   // MUFU.SQRT, ~1 ulp
     my_pk[k] = pack_rgb(r, g, bl);
     my_nn[k] = nn;
     my_nrm[k] = nrm;
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
 #pragma unroll
   for (int k = 0; k < OPT; ++k)
 #pragma unroll
-    for (int i = 0; i < N; ++i) Ra[k][i] = 0.0f;
+    for (int i = 0; i < N; ++i) Ra[k][i] = -0.0f;   // -0 + v == v: the first add folds away
 
   shared_groups<WIN, VAR, GD, OPT>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, Ra, tid,
                                    blk_zero);

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
 
     float Ra[N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) Ra[k] = 0.0f;
+    for (int k = 0; k < N; ++k) Ra[k] = (S1 != 0u) ? -0.0f : 0.0f;   // -0 + v == v: first add folds
     if (S1 != 0u) {                                          // flat window: all D = 0 (R18)
       const float sc = L.kscale * rcp_approx((float)S1);     // c_E = 1/h_W, or c_L (<= 1 ulp + rounding)
       const float bias = -sc * F2P23;                        // exact
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(TX * TY) vf_angular_window_kernel(const Launch
   }
   float Ra[N];
 #pragma unroll
-  for (int k = 0; k < N; ++k) Ra[k] = 0.0f;
+  for (int k = 0; k < N; ++k) Ra[k] = -0.0f;              // -0 + v == v: the first add folds away
 #pragma unroll
   for (int i = 0; i < N; ++i) {
 #pragma unroll
