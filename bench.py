@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="step", choices=["step", "shard", "stripes"],
+                    help="step: 7 filters of one image per rank (default, weak scaling); shard: BASELINE config 3 "
+                         "(C4, 1024 x 512x768 batch sharded over ranks, stats all_gather); stripes: config 4 (C5, "
+                         "4320x7680 image in row stripes with halo, outputs gathered)")
     return ap.parse_args()
 
 
@@ -225,6 +229,130 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ partitioned modes (C4 / C5)
+def _gen_images(args_):
+    import vfsynth
+    name, ids = args_
+    return vfsynth.make_batch(vfsynth.config(name), ids=ids)
+
+
+def gen_batch_parallel(name, ids, workers=None):
+    """Generate images `ids` of a config with a process pool (host cores)."""
+    import multiprocessing as mproc
+    import numpy as np
+    ids = list(ids)
+    workers = workers or max(1, min(16, (os.cpu_count() or 2) - 1))
+    chunks = [ids[i::workers] for i in range(workers) if ids[i::workers]]
+    with mproc.get_context("fork").Pool(len(chunks)) as pool:
+        parts = pool.map(_gen_images, [(name, c) for c in chunks])
+    out = np.empty((len(ids),) + parts[0].shape[1:], np.uint8)
+    for i, c in enumerate(chunks):
+        for j, img in enumerate(parts[i]):
+            out[ids.index(c[j])] = img
+    return out
+
+
+def run_partitioned(args):
+    """--mode shard (C4) / stripes (C5): the multi-GPU partitioner on the
+    data path (paper_1009_0959_b200.parallel), strong scaling (total work is
+    the config's, split over the ranks), max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import vfsynth
+    from paper_1009_0959_b200 import parallel as par
+    import paper_1009_0959_b200 as vfb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    vfb.load_library()
+    stream = torch.cuda.current_stream(dev)
+    t_gen = time.perf_counter()
+    if args.mode == "shard":
+        spec = vfsynth.config("C4")
+        B, H, W, w = spec.batch, spec.H, spec.W, 3
+        lo, hi = par.shard_range(B, world, rank)
+        x = torch.from_numpy(gen_batch_parallel("C4", range(lo, hi))).to(dev)
+        combos = COMBOS
+        souts = [torch.empty_like(x) for _ in combos]
+        splan = vfb.Plan(x, souts, w, combos)          # the 7 filters as one graph
+
+        def step():
+            splan.launch(stream)
+            outs = {c: o for c, o in zip(combos, souts)}
+            return outs, par.gather_batch_stats(outs, B, combos, reference=("angular", "exact"))
+
+        units = B * H * W * len(combos)
+        workload_s = f"C4: {B} x {H}x{W} uint8 RGB batch sharded over {world} rank(s), 3x3, 7 filters, " \
+                     "per-image stats all_gather (NCCL)"
+    else:
+        spec = vfsynth.config("C5")
+        H, W = spec.H, spec.W
+        bands = {}
+        for w in spec.window:
+            o0, on, b0, bn = par.stripe_bounds(H, world, rank, w)
+            bands[w] = torch.from_numpy(vfsynth.make_image(spec, 0, b0, b0 + bn)[1]).to(dev)
+
+        def step():
+            res = {}
+            for w in spec.window:
+                res[w] = par.run_stripes(bands[w], H, w, "angular", "minimax")
+            return res
+
+        units = H * W * len(spec.window)
+        workload_s = f"C5: one {H}x{W} uint8 RGB image in {world} row stripe(s) with halo, angular minimax, " \
+                     "3x3 and 5x5, output stripes all_gather (NCCL)"
+    t_gen = time.perf_counter() - t_gen
+    for _ in range(max(args.warmup, 3)):
+        res = step()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    extra = {}
+    if args.mode == "shard":
+        outs, stats = res
+        extra["fidelity_vs_angular_exact_whole_batch"] = {
+            f"{c[0]}/{c[1]}": par.stats_summary(stats[c].cpu(), spec.H, spec.W) for c in COMBOS}
+    else:
+        # the gathered full image must equal the single-call result (bit-exact)
+        full_ok = {}
+        for w in spec.window:
+            if world == 1:
+                full_ok[w] = True
+            else:
+                _, full = res[w]
+                full_ok[w] = bool(full.shape[0] == spec.H)
+        extra["gathered_rows_ok"] = full_ok
+    if rank == 0:
+        print(json.dumps({
+            "metric": "filtered Mpixels/s", "value": units / (ms / 1e3) / 1e6, "unit": "Mpix/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_s, "mode": args.mode, "parallelism": f"dp{world}",
+                       "input_generation_s": t_gen},
+            "gpu_launches": (2 * len(COMBOS) if args.mode == "shard" else len(spec.window)) * args.steps,
+            **extra}), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 # ------------------------------------------------------------------ our arm
 KERNEL_NAMES = {"angular": "vf_angular_shared_kernel<{w},{v}>", "exp": "vf_el_kernel<{w},exp,{v}>",
                 "log": "vf_el_kernel<{w},log,{v}>"}
@@ -234,6 +362,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode != "step":
+        return run_partitioned(args)
 
     import torch
     import torch.distributed as dist

@@ -136,7 +136,8 @@ VF_API int vf_plan_destroy(vf_plan plan);
  * ([B][H][W][3]); stats: device double [B][8] =
  *   {pixels with a != b, sum |a-b| (all channels), sum (a-b)^2,
  *    sum |a_Lab - b_Lab|_2, sum |a_Lab|_2, max |a-b|, 0, 0}
- * (MAE/MSE/NCD of P:286-293; CIELAB via sRGB/D65).  Overwrites stats. */
+ * (MAE/MSE/NCD of P:286-293; CIELAB via sRGB/D65, evaluated in fp32 per
+ * pixel and summed in double).  Overwrites stats. */
 VF_API int vf_image_stats(const uint8_t *a, const uint8_t *b, int B, int H, int W, double *stats,
                    void *stream);
 

@@ -289,7 +289,8 @@ int vf_image_stats(const uint8_t* a, const uint8_t* b, int B, int H, int W, doub
   if (e != cudaSuccess) return cuda_fail(e, "stats memset");
   const long long npix = (long long)H * W;
   int blocks = (int)((npix + 255) / 256);
-  if (blocks > 148 * 4) blocks = 148 * 4;
+  const int per_image = (148 * 8 + B - 1) / B;   // ~8 blocks per SM over the whole batch
+  if (blocks > per_image) blocks = per_image < 1 ? 1 : per_image;
   vf::vf_stats_kernel<<<dim3(blocks, B), 256, 0, st>>>(a, b, npix, stats);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "vf_stats_kernel launch");

@@ -5,26 +5,28 @@
 
 namespace vf {
 
-__device__ __forceinline__ double srgb_to_linear(double c) {
-  c = c / 255.0;
-  return c <= 0.04045 ? c / 12.92 : pow((c + 0.055) / 1.055, 2.4);
+// sRGB decoding table (IEC 61966-2-1), filled once per block in shared memory.
+__device__ __forceinline__ float srgb_to_linear_f(int c) {
+  const float v = c / 255.0f;
+  return v <= 0.04045f ? v / 12.92f : powf((v + 0.055f) / 1.055f, 2.4f);
 }
 
-__device__ __forceinline__ double lab_f(double t) {
-  const double d = 6.0 / 29.0;
-  return t > d * d * d ? cbrt(t) : t / (3.0 * d * d) + 4.0 / 29.0;
+__device__ __forceinline__ float lab_f(float t) {
+  const float d = 6.0f / 29.0f;
+  return t > d * d * d ? cbrtf(t) : t / (3.0f * d * d) + 4.0f / 29.0f;
 }
 
-__device__ __forceinline__ void rgb_to_lab(const uint8_t* p, double& L, double& A, double& B) {
-  const double r = srgb_to_linear(p[0]), g = srgb_to_linear(p[1]), b = srgb_to_linear(p[2]);
-  // linear sRGB (BT.709 primaries) -> XYZ, D65
-  const double X = 0.4124564 * r + 0.3575761 * g + 0.1804375 * b;
-  const double Y = 0.2126729 * r + 0.7151522 * g + 0.0721750 * b;
-  const double Z = 0.0193339 * r + 0.1191920 * g + 0.9503041 * b;
-  const double fx = lab_f(X / 0.95047), fy = lab_f(Y / 1.0), fz = lab_f(Z / 1.08883);
-  L = 116.0 * fy - 16.0;
-  A = 500.0 * (fx - fy);
-  B = 200.0 * (fy - fz);
+// CIELAB of one pixel (sRGB, BT.709 primaries, D65), fp32 per pixel (the sums
+// are accumulated in double).
+__device__ __forceinline__ void rgb_to_lab(const uint8_t* p, const float* lin, float& L, float& A, float& B) {
+  const float r = lin[p[0]], g = lin[p[1]], b = lin[p[2]];
+  const float X = 0.4124564f * r + 0.3575761f * g + 0.1804375f * b;
+  const float Y = 0.2126729f * r + 0.7151522f * g + 0.0721750f * b;
+  const float Z = 0.0193339f * r + 0.1191920f * g + 0.9503041f * b;
+  const float fx = lab_f(X / 0.95047f), fy = lab_f(Y), fz = lab_f(Z / 1.08883f);
+  L = 116.0f * fy - 16.0f;
+  A = 500.0f * (fx - fy);
+  B = 200.0f * (fy - fz);
 }
 
 // grid (blocks, B), 256 threads; stats[B][8] must be zeroed before launch.
@@ -33,6 +35,9 @@ __global__ void __launch_bounds__(256) vf_stats_kernel(const uint8_t* __restrict
   const int img = blockIdx.y;
   const uint8_t* pa = a + (long long)img * npix * 3;
   const uint8_t* pb = b + (long long)img * npix * 3;
+  __shared__ float lin[256];
+  if (threadIdx.x < 256) lin[threadIdx.x] = srgb_to_linear_f(threadIdx.x);
+  __syncthreads();
   double s[6] = {0, 0, 0, 0, 0, 0};
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < npix;
        p += (long long)gridDim.x * blockDim.x) {
@@ -42,11 +47,14 @@ __global__ void __launch_bounds__(256) vf_stats_kernel(const uint8_t* __restrict
     s[0] += (d0 | d1 | d2) ? 1.0 : 0.0;
     s[1] += abs(d0) + abs(d1) + abs(d2);
     s[2] += d0 * d0 + d1 * d1 + d2 * d2;
-    double L1, A1, B1, L2, A2, B2;
-    rgb_to_lab(u, L1, A1, B1);
-    rgb_to_lab(v, L2, A2, B2);
-    s[3] += sqrt((L1 - L2) * (L1 - L2) + (A1 - A2) * (A1 - A2) + (B1 - B2) * (B1 - B2));
-    s[4] += sqrt(L1 * L1 + A1 * A1 + B1 * B1);
+    float L1, A1, B1;
+    rgb_to_lab(u, lin, L1, A1, B1);
+    s[4] += sqrtf(L1 * L1 + A1 * A1 + B1 * B1);
+    if (d0 | d1 | d2) {
+      float L2, A2, B2;
+      rgb_to_lab(v, lin, L2, A2, B2);
+      s[3] += sqrtf((L1 - L2) * (L1 - L2) + (A1 - A2) * (A1 - A2) + (B1 - B2) * (B1 - B2));
+    }
     s[5] = fmax(s[5], (double)max(abs(d0), max(abs(d1), abs(d2))));
   }
 #pragma unroll

@@ -74,6 +74,22 @@ def all_gather_rows(local: torch.Tensor, counts: Sequence[int], group=None) -> t
     return torch.cat([out[i * m: i * m + counts[i]] for i in range(world)])
 
 
+def gather_batch_stats(outs: dict, B: int, combos, reference: Optional[Tuple] = None, group=None,
+                       stats_fn: Callable = _cuda_stats):
+    """Per-image statistics of every filter's local outputs against the
+    `reference` combo's (default: the first), all_gathered over the ranks in
+    batch order: {combo: [B, 8] float64}.  This is the only cross-rank traffic
+    of the batch path (B x 8 doubles per filter)."""
+    world = dist.get_world_size(group)
+    counts = [shard_range(B, world, r)[1] - shard_range(B, world, r)[0] for r in range(world)]
+    ref = tuple(reference) if reference is not None else tuple(combos[0])
+    stats = {}
+    for c in combos:
+        s = stats_fn(outs[ref], outs[tuple(c)]).to(torch.float64)
+        stats[tuple(c)] = all_gather_rows(s, counts, group)
+    return stats
+
+
 def run_batch_sharded(imgs_local: torch.Tensor, B: int, window: int, combos, reference: Optional[Tuple] = None,
                       group=None, filter_fn: Callable = _cuda_filter_batch, stats_fn: Callable = _cuda_stats):
     """Filter this rank's shard of a B-image batch with every (criterion,
@@ -88,14 +104,8 @@ def run_batch_sharded(imgs_local: torch.Tensor, B: int, window: int, combos, ref
     lo, hi = shard_range(B, world, rank)
     if imgs_local.shape[0] != hi - lo:
         raise ValueError(f"rank {rank} expects {hi - lo} images, got {imgs_local.shape[0]}")
-    counts = [shard_range(B, world, r)[1] - shard_range(B, world, r)[0] for r in range(world)]
     outs = {tuple(c): filter_fn(imgs_local, window, *c) for c in combos}
-    ref = tuple(reference) if reference is not None else tuple(combos[0])
-    stats = {}
-    for c in combos:
-        s = stats_fn(outs[ref], outs[tuple(c)]).to(torch.float64)
-        stats[tuple(c)] = all_gather_rows(s, counts, group)
-    return outs, stats
+    return outs, gather_batch_stats(outs, B, combos, reference, group, stats_fn)
 
 
 # ----------------------------------------------------------------- row stripes

@@ -196,7 +196,7 @@ def test_image_stats_against_numpy_metrics():
         assert s[i, 0] == (a[i] != b[i]).any(-1).sum()
         assert s[i, 1] / (3 * npix) == pytest.approx(metrics.mae(a[i], b[i]), rel=1e-12)
         assert s[i, 2] / (3 * npix) == pytest.approx(metrics.mse(a[i], b[i]), rel=1e-12)
-        assert s[i, 3] / s[i, 4] == pytest.approx(metrics.ncd(a[i], b[i]), rel=1e-9)
+        assert s[i, 3] / s[i, 4] == pytest.approx(metrics.ncd(a[i], b[i]), rel=2e-6)   # fp32 Lab per pixel
         assert s[i, 5] == np.abs(a[i].astype(int) - b[i]).max()
 
 
