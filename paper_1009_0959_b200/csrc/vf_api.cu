@@ -43,8 +43,15 @@ using vf::Launch;
 struct KernelDesc {
   const void* fn;
   dim3 grid, block;
+  size_t smem;   // dynamic shared memory bytes
   Launch L;
 };
+
+// One-time per-process kernel attribute setup (thread-safe).
+cudaError_t ensure_attributes() {
+  static cudaError_t status = vf::shared_set_attributes();
+  return status;
+}
 
 template <int WIN>
 const void* window_kernel(int crit, int var) {
@@ -92,11 +99,15 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
     kd->fn = vf::shared_kernel_fn(window, var);
     kd->grid = vf::shared_grid(L, B, window);
     kd->block = dim3(vf::shared::NTHR);
+    kd->smem = vf::shared_smem_bytes(window);
+    const cudaError_t e = ensure_attributes();
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   } else {
     kd->fn = window == 3 ? window_kernel<3>(crit, var) : window_kernel<5>(crit, var);
     const int th = crit == VF_ANGULAR ? vf::TY : vf::TY * vf::el_opt(window);
     kd->grid = dim3((W + vf::TX - 1) / vf::TX, (out_rows + th - 1) / th, B);
     kd->block = dim3(vf::TX, vf::TY);
+    kd->smem = 0;
   }
   if (kd->grid.y > 65535 || kd->grid.z > 65535)
     return fail(VF_EINVAL, "grid too large (%lld blocks in y or z)",
@@ -106,7 +117,7 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
 
 int launch_desc(KernelDesc& kd, cudaStream_t st) {
   void* args[] = {&kd.L};
-  cudaError_t e = cudaLaunchKernel(kd.fn, kd.grid, kd.block, args, 0, st);
+  cudaError_t e = cudaLaunchKernel(kd.fn, kd.grid, kd.block, args, kd.smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return VF_OK;
 }
@@ -245,7 +256,7 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
     kp.func = (void*)kd.fn;
     kp.gridDim = kd.grid;
     kp.blockDim = kd.block;
-    kp.sharedMemBytes = 0;
+    kp.sharedMemBytes = (unsigned)kd.smem;
     kp.kernelParams = args;
     cudaGraphNode_t kn;
     e = cudaGraphAddKernelNode(&kn, p->graph, h2d ? &h2d : nullptr, h2d ? 1 : 0, &kp);

@@ -70,8 +70,7 @@ __device__ __noinline__ bool angular_fixup(uint32_t pa, float nna, float nrma, u
 // Per-block shared-memory state of the pair-sharing kernel.
 template <int GD>
 struct SharedSmem {
-  uint32_t pk[shared::NP + shared::PAD];
-  float2 nm[shared::NP + shared::PAD];   // (|x|^2, |x|)
+  uint4 px[shared::NP + shared::PAD];    // (packed RGB0, |x|^2 bits, |x| bits, 0): one LDS.128 per neighbour
   float M[GD][shared::NP];
 };
 
@@ -101,8 +100,9 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD>& sm, const uint32_t 
     for (int k = 0; k < PPT; ++k) {
       const int p = tid + NTHR * k;
       const int q = p + off;                                  // in bounds (PAD); garbage if outside P
-      const uint32_t qk = sm.pk[q];
-      const float2 qn = sm.nm[q];
+      const uint4 qv = sm.px[q];
+      const uint32_t qk = qv.x;
+      const float2 qn = make_float2(__uint_as_float(qv.y), __uint_as_float(qv.z));
       const float D = __uint_as_float(__dp4a(my_pk[k], qk, F2P23_BITS)) - F2P23;   // exact dot
       const float Ph = __fmul_rn(my_nn[k], qn.x);
       const float Pl = fmaf(my_nn[k], qn.x, -Ph);
@@ -118,11 +118,10 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD>& sm, const uint32_t 
       sm.M[dl][p] = v;
       // cos < 0.5 <=> tau > 1/sqrt2: flag a superset (margin 2^-10 >> the
       // ~5e-7 relative error of tau) for the exact decision below.  Offsets
-      // reaching below the region read the zero padding: never flag those.
+      // reaching below the region read the zero padding: tau = 0, never flagged.
       const bool rare = tau > 0.70641626f;                    // (1/sqrt2) (1 - 2^-10)
-      const bool valid = (k < PPT - 1) || (q < NP);
       const int bit = dl * PPT + k;                           // compile-time after unrolling
-      if (rare && valid) flags[bit / 32] |= 1u << (bit % 32);
+      if (rare) flags[bit / 32] |= 1u << (bit % 32);
     }
   }
   // rare pairs: exact branch decision (re-evaluated, then overwritten)
@@ -135,9 +134,11 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD>& sm, const uint32_t 
       const int d = G * GD + dl;
       const int p = tid + NTHR * k;
       const int q = p + delta_dy(R, d) * PW + delta_dx(R, d);
-      const float2 pn = sm.nm[p], qn = sm.nm[q];
+      const uint4 pv = sm.px[p], qv = sm.px[q];
       float v;
-      if (angular_fixup<VAR>(sm.pk[p], pn.x, pn.y, sm.pk[q], qn.x, qn.y, &v)) sm.M[dl][p] = v;
+      if (angular_fixup<VAR>(pv.x, __uint_as_float(pv.y), __uint_as_float(pv.z), qv.x, __uint_as_float(qv.y),
+                             __uint_as_float(qv.z), &v))
+        sm.M[dl][p] = v;
     }
   }
   // zero vectors: block-uniform slow path, only in blocks that hold
@@ -202,7 +203,8 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
   constexpr int NG = ND / GD;
   constexpr int OPT = (TH + 7) / 8;         // outputs per thread (rows ty, ty+8, ty+16)
   static_assert(ND % GD == 0, "groups must tile the offsets");
-  __shared__ SharedSmem<GD> sm;
+  extern __shared__ __align__(16) unsigned char smem_raw[];   // sizeof(SharedSmem<GD>), dynamic (> 48 KB)
+  SharedSmem<GD>& sm = *reinterpret_cast<SharedSmem<GD>*>(smem_raw);
 
   const int b = blockIdx.z;
   const int ox0 = blockIdx.x * TW;                        // output tile origin (global)
@@ -228,10 +230,9 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
     my_nn[k] = nn;
     my_nrm[k] = nrm;
     has_zero |= (nn == 0.0f);
-    sm.pk[p] = my_pk[k];
-    sm.nm[p] = make_float2(nn, nrm);
+    sm.px[p] = make_uint4(my_pk[k], __float_as_uint(nn), __float_as_uint(nrm), 0u);
   }
-  if (tid < PAD) { sm.pk[NP + tid] = 0u; sm.nm[NP + tid] = make_float2(0.0f, 0.0f); }
+  if (tid < PAD) sm.px[NP + tid] = make_uint4(0u, 0u, 0u, 0u);
   const bool blk_zero = __syncthreads_or(has_zero) != 0;       // staging barrier
 
   float Ra[OPT][N];
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
       uint32_t pk[N];
       const int base = oy * PW + tx;
 #pragma unroll
-      for (int i = 0; i < N; ++i) pk[i] = sm.pk[base + (i / WIN) * PW + (i % WIN)];
+      for (int i = 0; i < N; ++i) pk[i] = sm.px[base + (i / WIN) * PW + (i % WIN)].x;
       argmin_store<N>(L, b, gx, gy, Ra[k], pk);
     }
   }
@@ -263,6 +264,22 @@ inline const void* shared_kernel_fn(int window, int var) {
   if (window == 3) return var == EXACT ? (const void*)vf_angular_shared_kernel<3, EXACT>
                                        : (const void*)vf_angular_shared_kernel<3, MINIMAX>;
   return var == EXACT ? (const void*)vf_angular_shared_kernel<5, EXACT> : (const void*)vf_angular_shared_kernel<5, MINIMAX>;
+}
+
+inline size_t shared_smem_bytes(int window) {
+  return window == 3 ? sizeof(SharedSmem<12>) : sizeof(SharedSmem<10>);
+}
+
+// Opt the kernels in to > 48 KB of dynamic shared memory (once per process).
+inline cudaError_t shared_set_attributes() {
+  const int ws[2] = {3, 5};
+  for (int w : ws)
+    for (int v = 0; v < 2; ++v) {
+      cudaError_t e = cudaFuncSetAttribute(shared_kernel_fn(w, v), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)shared_smem_bytes(w));
+      if (e != cudaSuccess) return e;
+    }
+  return cudaSuccess;
 }
 
 inline dim3 shared_grid(const Launch& L, int B, int window) {

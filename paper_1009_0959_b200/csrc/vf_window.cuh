@@ -75,6 +75,97 @@ __device__ __forceinline__ void argmin_store(const Launch& L, int b, int ox, int
 // each distance already biased into a float (2^23 + d1) and turns it into the
 // scaled argument with one FFMA.
 // ============================================================================
+// One exp/log window with kept biased distances (3x3).  SHIFTED: the kept
+// values hold the previous (one row higher) window's pairs; pairs of rows
+// 0..1 of this window are pairs of rows 1..2 of the previous one.
+template <int WIN, int CRIT, int VAR, bool SHIFTED>
+__device__ __forceinline__ void el_window(const Launch& L, int b, int ox, int oy, const uint32_t* w,
+                                          uint32_t (&keep)[WIN * WIN * (WIN * WIN - 1) / 2]) {
+  constexpr int N = WIN * WIN;
+  constexpr int NPR = N * (N - 1) / 2;
+  if (SHIFTED) {
+    uint32_t nk[NPR];
+#pragma unroll
+    for (int p = 0; p < NPR; ++p) nk[p] = keep[p];
+#pragma unroll
+    for (int i = 0, p = 0; i < N; ++i)
+#pragma unroll
+      for (int j = i + 1; j < N; ++j, ++p)
+        if (j < N - WIN) {
+          const int a = i + WIN, c = j + WIN;
+          keep[p] = nk[a * N - a * (a + 1) / 2 + (c - a - 1)];
+        }
+  }
+  // a3: S1 = sum - NPR * 0x4B000000 (mod 2^32; exact integer)
+  uint32_t acc[3] = {0u, 0u, 0u};
+#pragma unroll
+  for (int i = 0, p = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = i + 1; j < N; ++j, ++p) {
+      if (!SHIFTED || j >= N - WIN) keep[p] = sad4(w[i], w[j], F2P23_BITS);
+      acc[p % 3] += keep[p];
+    }
+  }
+  const uint32_t S1 = (acc[0] + acc[1]) + acc[2] - (uint32_t)(NPR * F2P23_BITS);
+  float Ra[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) Ra[k] = (S1 != 0u) ? -0.0f : 0.0f;   // -0 + v == v: first add folds
+  if (S1 != 0u) {                                                   // flat window: all D = 0 (R18)
+    const float sc = L.kscale * rcp_approx((float)S1);              // c_E = 1/h_W, or c_L
+    const float bias = -sc * F2P23;                                 // exact
+#pragma unroll
+    for (int i = 0, p = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = i + 1; j < N; ++j, ++p) {
+        const float zu = fmaf(sc, __uint_as_float(keep[p]), bias);  // c * d1, one rounding
+        const float v = CRIT == EXPC ? exp_crit<VAR>(zu) : log_crit<VAR>(zu);
+        Ra[i] += v;
+        Ra[j] += v;
+      }
+    }
+  }
+  uint32_t ww[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) ww[k] = w[k];
+  argmin_store<N>(L, b, ox, oy, Ra, ww);
+}
+
+// One exp/log window recomputing the distances in pass 2 (5x5: 300 pairs do
+// not fit in registers).
+template <int WIN, int CRIT, int VAR>
+__device__ __forceinline__ void el_window_nokeep(const Launch& L, int b, int ox, int oy, const uint32_t* w) {
+  constexpr int N = WIN * WIN;
+  uint32_t acc[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int i = 0, p = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = i + 1; j < N; ++j, ++p) acc[p & 3] = sad4(w[i], w[j], acc[p & 3]);
+  }
+  const uint32_t S1 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  float Ra[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) Ra[k] = (S1 != 0u) ? -0.0f : 0.0f;
+  if (S1 != 0u) {
+    const float sc = L.kscale * rcp_approx((float)S1);
+    const float bias = -sc * F2P23;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = i + 1; j < N; ++j) {
+        const float fb = __uint_as_float(sad4(w[i], w[j], F2P23_BITS));   // 2^23 + d1
+        const float zu = fmaf(sc, fb, bias);                               // c * d1
+        const float v = CRIT == EXPC ? exp_crit<VAR>(zu) : log_crit<VAR>(zu);
+        Ra[i] += v;
+        Ra[j] += v;
+      }
+    }
+  }
+  uint32_t ww[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) ww[k] = w[k];
+  argmin_store<N>(L, b, ox, oy, Ra, ww);
+}
+
 template <int WIN, int CRIT, int VAR>
 __global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
   constexpr int R = WIN / 2;
@@ -111,40 +202,22 @@ __global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
 #pragma unroll
   for (int k = 0; k < LR * WIN; ++k) pk[k] = s_pk[(OPT * ty + k / WIN) * SW + tx + k % WIN];
 
+  const int rows_here = min(OPT, L.out_row0 + L.out_rows - oyb);   // >= 1
+  if (N <= 9 && VAR == EXACT) {
+    // 3x3 exact: the biased L1 distances 2^23 + d1 of a window's 36 pairs are
+    // computed once (one VABSDIFF4 each) and kept in registers for both passes;
+    // the 15 pairs two vertically adjacent windows share are computed once per
+    // thread (measured: -10% time for the libm variants, no gain for the
+    // minimax ones, whose occupancy it lowers).
+    uint32_t keep[N * (N - 1) / 2];
+    el_window<WIN, CRIT, VAR, false>(L, b, ox, oyb, pk, keep);
 #pragma unroll
-  for (int o = 0; o < OPT; ++o) {
-    if (o > 0 && oyb + o >= L.out_row0 + L.out_rows) break;
-    uint32_t w[N];
+    for (int o = 1; o < OPT; ++o)
+      if (o < rows_here) el_window<WIN, CRIT, VAR, true>(L, b, ox, oyb + o, pk + o * WIN, keep);
+  } else {
 #pragma unroll
-    for (int k = 0; k < N; ++k) w[k] = pk[o * WIN + k];
-    // a3: S1 = sum_{i<j} d1_ij, exact, in 4 independent integer chains
-    uint32_t acc[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-    for (int i = 0, p = 0; i < N; ++i) {
-#pragma unroll
-      for (int j = i + 1; j < N; ++j, ++p) acc[p & 3] = sad4(w[i], w[j], acc[p & 3]);
-    }
-    const uint32_t S1 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-
-    float Ra[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) Ra[k] = (S1 != 0u) ? -0.0f : 0.0f;   // -0 + v == v: first add folds
-    if (S1 != 0u) {                                          // flat window: all D = 0 (R18)
-      const float sc = L.kscale * rcp_approx((float)S1);     // c_E = 1/h_W, or c_L (<= 1 ulp + rounding)
-      const float bias = -sc * F2P23;                        // exact
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-#pragma unroll
-        for (int j = i + 1; j < N; ++j) {
-          const float fb = __uint_as_float(sad4(w[i], w[j], F2P23_BITS));   // 2^23 + d1
-          const float zu = fmaf(sc, fb, bias);                               // c * d1
-          const float v = CRIT == EXPC ? exp_crit<VAR>(zu) : log_crit<VAR>(zu);
-          Ra[i] += v;
-          Ra[j] += v;
-        }
-      }
-    }
-    argmin_store<N>(L, b, ox, oyb + o, Ra, w);
+    for (int o = 0; o < OPT; ++o)
+      if (o < rows_here) el_window_nokeep<WIN, CRIT, VAR>(L, b, ox, oyb + o, pk + o * WIN);
   }
 }
 
