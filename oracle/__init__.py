@@ -21,7 +21,9 @@ LIB = os.path.join(HERE, "liboracle.so")
 
 ANGULAR, EXP, LOG = 0, 1, 2
 EXACT, MINIMAX, MINIMAX_POLY4 = 0, 1, 2
+AMNFE, AMNFG, EVMF = 3, 4, 5
 CRITERIA = {"angular": ANGULAR, "exp": EXP, "log": LOG}
+FILTERS = {"amnfe": AMNFE, "amnfg": AMNFG, "evmf": EVMF}
 VARIANTS = {"exact": EXACT, "minimax": MINIMAX, "poly4": MINIMAX_POLY4}
 
 FN = dict(arccos_exact=0, arccos_mm=1, p_arccos=2, p_arcsin=3, exp_exact=4,
@@ -64,6 +66,10 @@ def lib():
         L.oracle_eval.restype = I
         L.oracle_coeffs.argtypes = [I, P]
         L.oracle_coeffs.restype = I
+        L.oracle_paper_window.argtypes = [P, I, I, I, P, P]
+        L.oracle_paper_window.restype = I
+        L.oracle_paper_filter.argtypes = [P, I, I, I, I, I, P, P, ctypes.c_int64, P, P, P, I]
+        L.oracle_paper_filter.restype = I
         L.oracle_max_threads.argtypes = []
         L.oracle_max_threads.restype = I
         _lib = L
@@ -157,6 +163,50 @@ def coeffs(table: str) -> np.ndarray:
     out = np.zeros(8, np.float64)
     m = lib().oracle_coeffs(TABLES[table], _ptr(out))
     return out[:m].copy()
+
+
+def _fv(f):
+    return FILTERS[f] if isinstance(f, str) else int(f)
+
+
+def paper_window(samples, filt, variant):
+    """AMNF (Eq. 8) / EVMF (Eq. 9) on one window of n samples (uint8 [n, 3]).
+    Returns (selected index, out[3], aux[n + 3]) -- see vf_oracle.c."""
+    s = np.ascontiguousarray(samples, dtype=np.uint8).reshape(-1, 3)
+    n = s.shape[0]
+    out = np.zeros(3, np.uint8)
+    aux = np.zeros(n + 3, np.float64)
+    k = lib().oracle_paper_window(_ptr(s), n, _fv(filt), _vv(variant), _ptr(out), _ptr(aux))
+    if k < 0:
+        raise ValueError("oracle_paper_window: invalid arguments")
+    return k, out, aux
+
+
+def paper_filter(img, window: int, filt, variant, ys=None, xs=None, want_aux=True, nthreads: int = 0):
+    """AMNF / EVMF over a full image (ys = xs = None: outputs [H, W, ...]) or at
+    sampled pixels ([npix, ...]).  Returns (out, index, aux | None)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    H, W = img.shape[:2]
+    n = window * window
+    if ys is None:
+        npix = H * W
+        yp = xp = None
+    else:
+        yp = np.ascontiguousarray(ys, dtype=np.int32)
+        xp = np.ascontiguousarray(xs, dtype=np.int32)
+        npix = yp.shape[0]
+    out = np.zeros((npix, 3), np.uint8)
+    idx = np.zeros((npix,), np.uint8)
+    aux = np.zeros((npix, n + 3), np.float64) if want_aux else None
+    rc = lib().oracle_paper_filter(_ptr(img), H, W, window, _fv(filt), _vv(variant), _ptr(yp), _ptr(xp), npix,
+                                   _ptr(out), _ptr(idx), _ptr(aux), nthreads)
+    if rc != 0:
+        raise ValueError("oracle_paper_filter: invalid arguments")
+    if ys is None:
+        out = out.reshape(H, W, 3)
+        idx = idx.reshape(H, W)
+        aux = None if aux is None else aux.reshape(H, W, n + 3)
+    return out, idx, aux
 
 
 def max_threads() -> int:

@@ -450,6 +450,213 @@ ORACLE_API int oracle_coeffs(int table, double *out)
     return m;
 }
 
+/* ======================= the paper's AMNF and EVMF filters ================ *
+ * SURVEY.md 8(f2)-(f3).  Same window engine (Fig. 1, replicate border).      */
+
+enum { FILT_AMNFE = 3, FILT_AMNFG = 4, FILT_EVMF = 5 };
+
+/* AMNF, Eq. 8:
+ *   y = sum_i x_i w_i / sum_j w_j,  w_i = h_i^-3 K((x_C - x_i) / h_i),
+ *   h_i = n^(-kappa/3) sum_j |x_i - x_j|_1,  kappa = 0.33,
+ *   AMNFE: K(x) = exp(-|x|_1)  ->  K = exp(-|x_C - x_i|_1 / h_i)
+ *   AMNFG: K(x) = exp(-0.5 |x|_2^2) -> K = exp(-0.5 |x_C - x_i|_2^2 / h_i^2)
+ * exp evaluated exactly (libm) or by Table 3 (VAR_MINIMAX) / Table 2 p = 4
+ * (VAR_MINIMAX_POLY4), both with the P:163 cutoff.  Output rounded to nearest,
+ * half away from zero, clamped to [0, 255].  Degenerate
+ * windows (some h_i = 0, i.e. all samples equal, or sum w = 0) return x_C
+ * (S:343).  aux (n + 3 doubles): v[3] unrounded output, w_i / sum w.        */
+static int amnf_window(const uint8_t *smp, int n, int gauss, int var, uint8_t *out, double *aux)
+{
+    int C = (n - 1) / 2;
+    int64_t x[NMAX][3];
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k)
+            x[i][k] = smp[3 * i + k];
+    double nk = pow((double)n, -KAPPA / 3.0);
+    double h[NMAX], w[NMAX];
+    int degenerate = 0;
+    for (int i = 0; i < n; ++i) {
+        int64_t row = 0;
+        for (int j = 0; j < n; ++j)
+            for (int k = 0; k < 3; ++k)
+                row += x[i][k] > x[j][k] ? x[i][k] - x[j][k] : x[j][k] - x[i][k];
+        h[i] = nk * (double)row;                                   /* Eq. 8 */
+        if (h[i] == 0.0)
+            degenerate = 1;
+    }
+    double sw = 0.0;
+    if (!degenerate) {
+        for (int i = 0; i < n; ++i) {
+            int64_t l1 = 0, l2 = 0;
+            for (int k = 0; k < 3; ++k) {
+                int64_t d = x[C][k] - x[i][k];
+                l1 += d < 0 ? -d : d;
+                l2 += d * d;
+            }
+            double z = gauss ? 0.5 * (double)l2 / (h[i] * h[i]) : (double)l1 / h[i];
+            double K;
+            if (var == VAR_EXACT)
+                K = exp(-z);
+            else if (var == VAR_MINIMAX)
+                K = exp_mm_rational(z);
+            else
+                K = exp_mm_poly(z, 4);
+            w[i] = K / (h[i] * h[i] * h[i]);                       /* h_i^-3 K */
+            sw += w[i];
+        }
+        if (sw == 0.0)
+            degenerate = 1;
+    }
+    if (degenerate) {
+        for (int k = 0; k < 3; ++k) {
+            out[k] = (uint8_t)x[C][k];
+            if (aux) aux[k] = (double)x[C][k];
+        }
+        if (aux)
+            for (int i = 0; i < n; ++i) aux[3 + i] = (i == C);
+        return 0;
+    }
+    for (int k = 0; k < 3; ++k) {
+        double v = 0.0;
+        for (int i = 0; i < n; ++i)
+            v += (double)x[i][k] * w[i];
+        v /= sw;
+        if (aux) aux[k] = v;
+        double r = floor(v + 0.5);                                 /* v >= 0: half away from zero */
+        out[k] = (uint8_t)(r < 0.0 ? 0.0 : (r > 255.0 ? 255.0 : r));
+    }
+    if (aux)
+        for (int i = 0; i < n; ++i) aux[3 + i] = w[i] / sw;
+    return 0;
+}
+
+/* EVMF, Eq. 9:
+ *   y = argmin_i sum_j |x_i - x_j|_2 (vector median) if P_C > beta_C, else x_C;
+ *   P_i = |x_i - xbar|_2 / sum_j |x_j - xbar|_2,  xbar = window mean,
+ *   beta_i = -P_i log P_i / (-sum_j P_j log P_j) = ENT(P_i) / sum_j ENT(P_j),
+ *   ENT exact = z ln z (natural log, R10), minimax = Table 4 with the P:232
+ *   cutoff (0 below 0.05).  Degenerate: sum_j |x_j - xbar| = 0 ->
+ *   identity; sum_j ENT(P_j) = 0 -> beta_C = 0.  Ties of the median: lowest
+ *   index.  Returns the selected index (C when the switch does not
+ *   fire).  aux (n + 3 doubles): R_i (VMF aggregates), P_C, beta_C, fired.   */
+static int evmf_window(const uint8_t *smp, int n, int var, uint8_t *out, double *aux)
+{
+    int C = (n - 1) / 2;
+    int64_t x[NMAX][3];
+    double mean[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) {
+            x[i][k] = smp[3 * i + k];
+            mean[k] += (double)x[i][k];
+        }
+    for (int k = 0; k < 3; ++k)
+        mean[k] /= (double)n;
+    double dev[NMAX], S = 0.0;
+    for (int i = 0; i < n; ++i) {
+        double s2 = 0.0;
+        for (int k = 0; k < 3; ++k)
+            s2 += ((double)x[i][k] - mean[k]) * ((double)x[i][k] - mean[k]);
+        dev[i] = sqrt(s2);
+        S += dev[i];
+    }
+    double R[NMAX];
+    for (int i = 0; i < n; ++i) {
+        double r = 0.0;
+        for (int j = 0; j < n; ++j) {
+            if (j == i) continue;
+            int64_t d2 = 0;
+            for (int k = 0; k < 3; ++k)
+                d2 += (x[i][k] - x[j][k]) * (x[i][k] - x[j][k]);
+            r += sqrt((double)d2);
+        }
+        R[i] = r;
+    }
+    double PC = 0.0, betaC = 0.0;
+    int fired = 0;
+    if (S > 0.0) {
+        double sent = 0.0, entC = 0.0;
+        for (int i = 0; i < n; ++i) {
+            double P = dev[i] / S;
+            double e = var == VAR_EXACT ? ent_exact(P) : ent_mm(P);
+            sent += e;
+            if (i == C) { entC = e; PC = P; }
+        }
+        betaC = sent == 0.0 ? 0.0 : entC / sent;
+        fired = PC > betaC;
+    }
+    int sel = C;
+    if (fired) {
+        sel = 0;
+        for (int i = 1; i < n; ++i)
+            if (R[i] < R[sel]) sel = i;
+    }
+    for (int k = 0; k < 3; ++k)
+        out[k] = (uint8_t)x[sel][k];
+    if (aux) {
+        for (int i = 0; i < n; ++i) aux[i] = R[i];
+        aux[n] = PC;
+        aux[n + 1] = betaC;
+        aux[n + 2] = fired;
+    }
+    return sel;
+}
+
+static int paper_window(const uint8_t *smp, int n, int filt, int var, uint8_t *out, double *aux)
+{
+    if (filt == FILT_EVMF)
+        return evmf_window(smp, n, var, out, aux);
+    return amnf_window(smp, n, filt == FILT_AMNFG, var, out, aux);
+}
+
+static int check_paper_args(int n, int filt, int var)
+{
+    if (n < 2 || n > NMAX) return -1;
+    if (filt < FILT_AMNFE || filt > FILT_EVMF) return -1;
+    if (var < 0 || var > 2) return -1;
+    if (var == VAR_MINIMAX_POLY4 && filt == FILT_EVMF) return -1;
+    return 0;
+}
+
+/* One window of n raw samples.  Returns the selected index (EVMF) or 0
+ * (AMNF), or -1 on bad args.  out: 3 bytes; aux: n + 3 doubles or NULL.    */
+ORACLE_API int oracle_paper_window(const uint8_t *samples, int n, int filt, int var, uint8_t *out, double *aux)
+{
+    if (check_paper_args(n, filt, var) != 0)
+        return -1;
+    return paper_window(samples, n, filt, var, out, aux);
+}
+
+/* Full image (or sampled pixels when ys/xs != NULL): out (npix*3), optional
+ * index (npix, EVMF selection), optional aux (npix*(n+3)).                 */
+ORACLE_API int oracle_paper_filter(const uint8_t *img, int H, int W, int window, int filt, int var,
+                                   const int32_t *ys, const int32_t *xs, int64_t npix,
+                                   uint8_t *out, uint8_t *index, double *aux, int nthreads)
+{
+    if (H < 1 || W < 1 || window < 3 || window % 2 == 0 || window > H || window > W || !img || !out)
+        return -1;
+    int n = window * window;
+    if (check_paper_args(n, filt, var) != 0)
+        return -1;
+    int64_t total = ys ? npix : (int64_t)H * W;
+#ifdef _OPENMP
+    if (nthreads > 0)
+        omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 256)
+#endif
+    for (int64_t i = 0; i < total; ++i) {
+        uint8_t smp[NMAX * 3];
+        int y = ys ? ys[i] : (int)(i / W), x = xs ? xs[i] : (int)(i % W);
+        if (y < 0 || y >= H || x < 0 || x >= W)
+            continue;
+        gather_window(img, H, W, window, y, x, smp);
+        int k = paper_window(smp, n, filt, var, out + 3 * i, aux ? aux + i * (size_t)(n + 3) : NULL);
+        if (index)
+            index[i] = (uint8_t)k;
+    }
+    (void)nthreads;
+    return 0;
+}
+
 ORACLE_API int oracle_max_threads(void)
 {
 #ifdef _OPENMP

@@ -1,0 +1,215 @@
+"""Pins for the oracle's AMNF (Eq. 8) and EVMF (Eq. 9) filters.
+
+Expected values come from closed forms of special windows derived by hand from
+Eq. 8 / Eq. 9, SPEC's worked examples, an independent 50-digit
+mpmath implementation of the equations, and invariants.
+"""
+import math
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import oracle
+
+mp.mp.dps = 50
+KAPPA = mp.mpf("0.33")
+
+
+@pytest.fixture(scope="module")
+def T(paper_tables):
+    return {k: [mp.mpf(repr(v)) for v in d["values"]] for k, d in paper_tables.items()}
+
+
+def hornerm(a, z):
+    r = mp.mpf(0)
+    for c in reversed(a):
+        r = r * z + c
+    return r
+
+
+def E_mm(z, var, T):
+    if z > 10:
+        return mp.mpf(0)
+    if var == "minimax":
+        return hornerm(T["EXP_NUM"], z) / hornerm(T["EXP_DEN"], z)
+    return hornerm(T["EXP_P4"], z)
+
+
+def ENT(z, var, T):
+    if var == "exact":
+        return z * mp.log(z) if z > 0 else mp.mpf(0)
+    if z < mp.mpf("0.05"):
+        return mp.mpf(0)
+    return hornerm(T["ENT_NUM"], z) / hornerm(T["ENT_DEN"], z)
+
+
+# ----------------------------------------------------------- mpmath reference
+def mp_amnf(s, gauss, var, T):
+    s = [[int(v) for v in x] for x in s]
+    n = len(s)
+    C = (n - 1) // 2
+    nk = mp.mpf(n) ** (-KAPPA / 3)
+    h = [nk * sum(abs(s[i][k] - s[j][k]) for j in range(n) for k in range(3)) for i in range(n)]
+    if any(v == 0 for v in h):
+        return [mp.mpf(v) for v in s[C]], None
+    w = []
+    for i in range(n):
+        d = [mp.mpf(s[C][k] - s[i][k]) / h[i] for k in range(3)]    # (x_C - x_i) / h_i, Eq. 8
+        z = mp.mpf("0.5") * sum(v * v for v in d) if gauss else sum(abs(v) for v in d)
+        K = mp.exp(-z) if var == "exact" else E_mm(z, var, T)
+        w.append(K / h[i] ** 3)
+    sw = mp.fsum(w)
+    return [mp.fsum(s[i][k] * w[i] for i in range(n)) / sw for k in range(3)], [v / sw for v in w]
+
+
+def mp_evmf(s, var, T):
+    s = [[int(v) for v in x] for x in s]
+    n = len(s)
+    C = (n - 1) // 2
+    mean = [mp.mpf(sum(x[k] for x in s)) / n for k in range(3)]
+    dev = [mp.sqrt(sum((x[k] - mean[k]) ** 2 for k in range(3))) for x in s]
+    S = mp.fsum(dev)
+    R = [mp.fsum(mp.sqrt(sum((s[i][k] - s[j][k]) ** 2 for k in range(3))) for j in range(n) if j != i)
+         for i in range(n)]
+    if S == 0:
+        return False, None, None, R
+    P = [d / S for d in dev]
+    ents = [ENT(p, var, T) for p in P]
+    se = mp.fsum(ents)
+    beta = mp.mpf(0) if se == 0 else ents[C] / se
+    return P[C] > beta, P[C], beta, R
+
+
+# ----------------------------------------------------------- degenerate windows
+@pytest.mark.parametrize("filt,var", [("amnfe", "exact"), ("amnfe", "minimax"), ("amnfe", "poly4"),
+                                      ("amnfg", "exact"), ("amnfg", "minimax"), ("evmf", "exact"),
+                                      ("evmf", "minimax")])
+@pytest.mark.parametrize("n", [9, 25])
+def test_uniform_window_returns_centre(filt, var, n):
+    """S:310 / S:320: all h_i = 0 (AMNF) or sum |x_j - xbar| = 0 (EVMF) -> x_C."""
+    s = np.array([[33, 140, 7]] * n, np.uint8)
+    k, out, aux = oracle.paper_window(s, filt, var)
+    assert list(out) == [33, 140, 7]
+    if filt == "evmf":
+        assert k == (n - 1) // 2 and aux[n + 2] == 0
+
+
+# ----------------------------------------------------------- AMNF closed forms
+@pytest.mark.parametrize("n", [9, 25])
+@pytest.mark.parametrize("var", ["exact", "minimax", "poly4"])
+@pytest.mark.parametrize("a,b", [((10, 20, 30), (200, 5, 90)), ((128, 128, 128), (129, 128, 128)),
+                                 ((0, 0, 0), (255, 255, 255))])
+def test_amnfe_single_impulse_closed_form(n, var, a, b, T):
+    """n-1 samples a, one impulse b.  Eq. 8 gives h_inlier = n^(-k/3) d,
+    h_impulse = (n-1) h_inlier (d = |a-b|_1), so with the centre an inlier
+    v = a + (b - a) r / (n - 1 + r), r = K(z*) / (n-1)^3, z* = n^(k/3) / (n-1);
+    with the centre the impulse, v = b + (a - b) (n-1) q / ((n-1) q + 1),
+    q = K(n^(k/3)) (n-1)^3."""
+    K = (lambda z: mp.exp(-z)) if var == "exact" else (lambda z: E_mm(z, var, T))
+    C = (n - 1) // 2
+    for pos in (0, C):
+        s = np.array([a] * n, np.uint8)
+        s[pos] = b
+        _, out, aux = oracle.paper_window(s, "amnfe", var)
+        if pos != C:
+            r = K(mp.mpf(n) ** (KAPPA / 3) / (n - 1)) / K(mp.mpf(0)) / (n - 1) ** 3
+            v = [a[k] + (b[k] - a[k]) * r / (n - 1 + r) for k in range(3)]
+        else:
+            q = K(mp.mpf(n) ** (KAPPA / 3)) / K(mp.mpf(0)) * (n - 1) ** 3
+            v = [b[k] + (a[k] - b[k]) * (n - 1) * q / ((n - 1) * q + 1) for k in range(3)]
+        np.testing.assert_allclose(aux[:3], [float(t) for t in v], rtol=1e-12, atol=1e-12)
+        assert list(out) == [min(255, max(0, math.floor(float(t) + 0.5))) for t in v]
+
+
+def test_amnf_convex_combination():
+    """nonnegative weights; the unrounded output lies in the per-channel
+    envelope of the window."""
+    rng = np.random.default_rng(4)
+    for _ in range(300):
+        n = 9 if rng.random() < 0.5 else 25
+        s = rng.integers(0, 256, size=(n, 3)).astype(np.uint8)
+        for filt in ("amnfe", "amnfg"):
+            _, _, aux = oracle.paper_window(s, filt, "minimax")
+            assert np.all(aux[3:] >= 0) and abs(aux[3:].sum() - 1) < 1e-12
+            assert np.all(aux[:3] >= s.min(0) - 1e-9) and np.all(aux[:3] <= s.max(0) + 1e-9)
+
+
+# ----------------------------------------------------------- EVMF closed forms
+@pytest.mark.parametrize("n", [9, 25])
+@pytest.mark.parametrize("var", ["exact", "minimax"])
+def test_evmf_centre_impulse_closed_form(n, var, T):
+    """Centre impulse b in n-1 samples a: P_C = 1/2, P_inlier = 1/(2(n-1)),
+    beta_C = ENT(1/2) / (ENT(1/2) + (n-1) ENT(1/(2(n-1)))).  For n = 25 the
+    inlier share 1/48 is below the P:232 cutoff, so the minimax beta_C = 1 and
+    the switch does NOT fire (the exact one does)."""
+    C = (n - 1) // 2
+    s = np.array([[50, 50, 50]] * n, np.uint8)
+    s[C] = [255, 255, 255]
+    k, out, aux = oracle.paper_window(s, "evmf", var)
+    half = mp.mpf(1) / 2
+    pi = mp.mpf(1) / (2 * (n - 1))
+    se = ENT(half, var, T) + (n - 1) * ENT(pi, var, T)
+    beta = ENT(half, var, T) / se if se != 0 else mp.mpf(0)
+    assert aux[n] == pytest.approx(0.5, abs=1e-15)
+    assert aux[n + 1] == pytest.approx(float(beta), rel=1e-12)
+    fires = half > beta
+    assert bool(aux[n + 2]) == fires
+    if fires:
+        assert list(out) == [50, 50, 50] and k != C        # the median replaces the centre
+    else:
+        assert list(out) == [255, 255, 255] and k == C
+    if n == 9:
+        assert fires and float(beta) == pytest.approx(0.2, abs=1e-5)
+    if n == 25:
+        assert fires == (var == "exact")
+
+
+# ----------------------------------------------------------- brute force
+@pytest.mark.parametrize("n", [9, 25])
+def test_random_windows_vs_mpmath(n, T):
+    rng = np.random.default_rng(200 + n)
+    for t in range(20 if n == 9 else 6):
+        if t % 2:
+            s = np.clip(rng.integers(90, 110, size=(n, 3)), 0, 255).astype(np.uint8)
+            m = rng.random(n) < 0.2
+            s[m] = rng.integers(0, 256, size=(m.sum(), 3))
+        else:
+            s = rng.integers(0, 256, size=(n, 3)).astype(np.uint8)
+        for filt, gauss in (("amnfe", False), ("amnfg", True)):
+            for var in ("exact", "minimax", "poly4"):
+                _, out, aux = oracle.paper_window(s, filt, var)
+                v, w = mp_amnf(s, gauss, var, T)
+                np.testing.assert_allclose(aux[:3], [float(x) for x in v], rtol=1e-12, atol=1e-12)
+                np.testing.assert_allclose(aux[3:], [float(x) for x in w], rtol=1e-10, atol=1e-15)
+        for var in ("exact", "minimax"):
+            k, out, aux = oracle.paper_window(s, "evmf", var)
+            fires, PC, beta, R = mp_evmf(s, var, T)
+            np.testing.assert_allclose(aux[:n], [float(x) for x in R], rtol=1e-12)
+            assert aux[n] == pytest.approx(float(PC), rel=1e-12)
+            assert aux[n + 1] == pytest.approx(float(beta), rel=1e-10, abs=1e-15)
+            if abs(PC - beta) > mp.mpf("1e-12"):
+                assert bool(aux[n + 2]) == fires
+            if aux[n + 2]:
+                m = min(R)
+                assert R[k] - m <= mp.mpf("1e-12") * m
+            else:
+                assert k == (n - 1) // 2
+
+
+def test_paper_filter_image_matches_windows():
+    rng = np.random.default_rng(9)
+    img = rng.integers(0, 256, size=(17, 23, 3)).astype(np.uint8)
+    for filt, var in (("amnfe", "minimax"), ("amnfg", "exact"), ("evmf", "minimax")):
+        out, idx, aux = oracle.paper_filter(img, 3, filt, var)
+        for y, x in [(0, 0), (5, 7), (16, 22), (8, 0)]:
+            s = oracle.gather_window(img, 3, y, x)
+            k, o, a = oracle.paper_window(s, filt, var)
+            assert np.array_equal(out[y, x], o) and np.array_equal(aux[y, x], a)
+            if filt == "evmf":
+                assert idx[y, x] == k
+        ys, xs = np.array([3, 9]), np.array([4, 11])
+        o2, i2, a2 = oracle.paper_filter(img, 3, filt, var, ys=ys, xs=xs)
+        assert np.array_equal(o2, out[ys, xs]) and np.array_equal(a2, aux[ys, xs])
+    with pytest.raises(ValueError):
+        oracle.paper_filter(img, 3, "evmf", "poly4")
