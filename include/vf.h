@@ -47,7 +47,7 @@
  *   Every entry point returns a vf_status.  VF_EINVAL: invalid argument
  *   (window even or < 3, H or W < 1, window > min(H, W), B < 1, NULL
  *   img/out, input and output ranges overlap, criterion/variant out of range,
- *   VF_MINIMAX_POLY4 with a criterion other than VF_EXP, a row band that does
+ *   VF_MINIMAX_POLY4 with a criterion other than VF_EXP/VF_AMNFE/VF_AMNFG, a row band that does
  *   not cover the rows the output stripe reads).  VF_EUNSUPPORTED: an odd
  *   window >= 7 (valid, not compiled).  VF_ECUDA: a CUDA launch/copy error
  *   (details from vf_last_error()).  No exception crosses the ABI.  On error
@@ -69,7 +69,21 @@
 extern "C" {
 #endif
 
-typedef enum { VF_ANGULAR = 0, VF_EXP = 1, VF_LOG = 2 } vf_criterion;
+/* criterion: the pairwise ordering criteria of the order-statistics filter
+ * (0-2), or one of the paper's other two filters (3-5):
+ *   VF_AMNFE / VF_AMNFG  AMNF of Eq. 8 with the exponential /
+ *                        Gaussian kernel: a weighted average, output rounded
+ *                        half away from zero; exp exact (expf) or the
+ *                        Table 3 rational (VF_MINIMAX) / Table 2 p=4
+ *                        (VF_MINIMAX_POLY4), cutoff T = 10;
+ *                        `aggregates` [..][n]: the 3 unrounded output channels
+ *                        then zeros; `index`: the centre index.
+ *   VF_EVMF              EVMF of Eq. 9: L2 vector median when
+ *                        P_C > beta_C, else the centre; ENT exact (logf) or
+ *                        Table 4 with cutoff T = 0.05; `aggregates`:
+ *                        the median's sums R_i = sum_j |x_i - x_j|_2; `index`:
+ *                        selected sample, bit 7 set iff the switch fired. */
+typedef enum { VF_ANGULAR = 0, VF_EXP = 1, VF_LOG = 2, VF_AMNFE = 3, VF_AMNFG = 4, VF_EVMF = 5 } vf_criterion;
 typedef enum { VF_EXACT = 0, VF_MINIMAX = 1, VF_MINIMAX_POLY4 = 2 } vf_variant;
 typedef enum { VF_OK = 0, VF_EINVAL = -1, VF_EUNSUPPORTED = -2, VF_ECUDA = -3 } vf_status;
 

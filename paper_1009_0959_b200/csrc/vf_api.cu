@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/vf.h"
+#include "vf_paper.cuh"
 #include "vf_shared.cuh"
 #include "vf_stats.cuh"
 #include "vf_window.cuh"
@@ -56,6 +57,15 @@ cudaError_t ensure_attributes() {
 template <int WIN>
 const void* window_kernel(int crit, int var) {
   using namespace vf;
+  if (crit == AMNFE)
+    return var == EXACT ? (const void*)vf_amnf_kernel<WIN, 0, EXACT>
+                        : (var == MINIMAX ? (const void*)vf_amnf_kernel<WIN, 0, MINIMAX>
+                                          : (const void*)vf_amnf_kernel<WIN, 0, POLY4>);
+  if (crit == AMNFG)
+    return var == EXACT ? (const void*)vf_amnf_kernel<WIN, 1, EXACT>
+                        : (var == MINIMAX ? (const void*)vf_amnf_kernel<WIN, 1, MINIMAX>
+                                          : (const void*)vf_amnf_kernel<WIN, 1, POLY4>);
+  if (crit == EVMF) return var == EXACT ? (const void*)vf_evmf_kernel<WIN, EXACT> : (const void*)vf_evmf_kernel<WIN, MINIMAX>;
   if (crit == ANGULAR)
     return var == EXACT ? (const void*)vf_angular_window_kernel<WIN, EXACT>
                         : (const void*)vf_angular_window_kernel<WIN, MINIMAX>;
@@ -72,9 +82,10 @@ int validate(int B, int H, int W, int window, int crit, int var) {
   if (B < 1) return fail(VF_EINVAL, "batch must be >= 1 (got %lld)", B);
   if (H < 1 || W < 1) return fail(VF_EINVAL, "image size must be positive");
   if (window > H || window > W) return fail(VF_EINVAL, "window larger than the image (S:64)");
-  if (crit < 0 || crit > 2) return fail(VF_EINVAL, "criterion out of range (%lld)", crit);
+  if (crit < 0 || crit > 5) return fail(VF_EINVAL, "criterion out of range (%lld)", crit);
   if (var < 0 || var > 2) return fail(VF_EINVAL, "variant out of range (%lld)", var);
-  if (var == VF_MINIMAX_POLY4 && crit != VF_EXP) return fail(VF_EINVAL, "VF_MINIMAX_POLY4 is only defined for VF_EXP");
+  if (var == VF_MINIMAX_POLY4 && crit != VF_EXP && crit != VF_AMNFE && crit != VF_AMNFG)
+    return fail(VF_EINVAL, "VF_MINIMAX_POLY4 is only defined for the EXP-based filters");
   if (window > 5) return fail(VF_EUNSUPPORTED, "window %lld is valid but not compiled (3 and 5 are)", window);
   return VF_OK;
 }
@@ -83,6 +94,7 @@ float kscale(int crit, int window) {
   const double n = (double)window * window;
   if (crit == VF_EXP) return (float)(std::pow(n, 1.0 + vf::coef::KAPPA / 3.0) / 2.0);  // c_E * S1
   if (crit == VF_LOG) return (float)(vf::coef::ONE_MINUS_INV_E * (n - 1.0));          // c_L * S1
+  if (crit == VF_AMNFE || crit == VF_AMNFG) return (float)std::pow(n, -vf::coef::KAPPA / 3.0);  // h_i / row sum
   return 0.0f;
 }
 
@@ -104,7 +116,7 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   } else {
     kd->fn = window == 3 ? window_kernel<3>(crit, var) : window_kernel<5>(crit, var);
-    const int th = crit == VF_ANGULAR ? vf::TY : vf::TY * vf::el_opt(window);
+    const int th = (crit == VF_EXP || crit == VF_LOG) ? vf::TY * vf::el_opt(window) : vf::TY;
     kd->grid = dim3((W + vf::TX - 1) / vf::TX, (out_rows + th - 1) / th, B);
     kd->block = dim3(vf::TX, vf::TY);
     kd->smem = 0;

@@ -60,6 +60,13 @@ __host__ __device__ constexpr P4f ENT_NEGN_U() { return P4f{(float)(-reexpand(T4
 __host__ __device__ constexpr P4f ENT_Q_U() { return P4f{(float)reexpand(T4_Q, 0), (float)reexpand(T4_Q, 1), (float)reexpand(T4_Q, 2),
                          (float)reexpand(T4_Q, 3), (float)reexpand(T4_Q, 4)}; }
 
+// Direct (unshifted) forms for the AMNF / EVMF filters, whose arguments are
+// not near the cancellation points: Table 3 numerator, Table 2 p = 4, Table 4.
+__host__ __device__ constexpr P4f EXP_N() { return P4f{(float)T3_N[0], (float)T3_N[1], (float)T3_N[2], (float)T3_N[3], (float)T3_N[4]}; }
+__host__ __device__ constexpr P4f EXP_P4() { return P4f{(float)T2_P4[0], (float)T2_P4[1], (float)T2_P4[2], (float)T2_P4[3], (float)T2_P4[4]}; }
+__host__ __device__ constexpr P4f ENT_N() { return P4f{(float)T4_N[0], (float)T4_N[1], (float)T4_N[2], (float)T4_N[3], (float)T4_N[4]}; }
+__host__ __device__ constexpr P4f ENT_Q() { return P4f{(float)T4_Q[0], (float)T4_Q[1], (float)T4_Q[2], (float)T4_Q[3], (float)T4_Q[4]}; }
+
 constexpr double KAPPA = 0.33;
 constexpr double ONE_MINUS_INV_E = 0.63212055882855767840;  // 1 - e^-1 (reading R3)
 

@@ -174,7 +174,7 @@ def test_host_api_matches_device_api():
 def test_invalid_arguments_return_status():
     x = torch.zeros((16, 16, 3), dtype=torch.uint8, device="cuda")
     for w, c, v, st in [(4, "angular", "exact", -1), (7, "angular", "exact", -2), (3, "angular", "poly4", -1),
-                        (3, 5, 0, -1), (3, 0, 9, -1), (17, "exp", "exact", -1)]:
+                        (3, 6, 0, -1), (3, 0, 9, -1), (3, "evmf", "poly4", -1), (17, "exp", "exact", -1)]:
         with pytest.raises(vfb.VFError) as e:
             vfb.filter(x, w, c, v)
         assert e.value.status == st, (w, c, v)

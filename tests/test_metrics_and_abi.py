@@ -86,9 +86,10 @@ def test_invalid_arguments_rejected_before_any_device_work(lib):
     assert f(p, 16, 16, 1, 0, 0, q, None, None, None) == -1          # window < 3
     assert f(p, 16, 16, 7, 0, 0, q, None, None, None) == -2          # valid, not compiled
     assert f(p, 2, 16, 3, 0, 0, q, None, None, None) == -1           # window > H
-    assert f(p, 16, 16, 3, 3, 0, q, None, None, None) == -1          # criterion
+    assert f(p, 16, 16, 3, 6, 0, q, None, None, None) == -1          # criterion
     assert f(p, 16, 16, 3, 0, 3, q, None, None, None) == -1          # variant
-    assert f(p, 16, 16, 3, 0, 2, q, None, None, None) == -1          # POLY4 only for EXP
+    assert f(p, 16, 16, 3, 0, 2, q, None, None, None) == -1          # POLY4 only for the EXP filters
+    assert f(p, 16, 16, 3, 5, 2, q, None, None, None) == -1          # (EVMF uses ENT, not EXP)
     assert f(None, 16, 16, 3, 0, 0, q, None, None, None) == -1       # NULL input
     assert f(p, 16, 16, 3, 0, 0, p, None, None, None) == -1          # aliasing
     assert b"overlap" in lib.vf_last_error()
