@@ -354,6 +354,57 @@ def run_partitioned(args):
 
 
 # ------------------------------------------------------------------ our arm
+PAPER_FILTERS = [("amnfe", "exact"), ("amnfe", "minimax"), ("amnfe", "poly4"), ("amnfg", "exact"),
+                 ("amnfg", "minimax"), ("evmf", "exact"), ("evmf", "minimax")]
+PAPER_TIME_PCT = {"BVDF": 1371.314, "AMNFE": 143.496, "EVMF": 236.105}   # Table 5, correlated 10%
+
+
+def paper_filters_section(vfb, torch, dev, stream, flush, x, x_np, spec, rank, w, outs):
+    """Isolated launches of AMNFE/AMNFG/EVMF (exact and minimax) plus the
+    angular BVDF outputs of the step; Time % and Table-5-style quality deltas
+    against the clean image (same image ids as the noisy input)."""
+    import vfsynth
+    res = {"kernels": {}}
+    pouts = {}
+    for c in PAPER_FILTERS:
+        o = torch.empty_like(x)
+        for _ in range(2):
+            vfb.vf_filter_batch(x, w, *c, out=o, stream=stream)
+        ts = []
+        for r in range(5):
+            flush.fill_(r)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            vfb.vf_filter_batch(x, w, *c, out=o, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            ts.append(a.elapsed_time(b))
+        ms = statistics.median(ts)
+        res["kernels"][f"{c[0]}/{c[1]}"] = {"ms": ms, "mpix_s": x.numel() / 3 / (ms / 1e3) / 1e6}
+        pouts[c] = o
+    res["time_pct"] = {}
+    res["quality_vs_clean"] = {}
+    # clean images of the same ids
+    if spec.name in ("C1", "C2"):
+        clean = vfsynth.make_image(spec, rank if spec.batch == 1 else 0)[0][None]
+        ct = torch.from_numpy(clean).to(dev)
+        pairs = {"BVDF": ((("angular", "exact"), outs[COMBOS.index(("angular", "exact"))]),
+                          (("angular", "minimax"), outs[COMBOS.index(("angular", "minimax"))])),
+                 "AMNFE": ((("amnfe", "exact"), pouts[("amnfe", "exact")]), (("amnfe", "minimax"), pouts[("amnfe", "minimax")])),
+                 "EVMF": ((("evmf", "exact"), pouts[("evmf", "exact")]), (("evmf", "minimax"), pouts[("evmf", "minimax")]))}
+        noisy_q = vfb.fidelity(ct, x)
+        res["quality_vs_clean"]["noisy_input"] = {"mae": noisy_q["mae"], "mse": noisy_q["mse"], "ncd": noisy_q["ncd"]}
+        for name, ((ce, oe), (cm, om)) in pairs.items():
+            qe, qm = vfb.fidelity(ct, oe), vfb.fidelity(ct, om)
+            d = {}
+            for m in ("mae", "mse", "ncd"):
+                d[m] = {"exact": qe[m], "approx": qm[m],
+                        "delta_pct": 100.0 * (qe[m] - qm[m]) / qe[m] if qe[m] else 0.0}
+            res["quality_vs_clean"][name] = d
+    return res
+
+
 KERNEL_NAMES = {"angular": "vf_angular_shared_kernel<{w},{v}>", "exp": "vf_el_kernel<{w},exp,{v}>",
                 "log": "vf_el_kernel<{w},log,{v}>"}
 
@@ -512,6 +563,17 @@ def main():
         f = vfb.fidelity(oi[(crit, "exact")], oi[(crit, mmv)])
         fid[f"{crit}/{mmv}"] = {"psnr_db": f["psnr_db"], "ncd": f["ncd"], "diff_frac": f["diff_frac"]}
 
+    # ---- the paper's three filters (Table 5 methodology on the synthetic
+    # stand-in): BVDF = angular order statistic, AMNFE (Eq. 8), EVMF (Eq. 9);
+    # Time % = 100 t_exact / t_approx (the paper's definition) and
+    # quality deltas of MAE / MSE / NCD against the noise-free image.
+    paper = paper_filters_section(vfb, torch, dev, stream, flush, x, x_np, spec, rank, w, outs)
+    pk = paper["kernels"]
+    for name, te, ta in (("BVDF", kern["angular/exact"]["ms"], kern["angular/minimax"]["ms"]),
+                         ("AMNFE", pk["amnfe/exact"]["ms"], pk["amnfe/minimax"]["ms"]),
+                         ("EVMF", pk["evmf/exact"]["ms"], pk["evmf/minimax"]["ms"])):
+        paper["time_pct"][name] = {"b200": 100.0 * te / ta, "paper_pentium_d": PAPER_TIME_PCT[name]}
+
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -538,6 +600,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "fidelity_minimax_vs_exact": fid,
+            "paper_filters": paper,
             "gpu_launches": len(COMBOS) * args.steps,
             "clocks": clocks,
             "wall_s_timed_region": t_wall,
