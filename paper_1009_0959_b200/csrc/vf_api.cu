@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -54,6 +55,17 @@ cudaError_t ensure_attributes() {
   return status;
 }
 
+template <int WIN, int OPT>
+const void* el_kernel(int crit, int var) {
+  using namespace vf;
+  if (crit == EXPC) {
+    if (var == EXACT) return (const void*)vf_el_kernel<WIN, EXPC, EXACT, OPT>;
+    if (var == MINIMAX) return (const void*)vf_el_kernel<WIN, EXPC, MINIMAX, OPT>;
+    return (const void*)vf_el_kernel<WIN, EXPC, POLY4, OPT>;
+  }
+  return var == EXACT ? (const void*)vf_el_kernel<WIN, LOGC, EXACT, OPT> : (const void*)vf_el_kernel<WIN, LOGC, MINIMAX, OPT>;
+}
+
 template <int WIN>
 const void* window_kernel(int crit, int var) {
   using namespace vf;
@@ -69,12 +81,7 @@ const void* window_kernel(int crit, int var) {
   if (crit == ANGULAR)
     return var == EXACT ? (const void*)vf_angular_window_kernel<WIN, EXACT>
                         : (const void*)vf_angular_window_kernel<WIN, MINIMAX>;
-  if (crit == EXPC) {
-    if (var == EXACT) return (const void*)vf_el_kernel<WIN, EXPC, EXACT>;
-    if (var == MINIMAX) return (const void*)vf_el_kernel<WIN, EXPC, MINIMAX>;
-    return (const void*)vf_el_kernel<WIN, EXPC, POLY4>;
-  }
-  return var == EXACT ? (const void*)vf_el_kernel<WIN, LOGC, EXACT> : (const void*)vf_el_kernel<WIN, LOGC, MINIMAX>;
+  return nullptr;   // exp/log: el_kernel
 }
 
 int validate(int B, int H, int W, int window, int crit, int var) {
@@ -107,16 +114,37 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
   L.H = H; L.W = W; L.band_row0 = band_row0; L.band_rows = band_rows;
   L.out_row0 = out_row0; L.out_rows = out_rows;
   L.kscale = kscale(crit, window);
+  const int tile = (algo >> 2) & 3;   // 0 = by size; 1..3 = forced rows per thread (tuning / tests)
+  algo &= 3;
   if (crit == VF_ANGULAR && algo != VF_ALGO_WINDOW) {
-    kd->fn = vf::shared_kernel_fn(window, var);
-    kd->grid = vf::shared_grid(L, B, window);
+    // region height: 3 pixels per thread measured fastest at every size
+    // (C2 262 K px, C4 6.3 M px, C3 33.5 M px; tools/tune_tiles.sh).
+    // VF_SHARED_PPT=1..3 or the algo tile bits override, for tuning and tests.
+    int ppt = 3;
+    static const int ppt_env = [] { const char* e = std::getenv("VF_SHARED_PPT"); return e ? std::atoi(e) : 0; }();
+    if (ppt_env >= 1 && ppt_env <= 3) ppt = ppt_env;
+    if (tile) ppt = tile;
+    kd->fn = vf::shared_kernel_fn(window, var, ppt);
+    kd->grid = vf::shared_grid(L, B, window, ppt);
     kd->block = dim3(vf::shared::NTHR);
-    kd->smem = vf::shared_smem_bytes(window);
+    kd->smem = vf::shared_smem_bytes(window, ppt);
     const cudaError_t e = ensure_attributes();
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   } else {
-    kd->fn = window == 3 ? window_kernel<3>(crit, var) : window_kernel<5>(crit, var);
-    const int th = (crit == VF_EXP || crit == VF_LOG) ? vf::TY * vf::el_opt(window) : vf::TY;
+    int th = vf::TY;
+    if (crit == VF_EXP || crit == VF_LOG) {
+      // 3x3: two output rows per thread for large launches, one for small ones
+      // (more blocks); 5x5: one (VF_EL_OPT=1|2 overrides for 3x3, for tuning)
+      const long long npix = (long long)B * out_rows * W;
+      int opt = (window == 3 && npix >= (1LL << 21)) ? 2 : 1;
+      static const int opt_env = [] { const char* e = std::getenv("VF_EL_OPT"); return e ? std::atoi(e) : 0; }();
+      if (window == 3 && (opt_env == 1 || opt_env == 2)) opt = opt_env;
+      if (window == 3 && (tile == 1 || tile == 2)) opt = tile;
+      kd->fn = window == 3 ? (opt == 2 ? el_kernel<3, 2>(crit, var) : el_kernel<3, 1>(crit, var)) : el_kernel<5, 1>(crit, var);
+      th = vf::TY * opt;
+    } else {
+      kd->fn = window == 3 ? window_kernel<3>(crit, var) : window_kernel<5>(crit, var);
+    }
     kd->grid = dim3((W + vf::TX - 1) / vf::TX, (out_rows + th - 1) / th, B);
     kd->block = dim3(vf::TX, vf::TY);
     kd->smem = 0;
@@ -161,7 +189,7 @@ int vf_filter_batch_algo(const uint8_t* imgs, int B, int H, int W, int window, i
   int rc = validate(B, H, W, window, criterion, variant);
   if (rc) return rc;
   if (!imgs || !outs) return fail(VF_EINVAL, "NULL image or output pointer");
-  if (algo < 0 || algo > 2) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
+  if (algo < 0 || (algo & 3) > 2 || algo > 15) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
   const size_t bytes = (size_t)B * H * W * 3;
   if (overlap(imgs, bytes, outs, bytes)) return fail(VF_EINVAL, "input and output overlap");
   const long long stride = (long long)H * W * 3;

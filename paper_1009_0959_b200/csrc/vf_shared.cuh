@@ -9,8 +9,9 @@
 // stored pair values, exactly as in Eq. 5, so results agree with the
 // per-window kernel and the oracle within the parity tolerance.
 //
-// Block = 256 threads over a 32 x PH region P of input pixels (PH = 24, i.e.
-// 3 pixels per thread); the output tile is the interior (32-2r) x (PH-2r).
+// Block = 256 threads over a 32 x PH region P of input pixels (PH = 8 PPT,
+// PPT = 1..3 pixels per thread); the output tile is the interior
+// (32-2r) x (PH-2r).
 //   stage   P (uint8 HWC, replicate-clamped) -> smem: packed RGB0, |x|^2, |x|
 //   phase A for every pair offset delta in the half plane (dy > 0, or dy = 0
 //           and dx > 0), |dy|,|dx| <= 2r, and every p in P:
@@ -36,11 +37,12 @@ namespace vf {
 namespace shared {
 
 constexpr int PW = 32;              // region width  (= warp width)
-constexpr int PH = 24;              // region height (3 pixels per thread)
-constexpr int NP = PW * PH;         // 768
 constexpr int PAD = 5 * PW;         // reads past the region stay in bounds
 constexpr int NTHR = 256;
-constexpr int PPT = NP / NTHR;      // pixels per thread (3)
+// PPT = region pixels per thread (1..3): region 32 x 8 PPT.  Large images use
+// PPT = 3 (least halo overhead), small ones fewer so more blocks fill the GPU.
+__host__ __device__ constexpr int region_h(int ppt) { return 8 * ppt; }
+__host__ __device__ constexpr int region_np(int ppt) { return PW * 8 * ppt; }
 
 __host__ __device__ constexpr int n_delta(int r) { return 4 * r * (2 * r + 1); }
 // offset index d -> (dy, dx): d < 2r: (0, d+1); else dy = 1 + (d-2r)/(4r+1), dx = -2r + (d-2r)%(4r+1)
@@ -68,19 +70,20 @@ __device__ __noinline__ bool angular_fixup(uint32_t pa, float nna, float nrma, u
 }
 
 // Per-block shared-memory state of the pair-sharing kernel.
-template <int GD>
+template <int GD, int PPT>
 struct SharedSmem {
-  uint4 px[shared::NP + shared::PAD];    // (packed RGB0, |x|^2 bits, |x| bits, 0): one LDS.128 per neighbour
-  float M[GD][shared::NP];
+  uint4 px[shared::region_np(PPT) + shared::PAD];   // (packed RGB0, |x|^2 bits, |x| bits, 0): one LDS.128 per neighbour
+  float M[GD][shared::region_np(PPT)];
 };
 
 // One group of GD offsets: phase A (pair maps) + rare fix-ups + phase C.
 // G is a template parameter so that every register index stays static.
-template <int WIN, int VAR, int GD, int OPT, int G>
-__device__ __forceinline__ void shared_group(SharedSmem<GD>& sm, const uint32_t (&my_pk)[shared::PPT],
-                                             const float (&my_nn)[shared::PPT], const float (&my_nrm)[shared::PPT],
+template <int WIN, int VAR, int GD, int OPT, int PPT, int G>
+__device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint32_t (&my_pk)[PPT],
+                                             const float (&my_nn)[PPT], const float (&my_nrm)[PPT],
                                              float (&Ra)[OPT][WIN * WIN], int tid, bool blk_zero) {
   using namespace shared;
+  constexpr int PH = region_h(PPT);
   constexpr int R = WIN / 2;
   constexpr int N = WIN * WIN;
   constexpr int TW = PW - 2 * R;
@@ -183,17 +186,19 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD>& sm, const uint32_t 
   }
 }
 
-template <int WIN, int VAR, int GD, int OPT, int... Gs>
-__device__ __forceinline__ void shared_groups(std::integer_sequence<int, Gs...>, SharedSmem<GD>& sm,
-                                              const uint32_t (&my_pk)[shared::PPT], const float (&my_nn)[shared::PPT],
-                                              const float (&my_nrm)[shared::PPT], float (&Ra)[OPT][WIN * WIN], int tid,
+template <int WIN, int VAR, int GD, int OPT, int PPT, int... Gs>
+__device__ __forceinline__ void shared_groups(std::integer_sequence<int, Gs...>, SharedSmem<GD, PPT>& sm,
+                                              const uint32_t (&my_pk)[PPT], const float (&my_nn)[PPT],
+                                              const float (&my_nrm)[PPT], float (&Ra)[OPT][WIN * WIN], int tid,
                                               bool blk_zero) {
-  (shared_group<WIN, VAR, GD, OPT, Gs>(sm, my_pk, my_nn, my_nrm, Ra, tid, blk_zero), ...);
+  (shared_group<WIN, VAR, GD, OPT, PPT, Gs>(sm, my_pk, my_nn, my_nrm, Ra, tid, blk_zero), ...);
 }
 
-template <int WIN, int VAR>
+template <int WIN, int VAR, int PPT>
 __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_shared_kernel(const Launch L) {
   using namespace shared;
+  constexpr int PH = region_h(PPT);
+  constexpr int NP = region_np(PPT);
   constexpr int R = WIN / 2;
   constexpr int N = WIN * WIN;
   constexpr int TW = PW - 2 * R;            // output tile width
@@ -203,8 +208,8 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
   constexpr int NG = ND / GD;
   constexpr int OPT = (TH + 7) / 8;         // outputs per thread (rows ty, ty+8, ty+16)
   static_assert(ND % GD == 0, "groups must tile the offsets");
-  extern __shared__ __align__(16) unsigned char smem_raw[];   // sizeof(SharedSmem<GD>), dynamic (> 48 KB)
-  SharedSmem<GD>& sm = *reinterpret_cast<SharedSmem<GD>*>(smem_raw);
+  extern __shared__ __align__(16) unsigned char smem_raw[];   // sizeof(SharedSmem<GD, PPT>), dynamic (> 48 KB)
+  SharedSmem<GD, PPT>& sm = *reinterpret_cast<SharedSmem<GD, PPT>*>(smem_raw);
 
   const int b = blockIdx.z;
   const int ox0 = blockIdx.x * TW;                        // output tile origin (global)
@@ -241,8 +246,8 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
 #pragma unroll
     for (int i = 0; i < N; ++i) Ra[k][i] = -0.0f;   // -0 + v == v: the first add folds away
 
-  shared_groups<WIN, VAR, GD, OPT>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, Ra, tid,
-                                   blk_zero);
+  shared_groups<WIN, VAR, GD, OPT, PPT>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, Ra, tid,
+                                        blk_zero);
 
   // ---- argmin + store ------------------------------------------------------------------
 #pragma unroll
@@ -260,32 +265,40 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
 }
 
 // Kernel + grid of the pair-sharing kernel for a launch (see vf_api.cu).
-inline const void* shared_kernel_fn(int window, int var) {
-  if (window == 3) return var == EXACT ? (const void*)vf_angular_shared_kernel<3, EXACT>
-                                       : (const void*)vf_angular_shared_kernel<3, MINIMAX>;
-  return var == EXACT ? (const void*)vf_angular_shared_kernel<5, EXACT> : (const void*)vf_angular_shared_kernel<5, MINIMAX>;
+template <int WIN, int PPT>
+inline const void* shared_kernel_fn_t(int var) {
+  return var == EXACT ? (const void*)vf_angular_shared_kernel<WIN, EXACT, PPT>
+                      : (const void*)vf_angular_shared_kernel<WIN, MINIMAX, PPT>;
 }
 
-inline size_t shared_smem_bytes(int window) {
-  return window == 3 ? sizeof(SharedSmem<12>) : sizeof(SharedSmem<10>);
+inline const void* shared_kernel_fn(int window, int var, int ppt) {
+  if (window == 3) return ppt == 1 ? shared_kernel_fn_t<3, 1>(var) : (ppt == 2 ? shared_kernel_fn_t<3, 2>(var)
+                                                                               : shared_kernel_fn_t<3, 3>(var));
+  return ppt == 1 ? shared_kernel_fn_t<5, 1>(var) : (ppt == 2 ? shared_kernel_fn_t<5, 2>(var) : shared_kernel_fn_t<5, 3>(var));
+}
+
+inline size_t shared_smem_bytes(int window, int ppt) {
+  if (window == 3) return ppt == 1 ? sizeof(SharedSmem<12, 1>) : (ppt == 2 ? sizeof(SharedSmem<12, 2>) : sizeof(SharedSmem<12, 3>));
+  return ppt == 1 ? sizeof(SharedSmem<10, 1>) : (ppt == 2 ? sizeof(SharedSmem<10, 2>) : sizeof(SharedSmem<10, 3>));
 }
 
 // Opt the kernels in to > 48 KB of dynamic shared memory (once per process).
 inline cudaError_t shared_set_attributes() {
   const int ws[2] = {3, 5};
   for (int w : ws)
-    for (int v = 0; v < 2; ++v) {
-      cudaError_t e = cudaFuncSetAttribute(shared_kernel_fn(w, v), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)shared_smem_bytes(w));
-      if (e != cudaSuccess) return e;
-    }
+    for (int ppt = 1; ppt <= 3; ++ppt)
+      for (int v = 0; v < 2; ++v) {
+        cudaError_t e = cudaFuncSetAttribute(shared_kernel_fn(w, v, ppt), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)shared_smem_bytes(w, ppt));
+        if (e != cudaSuccess) return e;
+      }
   return cudaSuccess;
 }
 
-inline dim3 shared_grid(const Launch& L, int B, int window) {
+inline dim3 shared_grid(const Launch& L, int B, int window, int ppt) {
   using namespace shared;
   const int R = window / 2;
-  const int TW = PW - 2 * R, TH = PH - 2 * R;
+  const int TW = PW - 2 * R, TH = region_h(ppt) - 2 * R;
   return dim3((L.W + TW - 1) / TW, (L.out_rows + TH - 1) / TH, B);
 }
 

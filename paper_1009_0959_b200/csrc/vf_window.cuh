@@ -22,7 +22,9 @@ namespace vf {
 
 constexpr int TX = 32;   // output tile width  (one warp per tile row)
 constexpr int TY = 8;    // output tile height (8 warps per block)
-__host__ __device__ constexpr int el_opt(int win) { return win == 3 ? 2 : 1; }  // exp/log: output rows per thread
+// exp/log kernel: output rows per thread (3x3, large launches: 2 -- shares
+// staging and, for the exact variants, 15 of 36 distances; small launches and
+// 5x5: 1)
 
 struct Launch {
   const uint8_t* in;   // global row band_row0 of image 0
@@ -166,11 +168,10 @@ __device__ __forceinline__ void el_window_nokeep(const Launch& L, int b, int ox,
   argmin_store<N>(L, b, ox, oy, Ra, ww);
 }
 
-template <int WIN, int CRIT, int VAR>
+template <int WIN, int CRIT, int VAR, int OPT>
 __global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
   constexpr int R = WIN / 2;
   constexpr int N = WIN * WIN;
-  constexpr int OPT = el_opt(WIN);             // output rows per thread (consecutive)
   constexpr int TYE = TY * OPT;                // output tile height
   constexpr int SW = TX + 2 * R;
   constexpr int SH = TYE + 2 * R;

@@ -86,6 +86,14 @@ def _var(v) -> int:
     return VARIANTS[v] if isinstance(v, str) else int(v)
 
 
+def _algo(a) -> int:
+    """'auto' | 'window' | 'shared' | int, optionally 'shared:2' / 'auto:1' (tile override, see vf.h)."""
+    if isinstance(a, str):
+        base, _, t = a.partition(":")
+        return ALGOS[base] | ((int(t) if t else 0) << 2)
+    return int(a)
+
+
 def _dev_u8(t: torch.Tensor, name: str):
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
@@ -122,7 +130,7 @@ def vf_filter_batch_algo(imgs: torch.Tensor, window: int, criterion, variant, al
                                    or not aggregates.is_cuda):
         raise ValueError("aggregates must be CUDA float32 with B*H*W*n elements")
     rc = L.vf_filter_batch_algo(_dev_u8(x, "imgs"), B, H, W, window, _crit(criterion), _var(variant),
-                                ALGOS[algo] if isinstance(algo, str) else int(algo),
+                                _algo(algo),
                                 _dev_u8(out, "out"), _ptr_or_none(index), _ptr_or_none(aggregates),
                                 _stream(stream))
     _check(rc, "vf_filter_batch_algo")

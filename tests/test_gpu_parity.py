@@ -31,9 +31,15 @@ def gpu_full(img_np, w, crit, var, algo="auto"):
 
 
 def full_parity(img_np, w, crit, var, algo=None):
-    """Both angular kernels (per-window and pair-sharing) are checked unless
-    `algo` is given; exp/log have one kernel."""
-    algos = ([algo] if algo else ["window", "shared"]) if crit == "angular" else ["auto"]
+    """Every kernel variant is checked unless `algo` is given: angular per-window
+    and pair-sharing with each region height (1..3 pixels per thread); exp/log
+    with 1 and (3x3) 2 output rows per thread."""
+    if algo:
+        algos = [algo]
+    elif crit == "angular":
+        algos = ["window", "shared:1", "shared:2", "shared:3"]
+    else:
+        algos = ["auto:1", "auto:2"] if w == 3 else ["auto"]
     _, o_idx, o_agg = oracle.filter_image(img_np, w, crit, var, want_agg=True)
     for a in algos:
         g_out, g_idx, g_agg = gpu_full(img_np, w, crit, var, a)

@@ -11,7 +11,9 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_1009_0959_b200 as vfb  # noqa: E402
 
-cfgs = [a for a in sys.argv[1:] if not a.startswith("--")] or ["C2", "C4", "C3"]
+args = sys.argv[1:]
+skip = {i + 1 for i, a in enumerate(args) if a in ("--algo", "--only")}
+cfgs = [a for i, a in enumerate(args) if not a.startswith("--") and i not in skip] or ["C2", "C4", "C3"]
 algo = "auto"
 if "--algo" in sys.argv:
     algo = sys.argv[sys.argv.index("--algo") + 1]
