@@ -16,6 +16,24 @@
 
 #include "vf_coeffs.cuh"
 
+// VF_CHECK: device-side bounds checks compiled in only for the debug build
+// (libvf_debug.so, `python -m paper_1009_0959_b200.build --debug`), which the
+// parity tests can load with VF_LIB=... to catch out-of-range smem / global
+// accesses (compute-sanitizer is not available on the GPU pool).
+#ifdef VF_DEBUG
+#include <cstdio>
+#define VF_CHECK(cond)                                                                         \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      printf("VF_CHECK failed: %s at %s:%d block (%d,%d,%d) thread (%d,%d)\n", #cond, __FILE__, \
+             __LINE__, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, threadIdx.y);         \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define VF_CHECK(cond) ((void)0)
+#endif
+
 namespace vf {
 
 enum { ANGULAR = 0, EXPC = 1, LOGC = 2 };

@@ -53,7 +53,8 @@ __device__ __forceinline__ void stage_packed(const Launch& L, const uint8_t* in,
                                              int SW, int SH) {
   constexpr int R = WIN / 2;
   for (int row = threadIdx.y; row < SH; row += TY) {
-    const int gy = clampi(y0 - R + row, 0, L.H - 1) - L.band_row0;
+    const int gy = clampi(y0 - R + row, L.band_row0, L.band_row0 + L.band_rows - 1) - L.band_row0;   // see pixel_ptr
+    VF_CHECK(gy >= 0 && gy < L.band_rows);
     const uint8_t* rp = in + (long long)gy * L.W * 3;
     for (int col = threadIdx.x; col < SW; col += TX) {
       const uint8_t* q = rp + clampi(x0 - R + col, 0, L.W - 1) * 3;
@@ -63,6 +64,7 @@ __device__ __forceinline__ void stage_packed(const Launch& L, const uint8_t* in,
 }
 
 __device__ __forceinline__ void store_pixel(const Launch& L, int b, int ox, int oy, uint32_t o, int idx) {
+  VF_CHECK(oy >= L.out_row0 && oy < L.out_row0 + L.out_rows && ox >= 0 && ox < L.W);
   const long long po = (long long)(oy - L.out_row0) * L.W + ox;
   uint8_t* op = L.out + (long long)b * L.out_stride + po * 3;
   op[0] = (uint8_t)(o & 0xff); op[1] = (uint8_t)((o >> 8) & 0xff); op[2] = (uint8_t)((o >> 16) & 0xff);

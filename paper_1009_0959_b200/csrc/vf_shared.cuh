@@ -103,6 +103,7 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
     for (int k = 0; k < PPT; ++k) {
       const int p = tid + NTHR * k;
       const int q = p + off;                                  // in bounds (PAD); garbage if outside P
+      VF_CHECK(q >= 0 && q < region_np(PPT) + PAD);
       const uint4 qv = sm.px[q];
       const uint32_t qk = qv.x;
       const float2 qn = make_float2(__uint_as_float(qv.y), __uint_as_float(qv.z));
@@ -176,6 +177,7 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
         for (int j = i + 1; j < N; ++j) {
           const int d = delta_index(R, j / WIN - i / WIN, j % WIN - i % WIN);
           if (d / GD == G) {
+            VF_CHECK(base + (i / WIN) * PW + (i % WIN) < region_np(PPT));
             const float v = sm.M[d - G * GD][base + (i / WIN) * PW + (i % WIN)];
             Ra[k][i] += v;
             Ra[k][j] += v;

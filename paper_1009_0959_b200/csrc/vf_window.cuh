@@ -40,8 +40,14 @@ struct Launch {
 
 // Pointer to the input pixel of global (clamped) coordinates (gy, gx).
 __device__ __forceinline__ const uint8_t* pixel_ptr(const Launch& L, const uint8_t* in, int gy, int gx) {
-  gy = clampi(gy, 0, L.H - 1) - L.band_row0;
+  // Replicate padding clamps to the GLOBAL rows [0, H); the band holds
+  // every clamped row a valid output reads (checked by vf_filter_rows), and
+  // rows a tile stages beyond the stripe's last output row are clamped into
+  // the band too (they feed no stored output).  band = [band_row0,
+  // band_row0 + band_rows) is inside [0, H), so one clamp does both.
+  gy = clampi(gy, L.band_row0, L.band_row0 + L.band_rows - 1) - L.band_row0;
   gx = clampi(gx, 0, L.W - 1);
+  VF_CHECK(gy >= 0 && gy < L.band_rows);
   return in + ((long long)gy * L.W + gx) * 3;
 }
 
@@ -58,6 +64,7 @@ __device__ __forceinline__ void argmin_store(const Launch& L, int b, int ox, int
   uint32_t o = pk[0];
 #pragma unroll
   for (int k = 1; k < N; ++k) o = (best == k) ? pk[k] : o;
+  VF_CHECK(oy >= L.out_row0 && oy < L.out_row0 + L.out_rows && ox >= 0 && ox < L.W);
   const long long po = (long long)(oy - L.out_row0) * L.W + ox;
   uint8_t* op = L.out + (long long)b * L.out_stride + po * 3;
   op[0] = (uint8_t)(o & 0xff); op[1] = (uint8_t)((o >> 8) & 0xff); op[2] = (uint8_t)((o >> 16) & 0xff);
@@ -185,7 +192,8 @@ __global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
   const int tx = threadIdx.x, ty = threadIdx.y;
   // a1 + a2: stage (rows per warp, columns per lane: no index division)
   for (int row = ty; row < SH; row += TY) {
-    const int gy = clampi(y0 - R + row, 0, L.H - 1) - L.band_row0;
+    const int gy = clampi(y0 - R + row, L.band_row0, L.band_row0 + L.band_rows - 1) - L.band_row0;   // see pixel_ptr
+    VF_CHECK(gy >= 0 && gy < L.band_rows);
     const uint8_t* rp = in + (long long)gy * L.W * 3;
 #pragma unroll
     for (int col = tx; col < SW; col += TX) {

@@ -13,7 +13,8 @@ from typing import Optional
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvf.so")
+# VF_LIB selects another build of the same ABI (e.g. libvf_debug.so with device bounds checks)
+LIB_PATH = os.environ.get("VF_LIB") or os.path.join(HERE, "libvf.so")
 
 VF_ANGULAR, VF_EXP, VF_LOG, VF_AMNFE, VF_AMNFG, VF_EVMF = 0, 1, 2, 3, 4, 5
 VF_EXACT, VF_MINIMAX, VF_MINIMAX_POLY4 = 0, 1, 2
