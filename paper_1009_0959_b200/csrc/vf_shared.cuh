@@ -54,27 +54,34 @@ __host__ __device__ constexpr int delta_index(int r, int dy, int dx) {
 
 }  // namespace shared
 
-// Exact re-evaluation of a flagged pair (rare path); returns true and the
-// value when it differs from the tau-branch value computed in phase A.
-template <int VAR>
-__device__ __noinline__ bool angular_fixup(uint32_t pa, float nna, float nrma, uint32_t pb, float nnb, float nrmb,
-                                           float* val) {
-  if (nna == 0.0f || nnb == 0.0f) { *val = 0.0f; return true; }
-  const float ra = (float)(pa & 0xff), ga = (float)((pa >> 8) & 0xff), ba = (float)(pa >> 16);
-  const float rb = (float)(pb & 0xff), gb = (float)((pb >> 8) & 0xff), bb = (float)(pb >> 16);
-  const AngGeo g = angular_geo(ra, ga, ba, nna, nrma, rb, gb, bb, nnb, nrmb);
-  if (!g.acos_branch) return false;                                       // phase A value stands
-  const float c = g.D / __fmul_rn(nrma, nrmb);                            // cos < 0.5
-  *val = (VAR == EXACT) ? acosf(c) : horner4(coef::ACOS(), c);
-  return true;
-}
-
 // Per-block shared-memory state of the pair-sharing kernel.
 template <int GD, int PPT>
 struct SharedSmem {
+  static constexpr int QCAP = 64;                   // rare-pair queue entries per warp
   uint4 px[shared::region_np(PPT) + shared::PAD];   // (packed RGB0, |x|^2 bits, |x| bits, 0): one LDS.128 per neighbour
   float M[GD][shared::region_np(PPT)];
+  uint32_t queue[shared::NTHR / 32][QCAP];          // flagged pairs of one warp: p | dl << 16
+  int off[40];                                      // region offset of pair offset d (d < n_delta(r) <= 40)
 };
+
+// Exact re-evaluation of a flagged pair (p, p + off) of offset slot dl: the
+// exact branch predicate 4D^2 < P; if the pair is on the
+// arccos branch (cos < 0.5), its map entry is replaced by the ARCCOS row /
+// acosf of cos = D / (|x_p||x_q|).  Zero vectors never get here (tau = 0 is
+// never flagged) and are handled by the block-uniform path anyway.
+template <int VAR, int GD, int PPT>
+__device__ __forceinline__ void angular_fix(SharedSmem<GD, PPT>& sm, int p, int dl, int d) {
+  const uint4 pv = sm.px[p], qv = sm.px[p + sm.off[d]];
+  const float D = __uint_as_float(__dp4a(pv.x, qv.x, F2P23_BITS)) - F2P23;   // exact dot
+  const float nna = __uint_as_float(pv.y), nnb = __uint_as_float(qv.y);
+  const float Ph = __fmul_rn(nna, nnb);
+  const float Pl = fmaf(nna, nnb, -Ph);                     // exact residual
+  const float t = fmaf(__fmul_rn(4.0f, D), D, -Ph);         // fl(4D^2 - Ph)
+  if (t < Pl) {                                             // 4D^2 < P, exact
+    const float c = D * rcp_approx(__fmul_rn(__uint_as_float(pv.z), __uint_as_float(qv.z)));
+    sm.M[dl][p] = (VAR == EXACT) ? acosf(c) : horner4(coef::ACOS(), c);
+  }
+}
 
 // One group of GD offsets: phase A (pair maps) + rare fix-ups + phase C.
 // G is a template parameter so that every register index stays static.
@@ -88,13 +95,13 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
   constexpr int N = WIN * WIN;
   constexpr int TW = PW - 2 * R;
   constexpr int TH = PH - 2 * R;
+  constexpr int QCAP = SharedSmem<GD, PPT>::QCAP;
   const int tx = tid & 31, ty = tid >> 5;
   if (G > 0) __syncthreads();   // previous phase C done with M (G = 0: the staging barrier)
   // ---- phase A: pair maps for offsets [G*GD, G*GD + GD) ------------------------------
-  constexpr int NFW = (GD * PPT + 31) / 32;                 // flag words
-  uint32_t flags[NFW];
+  uint32_t flags[PPT];                                      // bit dl: pair (p_k, p_k + delta) flagged
 #pragma unroll
-  for (int f = 0; f < NFW; ++f) flags[f] = 0u;
+  for (int k = 0; k < PPT; ++k) flags[k] = 0u;
 #pragma unroll
   for (int dl = 0; dl < GD; ++dl) {
     const int d = G * GD + dl;
@@ -123,26 +130,53 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
       // cos < 0.5 <=> tau > 1/sqrt2: flag a superset (margin 2^-10 >> the
       // ~5e-7 relative error of tau) for the exact decision below.  Offsets
       // reaching below the region read the zero padding: tau = 0, never flagged.
-      const bool rare = tau > 0.70641626f;                    // (1/sqrt2) (1 - 2^-10)
-      const int bit = dl * PPT + k;                           // compile-time after unrolling
-      if (rare) flags[bit / 32] |= 1u << (bit % 32);
+      if (tau > 0.70641626f) flags[k] |= 1u << dl;           // (1/sqrt2) (1 - 2^-10)
     }
   }
-  // rare pairs: exact branch decision (re-evaluated, then overwritten)
+  // ---- rare pairs: exact branch decision, warp-cooperative ---------------------------
+  // The flagged pairs of the warp (~1% of its pairs, spread over a few lanes)
+  // are compacted into a per-warp queue and re-evaluated one per lane, so the
+  // warp pays ~one fix-up pass instead of one per flagged pair of its busiest
+  // lane.  Entries beyond QCAP (adversarial images) fall back to per-lane loops.
+  {
+    const int lane = tx;
+    int cnt = 0;
 #pragma unroll
-  for (int f = 0; f < NFW; ++f) {
-    while (flags[f]) {
-      const int bit = 32 * f + __ffs(flags[f]) - 1;
-      flags[f] &= flags[f] - 1;
-      const int dl = bit / PPT, k = bit - dl * PPT;
-      const int d = G * GD + dl;
-      const int p = tid + NTHR * k;
-      const int q = p + delta_dy(R, d) * PW + delta_dx(R, d);
-      const uint4 pv = sm.px[p], qv = sm.px[q];
-      float v;
-      if (angular_fixup<VAR>(pv.x, __uint_as_float(pv.y), __uint_as_float(pv.z), qv.x, __uint_as_float(qv.y),
-                             __uint_as_float(qv.z), &v))
-        sm.M[dl][p] = v;
+    for (int k = 0; k < PPT; ++k) cnt += __popc(flags[k]);
+    if (__any_sync(0xffffffffu, cnt != 0)) {
+      int incl = cnt;                                         // inclusive warp scan of cnt
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      int pos = incl - cnt;
+      uint32_t* q = sm.queue[ty];
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const uint32_t p = tid + NTHR * k;
+        while (flags[k] && pos < QCAP) {
+          const uint32_t dl = __ffs(flags[k]) - 1;
+          flags[k] &= flags[k] - 1;
+          q[pos++] = p | (dl << 16);
+        }
+      }
+      __syncwarp();
+      const int nq = total < QCAP ? total : QCAP;
+      for (int e = lane; e < nq; e += 32) {
+        const uint32_t en = q[e];
+        angular_fix<VAR>(sm, (int)(en & 0xffffu), (int)(en >> 16), G * GD + (int)(en >> 16));
+      }
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {                         // overflow only
+        while (flags[k]) {
+          const int dl = __ffs(flags[k]) - 1;
+          flags[k] &= flags[k] - 1;
+          angular_fix<VAR>(sm, tid + NTHR * k, dl, G * GD + dl);
+        }
+      }
+      __syncwarp();                                           // queue reusable by the next group
     }
   }
   // zero vectors: block-uniform slow path, only in blocks that hold
@@ -166,6 +200,9 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
   }
   __syncthreads();
   // ---- phase C: accumulate the window aggregates ------------------------------------
+  // Rows past the output tile (TH not a multiple of 8) are skipped warp-
+  // uniformly; the aggregates start at -0 inside the branch so that the first
+  // addition of each folds away.
 #pragma unroll
   for (int k = 0; k < OPT; ++k) {
     const int oy = ty + 8 * k;
@@ -240,13 +277,14 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
     sm.px[p] = make_uint4(my_pk[k], __float_as_uint(nn), __float_as_uint(nrm), 0u);
   }
   if (tid < PAD) sm.px[NP + tid] = make_uint4(0u, 0u, 0u, 0u);
+  if (tid < ND) sm.off[tid] = delta_dy(R, tid) * PW + delta_dx(R, tid);
   const bool blk_zero = __syncthreads_or(has_zero) != 0;       // staging barrier
 
   float Ra[OPT][N];
 #pragma unroll
   for (int k = 0; k < OPT; ++k)
 #pragma unroll
-    for (int i = 0; i < N; ++i) Ra[k][i] = -0.0f;   // -0 + v == v: the first add folds away
+    for (int i = 0; i < N; ++i) Ra[k][i] = -0.0f;
 
   shared_groups<WIN, VAR, GD, OPT, PPT>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, Ra, tid,
                                         blk_zero);
@@ -257,11 +295,18 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
     const int oy = ty + 8 * k;
     const int gy = oy0 + oy, gx = ox0 + tx;
     if ((TH % 8 == 0 || oy < TH) && tx < TW && gx < L.W && gy < L.out_row0 + L.out_rows) {
-      uint32_t pk[N];
+      // argmin over the window (lowest index on ties), tracking the region
+      // offset of the selected sample, then one load of its packed RGB
       const int base = oy * PW + tx;
+      float bv = Ra[k][0];
+      int so = 0;
 #pragma unroll
-      for (int i = 0; i < N; ++i) pk[i] = sm.px[base + (i / WIN) * PW + (i % WIN)].x;
-      argmin_store<N>(L, b, gx, gy, Ra[k], pk);
+      for (int i = 1; i < N; ++i) {
+        const bool lt = Ra[k][i] < bv;
+        bv = lt ? Ra[k][i] : bv;
+        so = lt ? (i / WIN) * PW + (i % WIN) : so;
+      }
+      store_result<N>(L, b, gx, gy, Ra[k], sm.px[base + so].x);
     }
   }
 }

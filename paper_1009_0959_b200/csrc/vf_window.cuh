@@ -51,30 +51,43 @@ __device__ __forceinline__ const uint8_t* pixel_ptr(const Launch& L, const uint8
   return in + ((long long)gy * L.W + gx) * 3;
 }
 
-// a7 + a8: argmin (lowest index on ties) and store.
+// a7 + a8: argmin (lowest index on ties) and store.  The selected sample is
+// tracked directly (one FSETP + FSEL + SEL per candidate); its index is only
+// formed when the caller asked for it.
 template <int N>
-__device__ __forceinline__ void argmin_store(const Launch& L, int b, int ox, int oy, const float (&Ra)[N],
-                                             const uint32_t (&pk)[N]) {
-  int best = 0;
-  float bv = Ra[0];
-#pragma unroll
-  for (int k = 1; k < N; ++k) {
-    if (Ra[k] < bv) { bv = Ra[k]; best = k; }
-  }
-  uint32_t o = pk[0];
-#pragma unroll
-  for (int k = 1; k < N; ++k) o = (best == k) ? pk[k] : o;
+__device__ __forceinline__ void store_result(const Launch& L, int b, int ox, int oy, const float (&Ra)[N], uint32_t o) {
   VF_CHECK(oy >= L.out_row0 && oy < L.out_row0 + L.out_rows && ox >= 0 && ox < L.W);
   const long long po = (long long)(oy - L.out_row0) * L.W + ox;
   uint8_t* op = L.out + (long long)b * L.out_stride + po * 3;
   op[0] = (uint8_t)(o & 0xff); op[1] = (uint8_t)((o >> 8) & 0xff); op[2] = (uint8_t)((o >> 16) & 0xff);
   const long long npix_img = (long long)L.out_rows * L.W;
-  if (L.idx) L.idx[b * npix_img + po] = (uint8_t)best;
+  if (L.idx) {
+    int best = 0;
+    float bv = Ra[0];
+#pragma unroll
+    for (int k = 1; k < N; ++k)
+      if (Ra[k] < bv) { bv = Ra[k]; best = k; }
+    L.idx[b * npix_img + po] = (uint8_t)best;
+  }
   if (L.agg) {
     float* a = L.agg + (b * npix_img + po) * N;
 #pragma unroll
     for (int k = 0; k < N; ++k) a[k] = Ra[k];
   }
+}
+
+template <int N>
+__device__ __forceinline__ void argmin_store(const Launch& L, int b, int ox, int oy, const float (&Ra)[N],
+                                             const uint32_t (&pk)[N]) {
+  float bv = Ra[0];
+  uint32_t o = pk[0];
+#pragma unroll
+  for (int k = 1; k < N; ++k) {
+    const bool lt = Ra[k] < bv;   // strict: the lowest index wins exact ties
+    bv = lt ? Ra[k] : bv;
+    o = lt ? pk[k] : o;
+  }
+  store_result<N>(L, b, ox, oy, Ra, o);
 }
 
 // ============================================================================
