@@ -118,8 +118,8 @@ VF_API int vf_filter_rows(const uint8_t *band, int band_row0, int band_rows, int
 /* As vf_filter_batch with an explicit kernel choice: algo = a vf_algo value,
  * optionally | (t << 2) with t in 1..3 forcing the tile height (pixel rows
  * per thread) instead of the size-based choice: t pixels per thread of the
- * angular sharing kernel's region, t output rows per thread of the 3x3 exp/log
- * kernel (1..2).  Results are identical within the parity tolerance for every
+ * angular sharing kernel's region, output rows per thread of the 3x3 exp/log
+ * kernel (t = 1, 2, 3 -> 1, 2, 4 rows).  Results are identical within the parity tolerance for every
  * choice (tested); the knob exists for tuning and tests. */
 VF_API int vf_filter_batch_algo(const uint8_t *imgs, int B, int H, int W, int window, int criterion,
                          int variant, int algo, uint8_t *outs, uint8_t *index,

@@ -133,14 +133,18 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
   } else {
     int th = vf::TY;
     if (crit == VF_EXP || crit == VF_LOG) {
-      // 3x3: two output rows per thread for large launches, one for small ones
-      // (more blocks); 5x5: one (VF_EL_OPT=1|2 overrides for 3x3, for tuning)
+      // 3x3: 4 output rows per thread for large launches (staging and the S1
+      // row sums shared by 4 windows; exact variants 2, whose kept distances
+      // need the registers), 1 for small ones (more blocks); 5x5: 1.
+      // VF_EL_OPT=1|2|4 or the algo tile bits (1, 2, 3 -> 1, 2, 4) override.
       const long long npix = (long long)B * out_rows * W;
-      int opt = (window == 3 && npix >= (1LL << 21)) ? 2 : 1;
+      int opt = (window == 3 && npix >= (1LL << 21)) ? (var == VF_EXACT ? 2 : 4) : 1;
       static const int opt_env = [] { const char* e = std::getenv("VF_EL_OPT"); return e ? std::atoi(e) : 0; }();
-      if (window == 3 && (opt_env == 1 || opt_env == 2)) opt = opt_env;
-      if (window == 3 && (tile == 1 || tile == 2)) opt = tile;
-      kd->fn = window == 3 ? (opt == 2 ? el_kernel<3, 2>(crit, var) : el_kernel<3, 1>(crit, var)) : el_kernel<5, 1>(crit, var);
+      if (window == 3 && (opt_env == 1 || opt_env == 2 || opt_env == 4)) opt = opt_env;
+      if (window == 3 && tile) opt = tile == 3 ? 4 : tile;
+      kd->fn = window == 3 ? (opt == 4 ? el_kernel<3, 4>(crit, var)
+                                       : (opt == 2 ? el_kernel<3, 2>(crit, var) : el_kernel<3, 1>(crit, var)))
+                           : el_kernel<5, 1>(crit, var);
       th = vf::TY * opt;
     } else {
       kd->fn = window == 3 ? window_kernel<3>(crit, var) : window_kernel<5>(crit, var);

@@ -121,19 +121,35 @@ __device__ __forceinline__ float angular_pair(float ri, float gi, float bi, floa
 
 // ---- exp criterion D_E = 1 - E(z) (reading R2) --------------------------------
 // z = c_E * d1 never exceeds z*_n < 1, so the P:163 cutoff is dead code.
-template <int VAR>
-__device__ __forceinline__ float exp_crit(float z) {
-  if (VAR == EXACT) return -expm1f(-z);
-  if (VAR == MINIMAX) return horner4(coef::EXP_DELTA(), z) * rcp_approx(horner4(coef::EXP_Q(), z));
-  return horner4(coef::EXP_1MP4(), z);
-}
-
 // ---- log criterion D_L = -ENT(s), s = 1 - u (reading R3) -----------------------
 // u = c_L * d1 in [0, 1 - 1/e]; s >= 1/e > 0.05, so the P:232 cutoff is dead code.
-template <int VAR>
-__device__ __forceinline__ float log_crit(float u) {
-  if (VAR == EXACT) return -(1.0f - u) * log1pf(-u);
-  return horner4(coef::ENT_NEGN_U(), u) * rcp_approx(horner4(coef::ENT_Q_U(), u));
+//
+// crit_accumulate adds the pair's criterion value to both aggregates (a6).
+// Every rounding is spelled out (fmaf / __fadd_rn, which the compiler never
+// contracts), so all kernel instantiations (tile shapes, stripes, batches)
+// produce bit-identical aggregates for the same window.
+template <int CRIT, int VAR>
+__device__ __forceinline__ void crit_accumulate(float zu, float& Ri, float& Rj) {
+  if (VAR == MINIMAX) {
+    // exp: Delta(z) / Q(z) = 1 - N/Q;  log: -Ntilde(u) / Qtilde(u) = -ENT(1 - u)
+    const float num = CRIT == EXPC ? horner4(coef::EXP_DELTA(), zu) : horner4(coef::ENT_NEGN_U(), zu);
+    const float r = rcp_approx(CRIT == EXPC ? horner4(coef::EXP_Q(), zu) : horner4(coef::ENT_Q_U(), zu));
+    Ri = fmaf(num, r, Ri);
+    Rj = fmaf(num, r, Rj);
+  } else if (VAR == POLY4) {   // exp only: 1 - P4(z)
+    const float v = horner4(coef::EXP_1MP4(), zu);
+    Ri = __fadd_rn(Ri, v);
+    Rj = __fadd_rn(Rj, v);
+  } else if (CRIT == EXPC) {   // exact: 1 - exp(-z)
+    const float v = -expm1f(-zu);
+    Ri = __fadd_rn(Ri, v);
+    Rj = __fadd_rn(Rj, v);
+  } else {                     // exact: -s ln s = -(1 - u) log1p(-u)
+    const float ms = __fadd_rn(zu, -1.0f);   // -(1 - u), one rounding
+    const float l = log1pf(-zu);
+    Ri = fmaf(ms, l, Ri);
+    Rj = fmaf(ms, l, Rj);
+  }
 }
 
 }  // namespace vf

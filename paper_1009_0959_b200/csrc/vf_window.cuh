@@ -140,9 +140,7 @@ __device__ __forceinline__ void el_window(const Launch& L, int b, int ox, int oy
 #pragma unroll
       for (int j = i + 1; j < N; ++j, ++p) {
         const float zu = fmaf(sc, __uint_as_float(keep[p]), bias);  // c * d1, one rounding
-        const float v = CRIT == EXPC ? exp_crit<VAR>(zu) : log_crit<VAR>(zu);
-        Ra[i] += v;
-        Ra[j] += v;
+        crit_accumulate<CRIT, VAR>(zu, Ra[i], Ra[j]);
       }
     }
   }
@@ -152,40 +150,137 @@ __device__ __forceinline__ void el_window(const Launch& L, int b, int ox, int oy
   argmin_store<N>(L, b, ox, oy, Ra, ww);
 }
 
-// One exp/log window recomputing the distances in pass 2 (5x5: 300 pairs do
-// not fit in registers).
-template <int WIN, int CRIT, int VAR>
-__device__ __forceinline__ void el_window_nokeep(const Launch& L, int b, int ox, int oy, const uint32_t* w) {
-  constexpr int N = WIN * WIN;
-  uint32_t acc[4] = {0u, 0u, 0u, 0u};
+// a3 for a thread's column strip of OPT vertically adjacent windows (rows
+// 0..OPT+WIN-2 of samples w[row * WIN + col]): S1 of window o is the sum of
+// the intra-row pair sums T[r] of its rows and the cross-row sums C[r][dr] of
+// its row pairs, so the row pairs two windows share are summed once (3x3 with
+// 4 windows per thread: 99 instead of 144 VABSDIFF4).
+template <int WIN, int OPT>
+struct StripS1 {
+  static constexpr int LR = OPT + WIN - 1;
+  uint32_t T[LR];
+  uint32_t C[LR][WIN - 1];   // C[r][dr - 1]: pairs (row r, row r + dr)
+  __device__ __forceinline__ void build(const uint32_t* w) {
 #pragma unroll
-  for (int i = 0, p = 0; i < N; ++i) {
+    for (int r = 0; r < LR; ++r) {
+      uint32_t t = 0u;
 #pragma unroll
-    for (int j = i + 1; j < N; ++j, ++p) acc[p & 3] = sad4(w[i], w[j], acc[p & 3]);
-  }
-  const uint32_t S1 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-  float Ra[N];
+      for (int a = 0; a < WIN; ++a)
 #pragma unroll
-  for (int k = 0; k < N; ++k) Ra[k] = (S1 != 0u) ? -0.0f : 0.0f;
-  if (S1 != 0u) {
-    const float sc = L.kscale * rcp_approx((float)S1);
-    const float bias = -sc * F2P23;
+        for (int c = a + 1; c < WIN; ++c) t = sad4(w[r * WIN + a], w[r * WIN + c], t);
+      T[r] = t;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
+      for (int dr = 1; dr < WIN; ++dr) {
+        uint32_t x = 0u;
+        if (r + dr < LR) {
 #pragma unroll
-      for (int j = i + 1; j < N; ++j) {
-        const float fb = __uint_as_float(sad4(w[i], w[j], F2P23_BITS));   // 2^23 + d1
-        const float zu = fmaf(sc, fb, bias);                               // c * d1
-        const float v = CRIT == EXPC ? exp_crit<VAR>(zu) : log_crit<VAR>(zu);
-        Ra[i] += v;
-        Ra[j] += v;
+          for (int a = 0; a < WIN; ++a)
+#pragma unroll
+            for (int c = 0; c < WIN; ++c) x = sad4(w[r * WIN + a], w[(r + dr) * WIN + c], x);
+        }
+        C[r][dr - 1] = x;
       }
     }
   }
-  uint32_t ww[N];
+  __device__ __forceinline__ uint32_t window(int o) const {   // o compile-time after unrolling
+    uint32_t s = 0u;
 #pragma unroll
-  for (int k = 0; k < N; ++k) ww[k] = w[k];
-  argmin_store<N>(L, b, ox, oy, Ra, ww);
+    for (int r = 0; r < WIN; ++r) {
+      s += T[o + r];
+#pragma unroll
+      for (int dr = 1; dr < WIN - r; ++dr) s += C[o + r][dr - 1];
+    }
+    return s;
+  }
+};
+
+// One exp/log window recomputing the distances in pass 2, given S1.  A flat
+// window (S1 = 0, all samples equal) runs the same code with scale 0: every
+// pair then gets the same value D(0), all aggregates tie and the lowest index
+// (= the common sample) wins; the reported aggregates are 0 (reading R18).
+template <int WIN, int CRIT, int VAR>
+__device__ __forceinline__ void el_window_s1(const Launch& L, int b, int ox, int oy, const uint32_t* w, uint32_t S1) {
+  constexpr int N = WIN * WIN;
+  const float sc = (S1 != 0u) ? L.kscale * rcp_approx((float)S1) : 0.0f;   // c_E = 1/h_W, or c_L
+  const float bias = -sc * F2P23;                                         // exact
+  float Ra[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) Ra[k] = -0.0f;   // -0 + v == v: the first add folds away
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = i + 1; j < N; ++j) {
+      const float fb = __uint_as_float(sad4(w[i], w[j], F2P23_BITS));   // 2^23 + d1
+      const float zu = fmaf(sc, fb, bias);                               // c * d1, one rounding
+      crit_accumulate<CRIT, VAR>(zu, Ra[i], Ra[j]);
+    }
+  }
+  float bv = Ra[0];
+  uint32_t o = w[0];
+#pragma unroll
+  for (int k = 1; k < N; ++k) {
+    const bool lt = Ra[k] < bv;
+    bv = lt ? Ra[k] : bv;
+    o = lt ? w[k] : o;
+  }
+  if (L.agg && S1 == 0u) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) Ra[k] = 0.0f;
+  }
+  store_result<N>(L, b, ox, oy, Ra, o);
+}
+
+// a1 + a2: stage the block's SH x SW pixel region (global origin (gx0, gy0),
+// replicate-clamped against the image / band) as packed RGB0 words.
+// Interior regions (no clamping needed) are read as whole 32-bit words, one
+// warp per row (lane l loads word l of the row's byte range; the first and
+// last word may extend up to 3 bytes beyond the range but never beyond the
+// aligned words that hold its bytes), then repacked from shared memory with
+// one funnel shift per pixel.  Regions touching a border take the clamped
+// byte path.
+template <int SW, int SH>
+struct StageSmem {
+  static constexpr int RWW = (SW * 3 + 3 + 3) / 4 + 1;   // raw words per row (+1: the funnel shift's high word)
+  uint32_t pk[SH * SW];
+  uint32_t raw[SH * RWW];
+};
+
+template <int SW, int SH, int NTH_X, int NTH_Y>
+__device__ __forceinline__ void stage_packed(const Launch& L, const uint8_t* __restrict__ in, int gx0, int gy0,
+                                             StageSmem<SW, SH>& sm) {
+  constexpr int RWW = StageSmem<SW, SH>::RWW;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const bool inner = gx0 >= 0 && gx0 + SW <= L.W && gy0 >= L.band_row0 && gy0 + SH <= L.band_row0 + L.band_rows;
+  if (inner) {
+    const uint8_t* row0 = in + ((long long)(gy0 - L.band_row0) * L.W + gx0) * 3;
+    const long long rstride = (long long)L.W * 3;
+    for (int r = ty; r < SH; r += NTH_Y) {
+      const uintptr_t ra = (uintptr_t)(row0 + r * rstride);
+      const uint32_t* wp = (const uint32_t*)(ra & ~(uintptr_t)3);
+      const int nw = (int)(((ra & 3) + SW * 3 + 3) >> 2);   // words holding the row's bytes
+      for (int k = tx; k < nw; k += NTH_X) sm.raw[r * RWW + k] = __ldg(wp + k);
+    }
+    __syncthreads();
+    const int tid = ty * NTH_X + tx;
+    for (int p = tid; p < SH * SW; p += NTH_X * NTH_Y) {
+      const int r = p / SW, c = p - r * SW;
+      const int o = (int)((uintptr_t)(row0 + r * rstride) & 3) + 3 * c;
+      VF_CHECK((o >> 2) + 1 < RWW);
+      const uint32_t w0 = sm.raw[r * RWW + (o >> 2)], w1 = sm.raw[r * RWW + (o >> 2) + 1];
+      sm.pk[p] = __funnelshift_r(w0, w1, (o & 3) * 8) & 0x00ffffffu;
+    }
+  } else {
+    for (int row = ty; row < SH; row += NTH_Y) {
+      const int gy = clampi(gy0 + row, L.band_row0, L.band_row0 + L.band_rows - 1) - L.band_row0;   // see pixel_ptr
+      VF_CHECK(gy >= 0 && gy < L.band_rows);
+      const uint8_t* rp = in + (long long)gy * L.W * 3;
+      for (int col = tx; col < SW; col += NTH_X) {
+        const uint8_t* q = rp + clampi(gx0 + col, 0, L.W - 1) * 3;
+        sm.pk[row * SW + col] = pack_rgb(q[0], q[1], q[2]);
+      }
+    }
+  }
+  __syncthreads();
 }
 
 template <int WIN, int CRIT, int VAR, int OPT>
@@ -196,25 +291,14 @@ __global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
   constexpr int SW = TX + 2 * R;
   constexpr int SH = TYE + 2 * R;
   constexpr int LR = OPT + 2 * R;              // sample rows a thread reads
-  __shared__ uint32_t s_pk[SH * SW];
+  __shared__ StageSmem<SW, SH> sm;
 
   const int b = blockIdx.z;
   const int x0 = blockIdx.x * TX;
   const int y0 = L.out_row0 + blockIdx.y * TYE;
   const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  // a1 + a2: stage (rows per warp, columns per lane: no index division)
-  for (int row = ty; row < SH; row += TY) {
-    const int gy = clampi(y0 - R + row, L.band_row0, L.band_row0 + L.band_rows - 1) - L.band_row0;   // see pixel_ptr
-    VF_CHECK(gy >= 0 && gy < L.band_rows);
-    const uint8_t* rp = in + (long long)gy * L.W * 3;
-#pragma unroll
-    for (int col = tx; col < SW; col += TX) {
-      const uint8_t* q = rp + clampi(x0 - R + col, 0, L.W - 1) * 3;
-      s_pk[row * SW + col] = pack_rgb(q[0], q[1], q[2]);
-    }
-  }
-  __syncthreads();
+  stage_packed<SW, SH, TX, TY>(L, in, x0 - R, y0 - R, sm);
 
   const int ox = x0 + tx;
   const int oyb = y0 + OPT * ty;
@@ -222,7 +306,7 @@ __global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
 
   uint32_t pk[LR * WIN];
 #pragma unroll
-  for (int k = 0; k < LR * WIN; ++k) pk[k] = s_pk[(OPT * ty + k / WIN) * SW + tx + k % WIN];
+  for (int k = 0; k < LR * WIN; ++k) pk[k] = sm.pk[(OPT * ty + k / WIN) * SW + tx + k % WIN];
 
   const int rows_here = min(OPT, L.out_row0 + L.out_rows - oyb);   // >= 1
   if (N <= 9 && VAR == EXACT) {
@@ -237,9 +321,11 @@ __global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
     for (int o = 1; o < OPT; ++o)
       if (o < rows_here) el_window<WIN, CRIT, VAR, true>(L, b, ox, oyb + o, pk + o * WIN, keep);
   } else {
+    StripS1<WIN, OPT> s1;
+    s1.build(pk);
 #pragma unroll
     for (int o = 0; o < OPT; ++o)
-      if (o < rows_here) el_window_nokeep<WIN, CRIT, VAR>(L, b, ox, oyb + o, pk + o * WIN);
+      if (o < rows_here) el_window_s1<WIN, CRIT, VAR>(L, b, ox, oyb + o, pk + o * WIN, s1.window(o));
   }
 }
 
@@ -297,8 +383,8 @@ __global__ void __launch_bounds__(TX * TY) vf_angular_window_kernel(const Launch
     for (int j = i + 1; j < N; ++j) {
       const float d = angular_pair<VAR>(xr[i], xg[i], xb[i], xn[i], xm[i], xi[i],
                                         xr[j], xg[j], xb[j], xn[j], xm[j], xi[j]);
-      Ra[i] += d;
-      Ra[j] += d;
+      Ra[i] = __fadd_rn(Ra[i], d);   // never contracted with d's last product
+      Ra[j] = __fadd_rn(Ra[j], d);
     }
   }
   if (VAR != EXACT) {

@@ -39,7 +39,7 @@ def full_parity(img_np, w, crit, var, algo=None):
     elif crit == "angular":
         algos = ["window", "shared:1", "shared:2", "shared:3"]
     else:
-        algos = ["auto:1", "auto:2"] if w == 3 else ["auto"]
+        algos = ["auto:1", "auto:2", "auto:3"] if w == 3 else ["auto"]
     _, o_idx, o_agg = oracle.filter_image(img_np, w, crit, var, want_agg=True)
     for a in algos:
         g_out, g_idx, g_agg = gpu_full(img_np, w, crit, var, a)
@@ -80,6 +80,34 @@ def test_ragged_sizes(crit, var, w):
             continue
         x = vfsynth.random_image(11 + H, H, W)
         full_parity(x, w, crit, var)
+
+
+@pytest.mark.parametrize("crit,var", CV)
+@pytest.mark.parametrize("w", [3, 5])
+def test_misaligned_rows_and_image_bases(crit, var, w):
+    """Interior tiles are staged as whole 32-bit words: cover row strides that
+    are not a multiple of 4 bytes (W = 131, 3W = 393), batches whose images
+    start at odd byte offsets (H*W*3 odd), and an input starting at byte 1 of
+    its allocation -- against the oracle and bit-exact between layouts."""
+    x = vfsynth.random_image(31, 75, 131)
+    full_parity(x, w, crit, var)
+    g_out, g_idx, g_agg = gpu_full(x, w, crit, var)
+    buf = torch.zeros(x.size + 1, dtype=torch.uint8, device="cuda")
+    xv = buf[1:].view(x.shape)
+    xv.copy_(torch.from_numpy(x))
+    out, idx, agg = vfb.filter(xv, w, crit, var, want_index=True, want_agg=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), g_out)
+    assert np.array_equal(idx.cpu().numpy(), g_idx)
+    assert np.array_equal(agg.cpu().numpy(), g_agg)
+    xb = np.stack([vfsynth.random_image(40 + b, 41, 101) for b in range(3)])   # 41*101*3 = 12423 (odd)
+    ob, ib, ab = vfb.filter(torch.from_numpy(xb).cuda(), w, crit, var, want_index=True, want_agg=True)
+    torch.cuda.synchronize()
+    for b in range(3):
+        e_out, e_idx, e_agg = gpu_full(xb[b], w, crit, var)
+        assert np.array_equal(ob[b].cpu().numpy(), e_out)
+        assert np.array_equal(ib[b].cpu().numpy(), e_idx)
+        assert np.array_equal(ab[b].cpu().numpy(), e_agg)
 
 
 @pytest.mark.parametrize("crit,var", CV)
