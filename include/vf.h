@@ -90,8 +90,11 @@ typedef enum { VF_OK = 0, VF_EINVAL = -1, VF_EUNSUPPORTED = -2, VF_ECUDA = -3 } 
 /* Kernel selection for the angular criterion (both variants are window
  * independent, so pairs may be shared between overlapping windows,
  * SURVEY.md 8(f1)).  VF_ALGO_AUTO picks the fastest; results are identical
- * within the parity tolerance either way. */
-typedef enum { VF_ALGO_AUTO = 0, VF_ALGO_WINDOW = 1, VF_ALGO_SHARED = 2 } vf_algo;
+ * within the parity tolerance either way.  VF_ALGO_NO_TMA (or-ed in) keeps the
+ * exp/log criteria on the plain-load kernel instead of the persistent
+ * TMA-staged one (which needs 16-byte aligned rows: 3W % 16 == 0, a 16-byte
+ * aligned base and batch stride); the two give bit-identical results. */
+typedef enum { VF_ALGO_AUTO = 0, VF_ALGO_WINDOW = 1, VF_ALGO_SHARED = 2, VF_ALGO_NO_TMA = 16 } vf_algo;
 
 /* One image.  img, out: device [H][W][3]; index: device [H][W] or NULL;
  * aggregates: device [H][W][n] or NULL. */

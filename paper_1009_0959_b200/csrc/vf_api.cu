@@ -3,9 +3,12 @@
 // CUDA graph of parallel filter kernels) and error reporting.  Host code only
 // launches; every step of the filter runs in the kernels of vf_window.cuh /
 // vf_shared.cuh.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cmath>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -16,6 +19,7 @@
 #include "vf_paper.cuh"
 #include "vf_shared.cuh"
 #include "vf_stats.cuh"
+#include "vf_tma.cuh"
 #include "vf_window.cuh"
 
 namespace {
@@ -47,7 +51,45 @@ struct KernelDesc {
   dim3 grid, block;
   size_t smem;   // dynamic shared memory bytes
   Launch L;
+  bool tma = false;          // vf_el_tma_kernel: (map, L, tiles_x, tiles_y, ntiles)
+  alignas(64) CUtensorMap map;
+  int tiles_x = 0, tiles_y = 0, ntiles = 0;
+  void* args[5];
+  void** params() {
+    if (!tma) { args[0] = &L; return args; }
+    args[0] = &map; args[1] = &L; args[2] = &tiles_x; args[3] = &tiles_y; args[4] = &ntiles;
+    return args;
+  }
 };
+
+// cuTensorMapEncodeTiled from the driver (no -lcuda link: runtime entry point).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }();
+  return fn;
+}
+
+// Resident blocks per SM x SMs of the current device for a kernel (cached).
+int persistent_blocks(const void* fn, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : cache)
+    if (e.first.first == fn && e.first.second == dev) return e.second;
+  int per_sm = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1) per_sm = 1;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 1;
+  cache.push_back({{fn, dev}, per_sm * sms});
+  return per_sm * sms;
+}
 
 // One-time per-process kernel attribute setup (thread-safe).
 cudaError_t ensure_attributes() {
@@ -64,6 +106,18 @@ const void* el_kernel(int crit, int var) {
     return (const void*)vf_el_kernel<WIN, EXPC, POLY4, OPT>;
   }
   return var == EXACT ? (const void*)vf_el_kernel<WIN, LOGC, EXACT, OPT> : (const void*)vf_el_kernel<WIN, LOGC, MINIMAX, OPT>;
+}
+
+template <int WIN, int OPT>
+const void* el_tma_kernel(int crit, int var) {
+  using namespace vf;
+  if (crit == EXPC) {
+    if (var == EXACT) return (const void*)vf_el_tma_kernel<WIN, EXPC, EXACT, OPT>;
+    if (var == MINIMAX) return (const void*)vf_el_tma_kernel<WIN, EXPC, MINIMAX, OPT>;
+    return (const void*)vf_el_tma_kernel<WIN, EXPC, POLY4, OPT>;
+  }
+  return var == EXACT ? (const void*)vf_el_tma_kernel<WIN, LOGC, EXACT, OPT>
+                      : (const void*)vf_el_tma_kernel<WIN, LOGC, MINIMAX, OPT>;
 }
 
 template <int WIN>
@@ -115,6 +169,7 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
   L.out_row0 = out_row0; L.out_rows = out_rows;
   L.kscale = kscale(crit, window);
   const int tile = (algo >> 2) & 3;   // 0 = by size; 1..3 = forced rows per thread (tuning / tests)
+  const bool no_tma = (algo & VF_ALGO_NO_TMA) != 0;
   algo &= 3;
   if (crit == VF_ANGULAR && algo != VF_ALGO_WINDOW) {
     // region height: 3 pixels per thread measured fastest at every size
@@ -145,6 +200,43 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
       kd->fn = window == 3 ? (opt == 4 ? el_kernel<3, 4>(crit, var)
                                        : (opt == 2 ? el_kernel<3, 2>(crit, var) : el_kernel<3, 1>(crit, var)))
                            : el_kernel<5, 1>(crit, var);
+      // persistent TMA-staged kernel when the rows are 16-byte aligned
+      static const bool env_no_tma = [] { const char* e = std::getenv("VF_NO_TMA"); return e && e[0] == '1'; }();
+      const unsigned long long row_bytes = (unsigned long long)W * 3;
+      PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
+      // (measured on C3/C4: a few % faster for the 3x3 polynomial variants
+      // with 4 rows per thread; slower for the libm variants and 5x5, whose
+      // register budget the persistent loop tightens -- those stay on the
+      // plain-load kernel unless the caller forces it, for tests, with algo tile bits)
+      const bool tma_pays = window == 3 && var != VF_EXACT && opt == 4;
+      static const bool env_force_tma = [] { const char* e = std::getenv("VF_FORCE_TMA"); return e && e[0] == '1'; }();
+      if ((tma_pays || env_force_tma || tile) && !no_tma && !env_no_tma && enc && row_bytes % 16 == 0 && ((uintptr_t)in % 16) == 0 &&
+          (B == 1 || in_stride % 16 == 0) && row_bytes < (1ULL << 32)) {
+        const int tye = vf::TY * opt;
+        const cuuint64_t dims[3] = {row_bytes, (cuuint64_t)band_rows, (cuuint64_t)B};
+        const cuuint64_t strides[2] = {row_bytes, (cuuint64_t)(B == 1 ? row_bytes * band_rows : in_stride)};
+        const cuuint32_t box[3] = {(cuuint32_t)vf::tma::BOXW, (cuuint32_t)(tye + 2 * (window / 2)), 1u};
+        const cuuint32_t estr[3] = {1u, 1u, 1u};
+        CUresult cr = enc(&kd->map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)in, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr == CUDA_SUCCESS) {
+          kd->tma = true;
+          kd->fn = window == 3 ? (opt == 4 ? el_tma_kernel<3, 4>(crit, var)
+                                           : (opt == 2 ? el_tma_kernel<3, 2>(crit, var) : el_tma_kernel<3, 1>(crit, var)))
+                               : el_tma_kernel<5, 1>(crit, var);
+          kd->tiles_x = (W + vf::TX - 1) / vf::TX;
+          kd->tiles_y = (out_rows + tye - 1) / tye;
+          const long long nt = (long long)B * kd->tiles_x * kd->tiles_y;
+          if (nt > (1LL << 30)) return fail(VF_EINVAL, "too many tiles (%lld)", nt);
+          kd->ntiles = (int)nt;
+          const int cap = persistent_blocks(kd->fn, vf::TX * vf::TY, 0);
+          kd->grid = dim3(kd->ntiles < cap ? kd->ntiles : cap);
+          kd->block = dim3(vf::TX, vf::TY);
+          kd->smem = 0;
+          return VF_OK;
+        }
+      }
       th = vf::TY * opt;
     } else {
       kd->fn = window == 3 ? window_kernel<3>(crit, var) : window_kernel<5>(crit, var);
@@ -160,8 +252,7 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
 }
 
 int launch_desc(KernelDesc& kd, cudaStream_t st) {
-  void* args[] = {&kd.L};
-  cudaError_t e = cudaLaunchKernel(kd.fn, kd.grid, kd.block, args, kd.smem, st);
+  cudaError_t e = cudaLaunchKernel(kd.fn, kd.grid, kd.block, kd.params(), kd.smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return VF_OK;
 }
@@ -193,7 +284,7 @@ int vf_filter_batch_algo(const uint8_t* imgs, int B, int H, int W, int window, i
   int rc = validate(B, H, W, window, criterion, variant);
   if (rc) return rc;
   if (!imgs || !outs) return fail(VF_EINVAL, "NULL image or output pointer");
-  if (algo < 0 || (algo & 3) > 2 || algo > 15) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
+  if (algo < 0 || (algo & 3) > 2 || algo > 31) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
   const size_t bytes = (size_t)B * H * W * 3;
   if (overlap(imgs, bytes, outs, bytes)) return fail(VF_EINVAL, "input and output overlap");
   const long long stride = (long long)H * W * 3;
@@ -295,13 +386,12 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
     int rc = describe(&kd, d_in, stride, 0, H, B, H, W, 0, H, window, criteria[i], variants[i], VF_ALGO_AUTO,
                       d_outs[i], stride, nullptr, nullptr);
     if (rc) return bail(rc);
-    void* args[] = {&kd.L};
     cudaKernelNodeParams kp = {};
     kp.func = (void*)kd.fn;
     kp.gridDim = kd.grid;
     kp.blockDim = kd.block;
     kp.sharedMemBytes = (unsigned)kd.smem;
-    kp.kernelParams = args;
+    kp.kernelParams = kd.params();
     cudaGraphNode_t kn;
     e = cudaGraphAddKernelNode(&kn, p->graph, h2d ? &h2d : nullptr, h2d ? 1 : 0, &kp);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddKernelNode"));

@@ -13,6 +13,8 @@
 // tau = sqrt(1 - cos) keeps full relative precision for near-parallel pairs.
 #pragma once
 #include <cstdint>
+#include <type_traits>
+#include <utility>
 
 #include "vf_coeffs.cuh"
 
@@ -68,6 +70,36 @@ constexpr float F2P23 = 8388608.0f;
 __device__ __forceinline__ uint32_t pack_rgb(uint32_t r, uint32_t g, uint32_t b) { return r | (g << 8) | (b << 16); }
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// Pair p of the raster enumeration (0,1), (0,2), ..., (0,N-1), (1,2), ... of
+// the i < j pairs of N samples.
+template <int N>
+__host__ __device__ constexpr int pair_i(int p) {
+  int i = 0;
+  while (p >= N - 1 - i) { p -= N - 1 - i; ++i; }
+  return i;
+}
+template <int N>
+__host__ __device__ constexpr int pair_j(int p) {
+  int i = 0;
+  while (p >= N - 1 - i) { p -= N - 1 - i; ++i; }
+  return i + 1 + p;
+}
+template <int N>
+__host__ __device__ constexpr int pair_index(int i, int j) { return i * N - i * (i + 1) / 2 + (j - i - 1); }
+
+// Compile-time loop: f(std::integral_constant<int, k>) for k = 0..K-1, in
+// order.  Used for the pair loops so that every register index is static in
+// every kernel instantiation (the unroller's heuristics gave up on some of
+// them inside the persistent TMA kernel, demoting aggregates to local memory).
+template <typename F, int... Ks>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, Ks...>) {
+  (f(std::integral_constant<int, Ks>{}), ...);
+}
+template <int K, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, K>{});
+}
 
 __device__ __forceinline__ float horner4(const coef::P4f p, float x) {
   return fmaf(fmaf(fmaf(fmaf(p.a4, x, p.a3), x, p.a2), x, p.a1), x, p.a0);

@@ -106,28 +106,21 @@ __device__ __forceinline__ void el_window(const Launch& L, int b, int ox, int oy
   constexpr int N = WIN * WIN;
   constexpr int NPR = N * (N - 1) / 2;
   if (SHIFTED) {
-    uint32_t nk[NPR];
-#pragma unroll
-    for (int p = 0; p < NPR; ++p) nk[p] = keep[p];
-#pragma unroll
-    for (int i = 0, p = 0; i < N; ++i)
-#pragma unroll
-      for (int j = i + 1; j < N; ++j, ++p)
-        if (j < N - WIN) {
-          const int a = i + WIN, c = j + WIN;
-          keep[p] = nk[a * N - a * (a + 1) / 2 + (c - a - 1)];
-        }
+    // pairs of rows 1..WIN-1 of the previous window move to rows 0..WIN-2
+    static_for<NPR>([&](auto pc) {
+      constexpr int p = decltype(pc)::value;
+      constexpr int i = pair_i<N>(p), j = pair_j<N>(p);
+      if constexpr (j < N - WIN) keep[p] = keep[pair_index<N>(i + WIN, j + WIN)];   // source index > p: not yet overwritten
+    });
   }
   // a3: S1 = sum - NPR * 0x4B000000 (mod 2^32; exact integer)
   uint32_t acc[3] = {0u, 0u, 0u};
-#pragma unroll
-  for (int i = 0, p = 0; i < N; ++i) {
-#pragma unroll
-    for (int j = i + 1; j < N; ++j, ++p) {
-      if (!SHIFTED || j >= N - WIN) keep[p] = sad4(w[i], w[j], F2P23_BITS);
-      acc[p % 3] += keep[p];
-    }
-  }
+  static_for<NPR>([&](auto pc) {
+    constexpr int p = decltype(pc)::value;
+    constexpr int i = pair_i<N>(p), j = pair_j<N>(p);
+    if constexpr (!SHIFTED || j >= N - WIN) keep[p] = sad4(w[i], w[j], F2P23_BITS);
+    acc[p % 3] += keep[p];
+  });
   const uint32_t S1 = (acc[0] + acc[1]) + acc[2] - (uint32_t)(NPR * F2P23_BITS);
   float Ra[N];
 #pragma unroll
@@ -135,14 +128,11 @@ __device__ __forceinline__ void el_window(const Launch& L, int b, int ox, int oy
   if (S1 != 0u) {                                                   // flat window: all D = 0 (R18)
     const float sc = L.kscale * rcp_approx((float)S1);              // c_E = 1/h_W, or c_L
     const float bias = -sc * F2P23;                                 // exact
-#pragma unroll
-    for (int i = 0, p = 0; i < N; ++i) {
-#pragma unroll
-      for (int j = i + 1; j < N; ++j, ++p) {
-        const float zu = fmaf(sc, __uint_as_float(keep[p]), bias);  // c * d1, one rounding
-        crit_accumulate<CRIT, VAR>(zu, Ra[i], Ra[j]);
-      }
-    }
+    static_for<NPR>([&](auto pc) {
+      constexpr int p = decltype(pc)::value;
+      const float zu = fmaf(sc, __uint_as_float(keep[p]), bias);   // c * d1, one rounding
+      crit_accumulate<CRIT, VAR>(zu, Ra[pair_i<N>(p)], Ra[pair_j<N>(p)]);
+    });
   }
   uint32_t ww[N];
 #pragma unroll
@@ -206,15 +196,12 @@ __device__ __forceinline__ void el_window_s1(const Launch& L, int b, int ox, int
   float Ra[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) Ra[k] = -0.0f;   // -0 + v == v: the first add folds away
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-#pragma unroll
-    for (int j = i + 1; j < N; ++j) {
-      const float fb = __uint_as_float(sad4(w[i], w[j], F2P23_BITS));   // 2^23 + d1
-      const float zu = fmaf(sc, fb, bias);                               // c * d1, one rounding
-      crit_accumulate<CRIT, VAR>(zu, Ra[i], Ra[j]);
-    }
-  }
+  static_for<N * (N - 1) / 2>([&](auto pc) {
+    constexpr int i = pair_i<N>(decltype(pc)::value), j = pair_j<N>(decltype(pc)::value);
+    const float fb = __uint_as_float(sad4(w[i], w[j], F2P23_BITS));   // 2^23 + d1
+    const float zu = fmaf(sc, fb, bias);                               // c * d1, one rounding
+    crit_accumulate<CRIT, VAR>(zu, Ra[i], Ra[j]);
+  });
   float bv = Ra[0];
   uint32_t o = w[0];
 #pragma unroll
@@ -283,30 +270,22 @@ __device__ __forceinline__ void stage_packed(const Launch& L, const uint8_t* __r
   __syncthreads();
 }
 
+// a2-a8 for one staged tile: thread (tx, ty) reads its (OPT + w - 1) x w
+// samples (packed RGB0, region row-major with row length TX + w - 1) and
+// produces outputs (x0 + tx, y0 + OPT ty + o), o < OPT.
 template <int WIN, int CRIT, int VAR, int OPT>
-__global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
-  constexpr int R = WIN / 2;
+__device__ __forceinline__ void el_compute_tile(const Launch& L, int b, int x0, int y0, const uint32_t* s_pk) {
   constexpr int N = WIN * WIN;
-  constexpr int TYE = TY * OPT;                // output tile height
-  constexpr int SW = TX + 2 * R;
-  constexpr int SH = TYE + 2 * R;
-  constexpr int LR = OPT + 2 * R;              // sample rows a thread reads
-  __shared__ StageSmem<SW, SH> sm;
-
-  const int b = blockIdx.z;
-  const int x0 = blockIdx.x * TX;
-  const int y0 = L.out_row0 + blockIdx.y * TYE;
-  const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
+  constexpr int SW = TX + WIN - 1;
+  constexpr int LR = OPT + WIN - 1;            // sample rows a thread reads
   const int tx = threadIdx.x, ty = threadIdx.y;
-  stage_packed<SW, SH, TX, TY>(L, in, x0 - R, y0 - R, sm);
-
   const int ox = x0 + tx;
   const int oyb = y0 + OPT * ty;
   if (ox >= L.W || oyb >= L.out_row0 + L.out_rows) return;
 
   uint32_t pk[LR * WIN];
 #pragma unroll
-  for (int k = 0; k < LR * WIN; ++k) pk[k] = sm.pk[(OPT * ty + k / WIN) * SW + tx + k % WIN];
+  for (int k = 0; k < LR * WIN; ++k) pk[k] = s_pk[(OPT * ty + k / WIN) * SW + tx + k % WIN];
 
   const int rows_here = min(OPT, L.out_row0 + L.out_rows - oyb);   // >= 1
   if (N <= 9 && VAR == EXACT) {
@@ -327,6 +306,23 @@ __global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
     for (int o = 0; o < OPT; ++o)
       if (o < rows_here) el_window_s1<WIN, CRIT, VAR>(L, b, ox, oyb + o, pk + o * WIN, s1.window(o));
   }
+}
+
+template <int WIN, int CRIT, int VAR, int OPT>
+__global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
+  constexpr int R = WIN / 2;
+  constexpr int TYE = TY * OPT;                // output tile height
+  constexpr int SW = TX + 2 * R;
+  constexpr int SH = TYE + 2 * R;
+  __shared__ StageSmem<SW, SH> sm;
+
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * TX;
+  const int y0 = L.out_row0 + blockIdx.y * TYE;
+  const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
+  stage_packed<SW, SH, TX, TY>(L, in, x0 - R, y0 - R, sm);
+
+  el_compute_tile<WIN, CRIT, VAR, OPT>(L, b, x0, y0, sm.pk);
 }
 
 // ============================================================================

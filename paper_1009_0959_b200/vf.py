@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("VF_LIB") or os.path.join(HERE, "libvf.so")
 VF_ANGULAR, VF_EXP, VF_LOG, VF_AMNFE, VF_AMNFG, VF_EVMF = 0, 1, 2, 3, 4, 5
 VF_EXACT, VF_MINIMAX, VF_MINIMAX_POLY4 = 0, 1, 2
 VF_OK, VF_EINVAL, VF_EUNSUPPORTED, VF_ECUDA = 0, -1, -2, -3
-VF_ALGO_AUTO, VF_ALGO_WINDOW, VF_ALGO_SHARED = 0, 1, 2
+VF_ALGO_AUTO, VF_ALGO_WINDOW, VF_ALGO_SHARED, VF_ALGO_NO_TMA = 0, 1, 2, 16
 
 CRITERIA = {"angular": VF_ANGULAR, "exp": VF_EXP, "log": VF_LOG, "amnfe": VF_AMNFE, "amnfg": VF_AMNFG,
             "evmf": VF_EVMF}
@@ -88,10 +88,14 @@ def _var(v) -> int:
 
 
 def _algo(a) -> int:
-    """'auto' | 'window' | 'shared' | int, optionally 'shared:2' / 'auto:1' (tile override, see vf.h)."""
+    """'auto' | 'window' | 'shared' | int, optionally 'shared:2' / 'auto:1' (tile override, see vf.h)
+    and/or a '+notma' suffix (VF_ALGO_NO_TMA)."""
     if isinstance(a, str):
+        a, plus, flag = a.partition("+")
+        if plus and flag != "notma":
+            raise ValueError(f"unknown algo flag {flag!r}")
         base, _, t = a.partition(":")
-        return ALGOS[base] | ((int(t) if t else 0) << 2)
+        return ALGOS[base] | ((int(t) if t else 0) << 2) | (VF_ALGO_NO_TMA if plus else 0)
     return int(a)
 
 

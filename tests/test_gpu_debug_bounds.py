@@ -21,7 +21,7 @@ def test_all_kernels_under_bounds_checks():
     if not os.path.exists(DEBUG_LIB):
         from paper_1009_0959_b200 import build
         build.build(debug=True)
-    env = dict(os.environ, VF_LIB=DEBUG_LIB)
+    env = dict(os.environ, VF_LIB=DEBUG_LIB, VF_FORCE_TMA="1")   # stripes and "auto" through the TMA kernel too
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_driver.py")], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

@@ -3,6 +3,7 @@ same seeded inputs, with the acceptance rule of tests/parity.py (aggregates
 within 1e-5 relative, selected index exact unless the oracle's candidates are
 within 1e-5 relative, output = the window sample at the selected index)."""
 import dataclasses
+import os
 
 import numpy as np
 import pytest
@@ -39,7 +40,10 @@ def full_parity(img_np, w, crit, var, algo=None):
     elif crit == "angular":
         algos = ["window", "shared:1", "shared:2", "shared:3"]
     else:
-        algos = ["auto:1", "auto:2", "auto:3"] if w == 3 else ["auto"]
+        # tile bits force the TMA-staged kernel where the rows allow it (3W % 16 == 0);
+        # "+notma" the plain-load one
+        algos = ["auto", "auto:1", "auto:2", "auto:3"] if w == 3 else ["auto", "auto:1"]
+        algos += [a + "+notma" for a in algos[1:]]
     _, o_idx, o_agg = oracle.filter_image(img_np, w, crit, var, want_agg=True)
     for a in algos:
         g_out, g_idx, g_agg = gpu_full(img_np, w, crit, var, a)
@@ -108,6 +112,42 @@ def test_misaligned_rows_and_image_bases(crit, var, w):
         assert np.array_equal(ob[b].cpu().numpy(), e_out)
         assert np.array_equal(ib[b].cpu().numpy(), e_idx)
         assert np.array_equal(ab[b].cpu().numpy(), e_agg)
+
+
+@pytest.mark.parametrize("crit,var", [c for c in CV if c[0] != "angular"])
+@pytest.mark.parametrize("w", [3, 5])
+def test_tma_path_borders_batches_stripes(crit, var, w):
+    """The persistent TMA-staged exp/log kernel (3W % 16 == 0): ragged tile
+    tails in both directions, border tiles (zero-filled box + replicate
+    clamp), a batch (3-D tensor map), row stripes (band-relative rows) -- all
+    bit-identical to the plain-load kernel, and the image against the oracle."""
+    x = vfsynth.random_image(51, 77, 144)            # 3*144 = 432 = 27*16
+    full_parity(x, w, crit, var)
+    for a in (["auto:1", "auto:2", "auto:3"] if w == 3 else ["auto:1"]):
+        t = gpu_full(x, w, crit, var, a)
+        n = gpu_full(x, w, crit, var, a + "+notma")
+        for u, v in zip(t, n):
+            assert np.array_equal(u, v), a
+    xb = np.stack([vfsynth.random_image(60 + b, 45, 96) for b in range(3)])
+    ob, ib, ab = vfb.filter(torch.from_numpy(xb).cuda(), w, crit, var, algo="auto:1", want_index=True,
+                            want_agg=True)
+    torch.cuda.synchronize()
+    for b in range(3):
+        e_out, e_idx, e_agg = gpu_full(xb[b], w, crit, var, "auto:1+notma")
+        assert np.array_equal(ob[b].cpu().numpy(), e_out)
+        assert np.array_equal(ib[b].cpu().numpy(), e_idx)
+        assert np.array_equal(ab[b].cpu().numpy(), e_agg)
+
+
+def test_tma_path_row_stripes():
+    """Row stripes through the TMA-staged kernel (forced in a child process)
+    equal the full image on the plain-load kernel, bit for bit."""
+    import subprocess
+    import sys
+    child = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tma_stripes_child.py")
+    r = subprocess.run([sys.executable, child], env=dict(os.environ, VF_FORCE_TMA="1"), capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "tma stripes ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 @pytest.mark.parametrize("crit,var", CV)

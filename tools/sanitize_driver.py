@@ -13,19 +13,21 @@ import vfsynth  # noqa: E402
 combos = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp", "minimax"), ("exp", "poly4"),
           ("log", "exact"), ("log", "minimax"), ("amnfe", "minimax"), ("amnfg", "exact"), ("amnfe", "poly4"),
           ("evmf", "exact"), ("evmf", "minimax")]
-for H, W in [(37, 45), (64, 64), (5, 70)]:
+for H, W in [(37, 45), (64, 64), (5, 70), (77, 144), (300, 96)]:   # 3W % 16 == 0: TMA path
     x = torch.from_numpy(vfsynth.random_image(1, H, W)).cuda()
     for w in (3, 5):
         if w > min(H, W):
             continue
         for c in combos:
-            algos = ["window", "shared:1", "shared:2", "shared:3"] if c[0] == "angular" else ["auto:1", "auto:2"]
+            algos = (["window", "shared:1", "shared:2", "shared:3"] if c[0] == "angular" else
+                     ["auto:1", "auto:2", "auto:3", "auto:1+notma", "auto:2+notma", "auto:3+notma"])
             for a in algos:
                 vfb.filter(x, w, *c, algo=a, want_index=True, want_agg=True)
         # stripes
         for lo, hi in [(0, H // 2), (H // 2, H)]:
             blo, bhi = max(0, lo - w // 2), min(H, hi + w // 2)
-            vfb.vf_filter_rows(x[blo:bhi].contiguous(), blo, H, lo, hi - lo, w, "angular", "minimax")
+            for c in (("angular", "minimax"), ("exp", "minimax"), ("log", "exact")):
+                vfb.vf_filter_rows(x[blo:bhi].contiguous(), blo, H, lo, hi - lo, w, *c)
 xb = torch.from_numpy(vfsynth.make_batch(vfsynth.ImageSpec("t", 40, 56, 3, (3,), 4, False, "uncorrelated", 0.2))).cuda()
 outs = [torch.empty_like(xb) for _ in combos]
 plan = vfb.Plan(xb, outs, 3, combos)
