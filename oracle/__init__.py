@@ -20,16 +20,17 @@ SRC = os.path.join(HERE, "vf_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
 
 ANGULAR, EXP, LOG = 0, 1, 2
-EXACT, MINIMAX, MINIMAX_POLY4 = 0, 1, 2
+EXACT, MINIMAX, MINIMAX_POLY4, MINIMAX_REACH = 0, 1, 2, 3
 AMNFE, AMNFG, EVMF = 3, 4, 5
 CRITERIA = {"angular": ANGULAR, "exp": EXP, "log": LOG}
 FILTERS = {"amnfe": AMNFE, "amnfg": AMNFG, "evmf": EVMF}
-VARIANTS = {"exact": EXACT, "minimax": MINIMAX, "poly4": MINIMAX_POLY4}
+VARIANTS = {"exact": EXACT, "minimax": MINIMAX, "poly4": MINIMAX_POLY4, "reach": MINIMAX_REACH}
 
 FN = dict(arccos_exact=0, arccos_mm=1, p_arccos=2, p_arcsin=3, exp_exact=4,
-          exp_rational=5, exp_poly2=6, exp_poly3=7, exp_poly4=8, ent_exact=9, ent_mm=10)
+          exp_rational=5, exp_poly2=6, exp_poly3=7, exp_poly4=8, ent_exact=9, ent_mm=10,
+          exp_reach=11, log_reach=12)
 TABLES = dict(arcsin=0, arccos=1, exp_p2=2, exp_p3=3, exp_p4=4, exp_num=5, exp_den=6,
-              ent_num=7, ent_den=8, constants=9)
+              ent_num=7, ent_den=8, constants=9, exp_reach=10, log_reach=11)
 
 _lib = None
 

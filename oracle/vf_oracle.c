@@ -33,7 +33,7 @@
 #define ORACLE_API __attribute__((visibility("default")))
 
 enum { CRIT_ANGULAR = 0, CRIT_EXP = 1, CRIT_LOG = 2 };
-enum { VAR_EXACT = 0, VAR_MINIMAX = 1, VAR_MINIMAX_POLY4 = 2 };
+enum { VAR_EXACT = 0, VAR_MINIMAX = 1, VAR_MINIMAX_POLY4 = 2, VAR_MINIMAX_REACH = 3 };
 
 /* ---- Table 1: fourth degree minimax polynomials ------------ */
 /* ARCSIN row: fitted to g(tau) = 2 arcsin(tau/sqrt 2) on
@@ -59,6 +59,21 @@ static const double T4_NUM[5] = {-1.519742e-04, -6.835769e-02, -8.856923e-01,
                                  -5.369609e-01, 1.491165};
 static const double T4_DEN[5] = {1.532270e-02, 3.987796e-01, 1.461793,
                                  6.827004e-01, -4.469776e-02};
+
+/* ---- Re-derived minimax polynomials on the reachable arguments --------- *
+ * (VAR_MINIMAX_REACH.)  Computed by the Remez exchange of
+ * P:70 (oracle/minimax.py, tools/remez_reach.py -> tests/golden/
+ * remez_reach.txt, which these decimal strings repeat) for the criterion
+ * values themselves on the intervals the triangle-inequality bounds allow
+ * (DESIGN.md section 2):
+ *   D_E(z) = 1 - exp(-z) on [0, z*_25 = 0.7421166...], degree 5, eps 7.86e-8
+ *   D_L(u) = -(1 - u) ln(1 - u) on [0, 1 - 1/e], degree 7, eps 2.95e-7
+ * (u = 1 - s, s the ENT argument of reading R3).                            */
+static const double R_EXP[6] = {7.8607071043670362e-08, 0.99999223556347028, -0.49987553301909632,
+                                0.16593299907325132, -0.039686762479510071, 0.0057878343103810199};
+static const double R_LOG[8] = {2.951515920989309e-07, 0.99994488204903353, -0.49831625626187054,
+                                -0.18607535607515613, 0.02447556559350492, -0.36382847261870294,
+                                0.43713641586762925, -0.32653163848077049};
 
 static const double T_EXP = 10.0;  /* EXP cutoff                     */
 static const double T_ENT = 0.05;  /* ENT cutoff                     */
@@ -210,14 +225,15 @@ static void window_matrix(const uint8_t *smp, int n, int crit, int var, double *
         for (int i = 0; i < n; ++i)
             for (int j = i + 1; j < n; ++j) {
                 double z = (double)d1[i][j] / h_W;
-                double e;
+                double d;
                 if (var == VAR_EXACT)
-                    e = exp(-z);
+                    d = 1.0 - exp(-z);
                 else if (var == VAR_MINIMAX)
-                    e = exp_mm_rational(z);
+                    d = 1.0 - exp_mm_rational(z);
+                else if (var == VAR_MINIMAX_POLY4)
+                    d = 1.0 - exp_mm_poly(z, 4);
                 else
-                    e = exp_mm_poly(z, 4);
-                double d = 1.0 - e;
+                    d = horner(R_EXP, 5, z);                   /* f4: D_E itself */
                 Dm[i * n + j] = d;
                 Dm[j * n + i] = d;
             }
@@ -236,7 +252,9 @@ static void window_matrix(const uint8_t *smp, int n, int crit, int var, double *
         for (int j = i + 1; j < n; ++j) {
             double q = (double)(n - 1) * (double)d1[i][j] / (double)S1;
             double s = 1.0 - a * q;
-            double d = var == VAR_EXACT ? -ent_exact(s) : -ent_mm(s);
+            double d = var == VAR_EXACT ? -ent_exact(s)
+                     : var == VAR_MINIMAX ? -ent_mm(s)
+                     : horner(R_LOG, 7, a * q);                /* f4: D_L(u), u = 1 - s */
             Dm[i * n + j] = d;
             Dm[j * n + i] = d;
         }
@@ -290,8 +308,9 @@ static int check_args(int H, int W, int window, int crit, int var)
     if (window < 3 || window % 2 == 0 || window * window > NMAX) return -1;
     if (window > H || window > W) return -1;               /* S:64 */
     if (crit < 0 || crit > 2) return -1;
-    if (var < 0 || var > 2) return -1;
+    if (var < 0 || var > 3) return -1;
     if (var == VAR_MINIMAX_POLY4 && crit != CRIT_EXP) return -1;
+    if (var == VAR_MINIMAX_REACH && crit == CRIT_ANGULAR) return -1;
     return 0;
 }
 
@@ -367,9 +386,9 @@ ORACLE_API int oracle_filter_pixels(const uint8_t *img, int H, int W, int window
  * criterion matrix Dm (n*n).  Returns k* (lowest-index argmin) or -1.       */
 ORACLE_API int oracle_window(const uint8_t *samples, int n, int crit, int var, double *R, double *Dm)
 {
-    if (n < 2 || n > NMAX || crit < 0 || crit > 2 || var < 0 || var > 2)
+    if (n < 2 || n > NMAX || crit < 0 || crit > 2 || var < 0 || var > 3)
         return -1;
-    if (var == VAR_MINIMAX_POLY4 && crit != CRIT_EXP)
+    if ((var == VAR_MINIMAX_POLY4 && crit != CRIT_EXP) || (var == VAR_MINIMAX_REACH && crit == CRIT_ANGULAR))
         return -1;
     return window_eval(samples, n, crit, var, R, Dm);
 }
@@ -404,6 +423,8 @@ enum {
     FN_EXP_POLY4 = 8,
     FN_ENT_EXACT = 9,     /* z ln z                                       */
     FN_ENT_MM = 10,       /* Table 4 with cutoff                          */
+    FN_EXP_REACH = 11,    /* f4: D_E(z) polynomial (no cutoff)            */
+    FN_LOG_REACH = 12,    /* f4: D_L(u) polynomial                        */
 };
 
 ORACLE_API int oracle_eval(int fn, const double *z, int64_t n, double *out)
@@ -422,6 +443,8 @@ ORACLE_API int oracle_eval(int fn, const double *z, int64_t n, double *out)
         case FN_EXP_POLY4: r = exp_mm_poly(v, 4); break;
         case FN_ENT_EXACT: r = ent_exact(v); break;
         case FN_ENT_MM: r = ent_mm(v); break;
+        case FN_EXP_REACH: r = horner(R_EXP, 5, v); break;
+        case FN_LOG_REACH: r = horner(R_LOG, 7, v); break;
         default: return -1;
         }
         out[i] = r;
@@ -444,6 +467,8 @@ ORACLE_API int oracle_coeffs(int table, double *out)
     case 7: t = T4_NUM; m = 5; break;
     case 8: t = T4_DEN; m = 5; break;
     case 9: out[0] = T_EXP; out[1] = T_ENT; out[2] = KAPPA; return 3;
+    case 10: t = R_EXP; m = 6; break;
+    case 11: t = R_LOG; m = 8; break;
     default: return -1;
     }
     memcpy(out, t, sizeof(double) * (size_t)m);

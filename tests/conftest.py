@@ -35,3 +35,22 @@ def load_paper_tables():
 @pytest.fixture(scope="session")
 def paper_tables():
     return load_paper_tables()
+
+
+def load_remez_reach():
+    """Parse tests/golden/remez_reach.txt (written by tools/remez_reach.py) ->
+    {name: [decimal strings]}."""
+    out = {}
+    with open(golden_path("remez_reach.txt")) as fh:
+        for line in fh:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            name, *vals = line.split()
+            out[name] = vals
+    return out
+
+
+@pytest.fixture(scope="session")
+def remez_reach():
+    return load_remez_reach()

@@ -24,8 +24,12 @@ KAPPA = mp.mpf("0.33")
 
 
 @pytest.fixture(scope="module")
-def T(paper_tables):
-    return {k: [mp.mpf(repr(v)) for v in d["values"]] for k, d in paper_tables.items()}
+def T(paper_tables, remez_reach):
+    t = {k: [mp.mpf(repr(v)) for v in d["values"]] for k, d in paper_tables.items()}
+    # SURVEY 8(f4) polynomials on the reachable arguments, from their golden file
+    t["EXP_REACH"] = [mp.mpf(v) for v in remez_reach["exp_reach"]]
+    t["LOG_REACH"] = [mp.mpf(v) for v in remez_reach["log_reach"]]
+    return t
 
 
 def hornerm(a, z):
@@ -67,26 +71,29 @@ def mp_window(samples, crit, var, T):
             elif crit == "exp":
                 z = mp.mpf(n) ** (1 + KAPPA / 3) * d1[i][j] / (2 * S1)
                 if var == "exact":
-                    e = mp.exp(-z)
+                    d = 1 - mp.exp(-z)
                 elif var == "minimax":
-                    e = hornerm(T["EXP_NUM"], z) / hornerm(T["EXP_DEN"], z)
-                else:
-                    e = hornerm(T["EXP_P4"], z)
-                d = 1 - e
+                    d = 1 - hornerm(T["EXP_NUM"], z) / hornerm(T["EXP_DEN"], z)
+                elif var == "poly4":
+                    d = 1 - hornerm(T["EXP_P4"], z)
+                else:                                            # f4: the polynomial is D_E itself
+                    d = hornerm(T["EXP_REACH"], z)
             else:
                 q = mp.mpf(n - 1) * d1[i][j] / S1
                 sv = 1 - (1 - mp.exp(-1)) * q
                 if var == "exact":
                     d = -sv * mp.log(sv)
-                else:
+                elif var == "minimax":
                     d = -hornerm(T["ENT_NUM"], sv) / hornerm(T["ENT_DEN"], sv)
+                else:                                            # f4: D_L in u = 1 - s
+                    d = hornerm(T["LOG_REACH"], 1 - sv)
             Dm[i][j] = Dm[j][i] = d
     R = [mp.fsum(Dm[i][j] for j in range(n) if j != i) for i in range(n)]
     return R
 
 
 CV = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp", "minimax"),
-      ("exp", "poly4"), ("log", "exact"), ("log", "minimax")]
+      ("exp", "poly4"), ("log", "exact"), ("log", "minimax"), ("exp", "reach"), ("log", "reach")]
 
 
 # ------------------------------------------------------- angular closed forms
@@ -172,6 +179,8 @@ def test_single_impulse_closed_forms(n, pos, a, b, T):
         ("exp", "poly4"): (1 - P4(zs), 1 - P4(mp.mpf(0))),
         ("log", "exact"): (einv, mp.mpf(0)),              # -s ln s at s = 1/e, and at s = 1
         ("log", "minimax"): (-ENTm(einv), -ENTm(mp.mpf(1))),
+        ("exp", "reach"): (hornerm(T["EXP_REACH"], zs), hornerm(T["EXP_REACH"], mp.mpf(0))),
+        ("log", "reach"): (hornerm(T["LOG_REACH"], 1 - einv), hornerm(T["LOG_REACH"], mp.mpf(0))),
     }
     inl = [i for i in range(n) if i != pos]
     for (crit, var), (d_imp, d_same) in cases.items():
@@ -319,6 +328,8 @@ def test_invalid_arguments():
         oracle.filter_image(x, 3, "angular", "poly4")
     with pytest.raises(ValueError):
         oracle.filter_image(x, 3, "log", "poly4")
+    with pytest.raises(ValueError):
+        oracle.filter_image(x, 3, "angular", "reach")
     with pytest.raises(ValueError):
         oracle.filter_image(x[:2], 3, "exp", "exact")
 
