@@ -31,6 +31,9 @@ sys.path.insert(0, ROOT)
 
 COMBOS = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp", "minimax"),
           ("exp", "poly4"), ("log", "exact"), ("log", "minimax")]
+# the re-derived reachable-interval polynomials (VF_MINIMAX_REACH),
+# timed per kernel beside the paper's variants (not part of the 7-filter step)
+REACH_COMBOS = [("exp", "reach"), ("log", "reach")]
 
 # Algorithmic FP32 flops per pair (SURVEY.md 8(d) D4 counting rules: FMA = 2,
 # add/sub/mul = 1; robustness overhead not counted).  Exact variants: the
@@ -39,6 +42,8 @@ COMBOS = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp"
 FLOPS_PER_PAIR = {
     ("angular", "minimax"): 18, ("exp", "minimax"): 26, ("exp", "poly4"): 18, ("log", "minimax"): 26,
     ("angular", "exact"): 10 + 23, ("exp", "exact"): 10 + 24, ("log", "exact"): 11 + 28,
+    # f4 reach: L1 5 + S1 1 + scale 1 + Horner-5 / Horner-7 (10 / 14) + accumulate 2
+    ("exp", "reach"): 19, ("log", "reach"): 23,
 }
 NOMINAL_FP32_TFLOPS_AT_MAX = 2 * 128 * 148 * 1.965e9 / 1e12   # 74.4
 METRIC = ("filtered Mpixels/s (7 criterion x variant filters per pixel; per-kernel Mpix/s and % of FP32 roofline "
@@ -418,7 +423,7 @@ def paper_filters_section(vfb, torch, dev, stream, flush, x, x_np, spec, rank, w
 
 
 KERNEL_NAMES = {"angular": "vf_angular_shared_kernel<{w},{v}>", "exp": "vf_el_kernel<{w},exp,{v}>",
-                "log": "vf_el_kernel<{w},log,{v}>"}
+                "log": "vf_el_kernel<{w},log,{v}>"}   # (3x3 polynomial variants of large launches: vf_el_tma_kernel)
 
 
 def main():
@@ -497,14 +502,16 @@ def main():
     # ---- per-kernel breakdown: each filter launched alone (same L2 flush),
     # CUDA events on the launching stream; gives the roofline of each kernel
     kreps = max(3, min(args.steps, 20))
-    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in COMBOS]
+    KCOMBOS = COMBOS + REACH_COMBOS
+    kouts = outs + [torch.empty_like(x) for _ in REACH_COMBOS]
+    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in KCOMBOS]
            for _ in range(kreps)]
     t_k0 = time.perf_counter()
     for r in range(kreps):
-        for i, (crit, var) in enumerate(COMBOS):
+        for i, (crit, var) in enumerate(KCOMBOS):
             flush.fill_((r + i) & 0xFF)
             kev[r][i][0].record(stream)
-            vfb.vf_filter_batch(x, w, crit, var, out=outs[i], stream=stream)
+            vfb.vf_filter_batch(x, w, crit, var, out=kouts[i], stream=stream)
             kev[r][i][1].record(stream)
     torch.cuda.synchronize(dev)
     t_k1 = time.perf_counter()
@@ -513,7 +520,7 @@ def main():
     n = w * w
     pairs = n * (n - 1) // 2
     kern = {}
-    for i, c in enumerate(COMBOS):
+    for i, c in enumerate(KCOMBOS):
         ms = statistics.mean(kev[r][i][0].elapsed_time(kev[r][i][1]) for r in range(kreps))
         mpix = npix / (ms / 1e3) / 1e6
         tfl = FLOPS_PER_PAIR[c] * pairs * npix / (ms / 1e3) / 1e12
@@ -522,6 +529,7 @@ def main():
         if clocks.get("sm_mhz"):
             kern[f"{c[0]}/{c[1]}"]["frac_fp32_at_measured_clock"] = \
                 tfl / (NOMINAL_FP32_TFLOPS_AT_MAX * clocks["sm_mhz"] / 1965.0)
+    reach = {k: kern.pop(k) for k in [f"{c[0]}/{c[1]}" for c in REACH_COMBOS]}
     dom = max(kern, key=lambda k: kern[k]["ms"])
     d = kern[dom]
     roofline = {"bound": "alu", "kernel": d["kernel"], "achieved": d["alg_tflops"],
@@ -578,9 +586,10 @@ def main():
         hplan.close()
 
     # ---- fidelity: minimax vs exact (the paper's quality measure)
-    oi = {c: outs[i] for i, c in enumerate(COMBOS)}
+    oi = {c: kouts[i] for i, c in enumerate(KCOMBOS)}
     fid = {}
-    for crit, mmv in (("angular", "minimax"), ("exp", "minimax"), ("exp", "poly4"), ("log", "minimax")):
+    for crit, mmv in (("angular", "minimax"), ("exp", "minimax"), ("exp", "poly4"), ("log", "minimax"),
+                      ("exp", "reach"), ("log", "reach")):
         f = vfb.fidelity(oi[(crit, "exact")], oi[(crit, mmv)])
         fid[f"{crit}/{mmv}"] = {"psnr_db": f["psnr_db"], "ncd": f["ncd"], "diff_frac": f["diff_frac"]}
 
@@ -615,6 +624,12 @@ def main():
             "step_roofline": step_roofline,
             "best_minimax_kernel": {"name": best_mm, **kern[best_mm]},
             "per_kernel": kern,
+            "f4_reach": {"per_kernel": reach,
+                         "what": "SURVEY 8(f4): D_E / D_L as Remez minimax polynomials on the reachable arguments "
+                                 "(deg 5 eps 7.86e-8 / deg 7 eps 2.95e-7, no division), VF_MINIMAX_REACH; "
+                                 "not part of the 7-filter step",
+                         "speedup_vs_paper_minimax": {
+                             k: kern[k.replace("reach", "minimax")]["ms"] / v["ms"] for k, v in reach.items()}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "fidelity_minimax_vs_exact": fid,

@@ -25,6 +25,12 @@
  *     VF_LOG      D = -ENT(s), ENT(s) = s ln s, s = 1 - (1 - 1/e) q,
  *                 q = (n-1) |x_i-x_j|_1 / sum_{k<l} |x_k-x_l|_1;
  *                 minimax = Table 4 rational.
+ *     VF_MINIMAX_REACH (VF_EXP, VF_LOG only): the criterion
+ *                 value itself as one minimax polynomial re-derived by the
+ *                 Remez exchange on the arguments the criterion can
+ *                 reach (z <= z*_25, u = 1 - s <= 1 - 1/e):
+ *                 degree 5 for D_E (eps 7.86e-8), 7 for D_L (eps 2.95e-7),
+ *                 coefficients tests/golden/remez_reach.txt.
  *   Arithmetic: fp32 on the device, with exact integer geometry (dot
  *   products, squared norms, L1 distances and the cos < 0.5 branch decision
  *   are exact); aggregates agree with the double-precision oracle within
@@ -47,7 +53,8 @@
  *   Every entry point returns a vf_status.  VF_EINVAL: invalid argument
  *   (window even or < 3, H or W < 1, window > min(H, W), B < 1, NULL
  *   img/out, input and output ranges overlap, criterion/variant out of range,
- *   VF_MINIMAX_POLY4 with a criterion other than VF_EXP/VF_AMNFE/VF_AMNFG, a row band that does
+ *   VF_MINIMAX_POLY4 with a criterion other than VF_EXP/VF_AMNFE/VF_AMNFG,
+ *   VF_MINIMAX_REACH with one other than VF_EXP/VF_LOG, a row band that does
  *   not cover the rows the output stripe reads).  VF_EUNSUPPORTED: an odd
  *   window >= 7 (valid, not compiled).  VF_ECUDA: a CUDA launch/copy error
  *   (details from vf_last_error()).  No exception crosses the ABI.  On error
@@ -84,7 +91,7 @@ extern "C" {
  *                        the median's sums R_i = sum_j |x_i - x_j|_2; `index`:
  *                        selected sample, bit 7 set iff the switch fired. */
 typedef enum { VF_ANGULAR = 0, VF_EXP = 1, VF_LOG = 2, VF_AMNFE = 3, VF_AMNFG = 4, VF_EVMF = 5 } vf_criterion;
-typedef enum { VF_EXACT = 0, VF_MINIMAX = 1, VF_MINIMAX_POLY4 = 2 } vf_variant;
+typedef enum { VF_EXACT = 0, VF_MINIMAX = 1, VF_MINIMAX_POLY4 = 2, VF_MINIMAX_REACH = 3 } vf_variant;
 typedef enum { VF_OK = 0, VF_EINVAL = -1, VF_EUNSUPPORTED = -2, VF_ECUDA = -3 } vf_status;
 
 /* Kernel selection for the angular criterion (both variants are window

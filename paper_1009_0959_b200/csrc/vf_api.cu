@@ -103,8 +103,10 @@ const void* el_kernel(int crit, int var) {
   if (crit == EXPC) {
     if (var == EXACT) return (const void*)vf_el_kernel<WIN, EXPC, EXACT, OPT>;
     if (var == MINIMAX) return (const void*)vf_el_kernel<WIN, EXPC, MINIMAX, OPT>;
+    if (var == REACH) return (const void*)vf_el_kernel<WIN, EXPC, REACH, OPT>;
     return (const void*)vf_el_kernel<WIN, EXPC, POLY4, OPT>;
   }
+  if (var == REACH) return (const void*)vf_el_kernel<WIN, LOGC, REACH, OPT>;
   return var == EXACT ? (const void*)vf_el_kernel<WIN, LOGC, EXACT, OPT> : (const void*)vf_el_kernel<WIN, LOGC, MINIMAX, OPT>;
 }
 
@@ -114,8 +116,10 @@ const void* el_tma_kernel(int crit, int var) {
   if (crit == EXPC) {
     if (var == EXACT) return (const void*)vf_el_tma_kernel<WIN, EXPC, EXACT, OPT>;
     if (var == MINIMAX) return (const void*)vf_el_tma_kernel<WIN, EXPC, MINIMAX, OPT>;
+    if (var == REACH) return (const void*)vf_el_tma_kernel<WIN, EXPC, REACH, OPT>;
     return (const void*)vf_el_tma_kernel<WIN, EXPC, POLY4, OPT>;
   }
+  if (var == REACH) return (const void*)vf_el_tma_kernel<WIN, LOGC, REACH, OPT>;
   return var == EXACT ? (const void*)vf_el_tma_kernel<WIN, LOGC, EXACT, OPT>
                       : (const void*)vf_el_tma_kernel<WIN, LOGC, MINIMAX, OPT>;
 }
@@ -144,9 +148,11 @@ int validate(int B, int H, int W, int window, int crit, int var) {
   if (H < 1 || W < 1) return fail(VF_EINVAL, "image size must be positive");
   if (window > H || window > W) return fail(VF_EINVAL, "window larger than the image (S:64)");
   if (crit < 0 || crit > 5) return fail(VF_EINVAL, "criterion out of range (%lld)", crit);
-  if (var < 0 || var > 2) return fail(VF_EINVAL, "variant out of range (%lld)", var);
+  if (var < 0 || var > 3) return fail(VF_EINVAL, "variant out of range (%lld)", var);
   if (var == VF_MINIMAX_POLY4 && crit != VF_EXP && crit != VF_AMNFE && crit != VF_AMNFG)
     return fail(VF_EINVAL, "VF_MINIMAX_POLY4 is only defined for the EXP-based filters");
+  if (var == VF_MINIMAX_REACH && crit != VF_EXP && crit != VF_LOG)
+    return fail(VF_EINVAL, "VF_MINIMAX_REACH is only defined for the exp and log criteria");
   if (window > 5) return fail(VF_EUNSUPPORTED, "window %lld is valid but not compiled (3 and 5 are)", window);
   return VF_OK;
 }

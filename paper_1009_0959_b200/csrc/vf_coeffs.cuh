@@ -67,6 +67,30 @@ __host__ __device__ constexpr P4f EXP_P4() { return P4f{(float)T2_P4[0], (float)
 __host__ __device__ constexpr P4f ENT_N() { return P4f{(float)T4_N[0], (float)T4_N[1], (float)T4_N[2], (float)T4_N[3], (float)T4_N[4]}; }
 __host__ __device__ constexpr P4f ENT_Q() { return P4f{(float)T4_Q[0], (float)T4_Q[1], (float)T4_Q[2], (float)T4_Q[3], (float)T4_Q[4]}; }
 
+// ---- minimax polynomials re-derived (Remez exchange)
+// for the criterion values on the arguments they can reach:
+//   D_E(z) = 1 - exp(-z) on [0, z*_25 = 0.7421166], degree 5, eps 7.86e-8
+//   D_L(u) = -(1 - u) ln(1 - u) on [0, 1 - 1/e], degree 7, eps 2.95e-7
+// (the decimal strings of tests/golden/remez_reach.txt; no division, and
+// every coefficient beyond a0 is O(1), so fp32 Horner keeps its precision)
+struct R_EXP {
+  static constexpr int DEG = 5;
+  __host__ __device__ static constexpr double c(int k) {
+    constexpr double t[6] = {7.8607071043670362e-08, 0.99999223556347028, -0.49987553301909632,
+                             0.16593299907325132, -0.039686762479510071, 0.0057878343103810199};
+    return t[k];
+  }
+};
+struct R_LOG {
+  static constexpr int DEG = 7;
+  __host__ __device__ static constexpr double c(int k) {
+    constexpr double t[8] = {2.951515920989309e-07, 0.99994488204903353, -0.49831625626187054,
+                             -0.18607535607515613, 0.02447556559350492, -0.36382847261870294,
+                             0.43713641586762925, -0.32653163848077049};
+    return t[k];
+  }
+};
+
 constexpr double KAPPA = 0.33;
 constexpr double ONE_MINUS_INV_E = 0.63212055882855767840;  // 1 - e^-1 (reading R3)
 

@@ -39,7 +39,7 @@
 namespace vf {
 
 enum { ANGULAR = 0, EXPC = 1, LOGC = 2 };
-enum { EXACT = 0, MINIMAX = 1, POLY4 = 2 };
+enum { EXACT = 0, MINIMAX = 1, POLY4 = 2, REACH = 3 };
 
 // ---- single-instruction PTX helpers ------------------------------------------
 // MUFU.RCP / MUFU.RSQ without the denormal fix-up sequences that rcpf/rsqrtf
@@ -104,6 +104,16 @@ __device__ __forceinline__ void static_for(F&& f) {
 __device__ __forceinline__ float horner4(const coef::P4f p, float x) {
   return fmaf(fmaf(fmaf(fmaf(p.a4, x, p.a3), x, p.a2), x, p.a1), x, p.a0);
 }
+// Horner over a coefficient table T (T::DEG, constexpr T::c(k) in double),
+// each coefficient rounded to fp32 at compile time.
+template <typename T, int K>
+__device__ __forceinline__ float horner_rec(float x) {
+  constexpr float a = (float)T::c(K);
+  if constexpr (K == T::DEG) return a;
+  else return fmaf(horner_rec<T, K + 1>(x), x, a);
+}
+template <typename T>
+__device__ __forceinline__ float horner_tab(float x) { return horner_rec<T, 0>(x); }
 
 // ---- angular criterion A(x_i, x_j) of Eq. 5 --------------------------
 // Geometry shared by both variants: D, P = Ph + Pl, X, the exact branch
@@ -168,6 +178,10 @@ __device__ __forceinline__ void crit_accumulate(float zu, float& Ri, float& Rj) 
     const float r = rcp_approx(CRIT == EXPC ? horner4(coef::EXP_Q(), zu) : horner4(coef::ENT_Q_U(), zu));
     Ri = fmaf(num, r, Ri);
     Rj = fmaf(num, r, Rj);
+  } else if (VAR == REACH) {   // the criterion value as one polynomial, no division
+    const float v = CRIT == EXPC ? horner_tab<coef::R_EXP>(zu) : horner_tab<coef::R_LOG>(zu);
+    Ri = __fadd_rn(Ri, v);
+    Rj = __fadd_rn(Rj, v);
   } else if (VAR == POLY4) {   // exp only: 1 - P4(z)
     const float v = horner4(coef::EXP_1MP4(), zu);
     Ri = __fadd_rn(Ri, v);

@@ -21,7 +21,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_1009_0959_b200 as vfb  # noqa: E402
 
 CV = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp", "minimax"),
-      ("exp", "poly4"), ("log", "exact"), ("log", "minimax")]
+      ("exp", "poly4"), ("log", "exact"), ("log", "minimax"), ("exp", "reach"), ("log", "reach")]
 
 
 def gpu_full(img_np, w, crit, var, algo="auto"):
@@ -248,7 +248,8 @@ def test_host_api_matches_device_api():
 def test_invalid_arguments_return_status():
     x = torch.zeros((16, 16, 3), dtype=torch.uint8, device="cuda")
     for w, c, v, st in [(4, "angular", "exact", -1), (7, "angular", "exact", -2), (3, "angular", "poly4", -1),
-                        (3, 6, 0, -1), (3, 0, 9, -1), (3, "evmf", "poly4", -1), (17, "exp", "exact", -1)]:
+                        (3, 6, 0, -1), (3, 0, 9, -1), (3, "evmf", "poly4", -1), (17, "exp", "exact", -1),
+                        (3, "angular", "reach", -1), (3, "amnfe", "reach", -1)]:
         with pytest.raises(vfb.VFError) as e:
             vfb.filter(x, w, c, v)
         assert e.value.status == st, (w, c, v)

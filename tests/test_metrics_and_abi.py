@@ -87,7 +87,8 @@ def test_invalid_arguments_rejected_before_any_device_work(lib):
     assert f(p, 16, 16, 7, 0, 0, q, None, None, None) == -2          # valid, not compiled
     assert f(p, 2, 16, 3, 0, 0, q, None, None, None) == -1           # window > H
     assert f(p, 16, 16, 3, 6, 0, q, None, None, None) == -1          # criterion
-    assert f(p, 16, 16, 3, 0, 3, q, None, None, None) == -1          # variant
+    assert f(p, 16, 16, 3, 1, 4, q, None, None, None) == -1          # variant
+    assert f(p, 16, 16, 3, 0, 3, q, None, None, None) == -1          # REACH only for exp / log
     assert f(p, 16, 16, 3, 0, 2, q, None, None, None) == -1          # POLY4 only for the EXP filters
     assert f(p, 16, 16, 3, 5, 2, q, None, None, None) == -1          # (EVMF uses ENT, not EXP)
     assert f(None, 16, 16, 3, 0, 0, q, None, None, None) == -1       # NULL input
@@ -102,7 +103,7 @@ def test_invalid_arguments_rejected_before_any_device_work(lib):
     crit = (ctypes.c_int * 2)(0, 1)
     var = (ctypes.c_int * 2)(1, 2)
     outs = (ctypes.c_void_p * 2)(1 << 40, 1 << 41)
-    assert lib.vf_plan_create(ctypes.byref(h), 1, 16, 16, 3, 2, crit, (ctypes.c_int * 2)(1, 3), p, outs, None,
+    assert lib.vf_plan_create(ctypes.byref(h), 1, 16, 16, 3, 2, crit, (ctypes.c_int * 2)(1, 4), p, outs, None,
                               None) == -1
     assert lib.vf_plan_create(ctypes.byref(h), 1, 16, 16, 3, 0, crit, var, p, outs, None, None) == -1
     assert lib.vf_plan_create(ctypes.byref(h), 1, 16, 16, 4, 2, crit, var, p, outs, None, None) == -1

@@ -17,7 +17,8 @@ import vfsynth  # noqa: E402
 assert os.environ.get("VF_FORCE_TMA") == "1"
 x = vfsynth.random_image(51, 77, 144)
 H, W = x.shape[:2]
-for crit, var in [("exp", "exact"), ("exp", "minimax"), ("exp", "poly4"), ("log", "exact"), ("log", "minimax")]:
+for crit, var in [("exp", "exact"), ("exp", "minimax"), ("exp", "poly4"), ("log", "exact"), ("log", "minimax"),
+                  ("exp", "reach"), ("log", "reach")]:
     for w in (3, 5):
         xt = torch.from_numpy(x).cuda()
         full, fidx, fagg = vfb.filter(xt, w, crit, var, algo="auto+notma", want_index=True, want_agg=True)

@@ -29,7 +29,7 @@ for cfg in cfgs:
     n = w * w
     pairs = n * (n - 1) // 2
     line = [f"{cfg}({w}x{w},{npix/1e6:.1f}Mpx)"]
-    for c in bench.COMBOS:
+    for c in bench.COMBOS + bench.REACH_COMBOS:
         if only and only not in f"{c[0]}/{c[1]}":
             continue
         for _ in range(3):

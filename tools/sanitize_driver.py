@@ -11,7 +11,7 @@ import paper_1009_0959_b200 as vfb  # noqa: E402
 import vfsynth  # noqa: E402
 
 combos = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp", "minimax"), ("exp", "poly4"),
-          ("log", "exact"), ("log", "minimax"), ("amnfe", "minimax"), ("amnfg", "exact"), ("amnfe", "poly4"),
+          ("log", "exact"), ("log", "minimax"), ("exp", "reach"), ("log", "reach"), ("amnfe", "minimax"), ("amnfg", "exact"), ("amnfe", "poly4"),
           ("evmf", "exact"), ("evmf", "minimax")]
 for H, W in [(37, 45), (64, 64), (5, 70), (77, 144), (300, 96)]:   # 3W % 16 == 0: TMA path
     x = torch.from_numpy(vfsynth.random_image(1, H, W)).cuda()
