@@ -101,7 +101,13 @@ typedef enum { VF_OK = 0, VF_EINVAL = -1, VF_EUNSUPPORTED = -2, VF_ECUDA = -3 } 
  * exp/log criteria on the plain-load kernel instead of the persistent
  * TMA-staged one (which needs 16-byte aligned rows: 3W % 16 == 0, a 16-byte
  * aligned base and batch stride); the two give bit-identical results. */
-typedef enum { VF_ALGO_AUTO = 0, VF_ALGO_WINDOW = 1, VF_ALGO_SHARED = 2, VF_ALGO_NO_TMA = 16 } vf_algo;
+typedef enum {
+  VF_ALGO_AUTO = 0,     /* fastest measured choice                                              */
+  VF_ALGO_WINDOW = 1,   /* angular: one thread per window, all n(n-1)/2 pairs                    */
+  VF_ALGO_SHARED = 2,   /* angular: pairs shared across windows, per-window accumulation         */
+  VF_ALGO_ROLE = 3,     /* angular 5x5: pairs shared, per-pixel role sums (the 5x5 default)      */
+  VF_ALGO_NO_TMA = 16
+} vf_algo;
 
 /* One image.  img, out: device [H][W][3]; index: device [H][W] or NULL;
  * aggregates: device [H][W][n] or NULL. */

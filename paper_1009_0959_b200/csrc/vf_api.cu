@@ -17,6 +17,7 @@
 
 #include "../../include/vf.h"
 #include "vf_paper.cuh"
+#include "vf_role.cuh"
 #include "vf_shared.cuh"
 #include "vf_stats.cuh"
 #include "vf_tma.cuh"
@@ -93,7 +94,10 @@ int persistent_blocks(const void* fn, int threads, size_t smem) {
 
 // One-time per-process kernel attribute setup (thread-safe).
 cudaError_t ensure_attributes() {
-  static cudaError_t status = vf::shared_set_attributes();
+  static cudaError_t status = [] {
+    cudaError_t e = vf::shared_set_attributes();
+    return e != cudaSuccess ? e : vf::role_set_attributes();
+  }();
   return status;
 }
 
@@ -185,6 +189,17 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
     static const int ppt_env = [] { const char* e = std::getenv("VF_SHARED_PPT"); return e ? std::atoi(e) : 0; }();
     if (ppt_env >= 1 && ppt_env <= 3) ppt = ppt_env;
     if (tile) ppt = tile;
+    // 5x5: per-pixel role sums (vf_role.cuh) unless the per-window
+    // accumulation is asked for explicitly
+    if (window == 5 && algo != VF_ALGO_SHARED) {
+      kd->fn = vf::role_kernel_fn(var, ppt);
+      kd->grid = vf::shared_grid(L, B, window, ppt);
+      kd->block = dim3(vf::shared::NTHR);
+      kd->smem = vf::role_smem_bytes(ppt);
+      const cudaError_t e = ensure_attributes();
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+      return VF_OK;
+    }
     kd->fn = vf::shared_kernel_fn(window, var, ppt);
     kd->grid = vf::shared_grid(L, B, window, ppt);
     kd->block = dim3(vf::shared::NTHR);
@@ -290,7 +305,7 @@ int vf_filter_batch_algo(const uint8_t* imgs, int B, int H, int W, int window, i
   int rc = validate(B, H, W, window, criterion, variant);
   if (rc) return rc;
   if (!imgs || !outs) return fail(VF_EINVAL, "NULL image or output pointer");
-  if (algo < 0 || (algo & 3) > 2 || algo > 31) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
+  if (algo < 0 || algo > 31) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
   const size_t bytes = (size_t)B * H * W * 3;
   if (overlap(imgs, bytes, outs, bytes)) return fail(VF_EINVAL, "input and output overlap");
   const long long stride = (long long)H * W * 3;

@@ -1,0 +1,324 @@
+// vf_role.cuh -- angular criterion, 5x5 windows: cross-window pair sharing
+// with per-pixel ROLE SUMS instead of per-window pair
+// accumulation.
+//
+// In a window with top-left t, sample i sits at q = t + (a, b) and its
+// aggregate is (Eq. 5)
+//     R_i = sum over (dy, dx) in [-a, 4-a] x [-b, 4-b], (dy, dx) != 0, of A(q, q + (dy, dx)),
+// which depends only on the pixel q and its role (a, b) in the window.  So
+// every pixel of the block's region computes its 25 role sums once, from the
+// 80 pair values of its 9x9 neighbourhood, and every output window reads its
+// 25 aggregates with one load each -- 25 loads instead of 300 loads and 600
+// additions per window (the per-window accumulation of vf_shared.cuh).
+//
+// Per pixel and neighbourhood row dy, the five row sums
+//     H_b(dy) = sum_{dx=-b}^{4-b} A(q, q + (dy, dx)),  b = 0..4,
+// are formed without subtractions (14 additions: all terms are >= 0, so the
+// sums keep full relative precision), and R_(a,b) += H_b(dy) for every a with
+// -a <= dy <= 4-a.
+//
+// The pair maps are built one neighbourhood row at a time (group g = the
+// offsets with dy = g: 4 for g = 0, 9 for g = 1..4), exactly as in
+// vf_shared.cuh (phase A: tau-branch value of Table 1 / Eq. 6, superset flag
+// of the cos < 0.5 pairs re-decided exactly by a warp-cooperative pass,
+// block-uniform zero-vector rule S:342); phase B then adds the rows +g and -g
+// of every pixel's neighbourhood (row -g is the map of offset (g, -dx) read at
+// the neighbour) into its role sums.  After the last group the role sums
+// replace the maps in shared memory and the outputs take their argmin.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <utility>
+
+#include "vf_shared.cuh"
+
+namespace vf {
+
+namespace role {
+constexpr int PW = shared::PW;          // region width (32)
+constexpr int NTHR = shared::NTHR;      // 256
+constexpr int PRE = 5 * PW;             // map padding before the region: reverse reads reach 4 rows + 4 px back
+constexpr int POST = 5 * PW;            // and after it
+__host__ __device__ constexpr int nslots(int g) { return g == 0 ? 4 : 9; }
+__host__ __device__ constexpr int slot_dx(int g, int s) { return g == 0 ? s + 1 : s - 4; }
+}  // namespace role
+
+template <int PPT>
+struct RoleSmem {
+  static constexpr int NP = shared::region_np(PPT);
+  static constexpr int MS = role::PRE + NP + role::POST;   // map stride (floats)
+  static constexpr int QCAP = 64;
+  struct Maps {
+    uint4 px[NP + shared::PAD];   // (packed RGB0, |x|^2 bits, |x| bits, 0)
+    float M[9][MS];               // pair maps of one neighbourhood row g
+  };
+  union U {
+    Maps a;
+    float S[25][NP];              // role sums, after the last group
+  } u;
+  uint32_t pk[NP];                // packed RGB of the region (output store)
+  uint32_t queue[role::NTHR / 32][QCAP];
+};
+
+// Exact re-decision of a flagged pair (p, p + (g, dx)) of slot s: as
+// angular_fix in vf_shared.cuh, on this kernel's map layout.
+template <int VAR, int PPT>
+__device__ __forceinline__ void role_fix(RoleSmem<PPT>& sm, int p, int s, int off) {
+  const uint4 pv = sm.u.a.px[p], qv = sm.u.a.px[p + off];
+  const float D = __uint_as_float(__dp4a(pv.x, qv.x, F2P23_BITS)) - F2P23;   // exact dot
+  const float nna = __uint_as_float(pv.y), nnb = __uint_as_float(qv.y);
+  const float Ph = __fmul_rn(nna, nnb);
+  const float Pl = fmaf(nna, nnb, -Ph);
+  const float t = fmaf(__fmul_rn(4.0f, D), D, -Ph);         // fl(4D^2 - Ph)
+  if (t < Pl) {                                             // 4D^2 < P: cos < 0.5, exact
+    const float c = D * rcp_approx(__fmul_rn(__uint_as_float(pv.z), __uint_as_float(qv.z)));
+    sm.u.a.M[s][role::PRE + p] = (VAR == EXACT) ? acosf(c) : horner4(coef::ACOS(), c);
+  }
+}
+
+// H_b = sum_{dx=-b}^{4-b} v[4 + dx], b = 0..4, without subtractions.
+__device__ __forceinline__ void row_sums5(const float (&v)[9], float (&H)[5]) {
+  const float e = v[4] + v[5];
+  const float c = e + v[6];
+  H[0] = c + (v[7] + v[8]);
+  H[1] = c + (v[3] + v[7]);
+  H[2] = c + (v[2] + v[3]);
+  const float a12 = v[1] + v[2];
+  H[3] = a12 + (v[3] + e);
+  H[4] = (v[0] + a12) + (v[3] + v[4]);
+}
+
+template <int VAR, int PPT, int G>
+__device__ __forceinline__ void role_group(RoleSmem<PPT>& sm, const uint32_t (&my_pk)[PPT], const float (&my_nn)[PPT],
+                                           const float (&my_nrm)[PPT], float (&Rs)[PPT][25], int tid, bool blk_zero) {
+  using namespace role;
+  constexpr int NS = nslots(G);
+  constexpr int QCAP = RoleSmem<PPT>::QCAP;
+  const int lane = tid & 31, warp = tid >> 5;
+  if (G > 0) __syncthreads();   // previous phase B done with the maps (G = 0: the staging barrier)
+  // ---- phase A: maps of the offsets (G, dx) ----------------------------------------
+  uint32_t flags[PPT];
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) flags[k] = 0u;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int off = G * PW + slot_dx(G, s);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const int p = tid + NTHR * k;
+      VF_CHECK(p + off >= 0 && p + off < RoleSmem<PPT>::NP + shared::PAD);
+      const uint4 qv = sm.u.a.px[p + off];
+      const float D = __uint_as_float(__dp4a(my_pk[k], qv.x, F2P23_BITS)) - F2P23;   // exact dot
+      const float nnq = __uint_as_float(qv.y);
+      const float Ph = __fmul_rn(my_nn[k], nnq);
+      const float Pl = fmaf(my_nn[k], nnq, -Ph);
+      const float X = __fadd_rn(fmaf(-D, D, Ph), Pl);         // |x_p x x_q|^2
+      const float w = fmaf(__fmul_rn(my_nrm[k], __uint_as_float(qv.z)), D, Ph);   // s (s + D)
+      const float tau = __fmul_rn(X, rsqrt_approx(fmaf(X, w, 1e-30f)));          // sqrt(1 - cos)
+      const float v = (VAR == EXACT) ? 2.0f * asinf(tau * 0.70710678118654752f) : horner4(coef::ASIN(), tau);
+      sm.u.a.M[s][PRE + p] = v;
+      if (tau > 0.70641626f) flags[k] |= 1u << s;            // possible cos < 0.5 (see vf_shared.cuh)
+    }
+  }
+  // ---- flagged pairs, warp-cooperative (as in vf_shared.cuh) --------------------------
+  {
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) cnt += __popc(flags[k]);
+    if (__any_sync(0xffffffffu, cnt != 0)) {
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      int pos = incl - cnt;
+      uint32_t* q = sm.queue[warp];
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const uint32_t p = tid + NTHR * k;
+        while (flags[k] && pos < QCAP) {
+          const uint32_t s = __ffs(flags[k]) - 1;
+          flags[k] &= flags[k] - 1;
+          q[pos++] = p | (s << 16);
+        }
+      }
+      __syncwarp();
+      const int nq = total < QCAP ? total : QCAP;
+      for (int e = lane; e < nq; e += 32) {
+        const uint32_t en = q[e];
+        const int s = (int)(en >> 16);
+        role_fix<VAR>(sm, (int)(en & 0xffffu), s, G * PW + slot_dx(G, s));
+      }
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        while (flags[k]) {
+          const int s = __ffs(flags[k]) - 1;
+          flags[k] &= flags[k] - 1;
+          role_fix<VAR>(sm, tid + NTHR * k, s, G * PW + slot_dx(G, s));
+        }
+      }
+      __syncwarp();
+    }
+  }
+  // ---- zero vectors: block-uniform slow path -----------------------------------
+  if (blk_zero) {
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      if (my_nn[k] == 0.0f) {
+        const int p = tid + NTHR * k;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const int off = G * PW + slot_dx(G, s);
+          sm.u.a.M[s][PRE + p] = 0.0f;
+          if (p - off >= 0) sm.u.a.M[s][PRE + p - off] = 0.0f;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- phase B: rows +G and -G of every pixel's neighbourhood into its role sums -----
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int q = PRE + tid + NTHR * k;
+    float vf[9], H[5];
+    if (G == 0) {   // row 0: (0, dx) for dx > 0 from the maps, dx < 0 from the neighbour's map
+#pragma unroll
+      for (int dx = 1; dx <= 4; ++dx) {
+        vf[4 + dx] = sm.u.a.M[dx - 1][q];
+        vf[4 - dx] = sm.u.a.M[dx - 1][q - dx];
+      }
+      vf[4] = -0.0f;   // the sample itself (-0 + x == x: folds away)
+    } else {
+#pragma unroll
+      for (int dx = -4; dx <= 4; ++dx) vf[4 + dx] = sm.u.a.M[dx + 4][q];
+    }
+    row_sums5(vf, H);
+#pragma unroll
+    for (int b = 0; b < 5; ++b)
+#pragma unroll
+      for (int a = 0; a < 5; ++a)
+        if (-a <= G && G <= 4 - a) Rs[k][a * 5 + b] += H[b];
+    if (G > 0) {    // row -G: A(q, q + (-G, dx)) = map of offset (G, -dx) at q + (-G, dx)
+      float vr[9];
+#pragma unroll
+      for (int dx = -4; dx <= 4; ++dx) vr[4 + dx] = sm.u.a.M[4 - dx][q - G * PW + dx];
+      row_sums5(vr, H);
+#pragma unroll
+      for (int b = 0; b < 5; ++b)
+#pragma unroll
+        for (int a = 0; a < 5; ++a)
+          if (-a <= -G && -G <= 4 - a) Rs[k][a * 5 + b] += H[b];
+    }
+  }
+}
+
+template <int VAR, int PPT, int... Gs>
+__device__ __forceinline__ void role_groups(std::integer_sequence<int, Gs...>, RoleSmem<PPT>& sm,
+                                            const uint32_t (&my_pk)[PPT], const float (&my_nn)[PPT],
+                                            const float (&my_nrm)[PPT], float (&Rs)[PPT][25], int tid, bool blk_zero) {
+  (role_group<VAR, PPT, Gs>(sm, my_pk, my_nn, my_nrm, Rs, tid, blk_zero), ...);
+}
+
+template <int VAR, int PPT>
+__global__ void __launch_bounds__(role::NTHR, 2) vf_angular_role_kernel(const Launch L) {
+  using namespace role;
+  constexpr int WIN = 5, R = 2, N = 25;
+  constexpr int NP = RoleSmem<PPT>::NP;
+  constexpr int PH = shared::region_h(PPT);
+  constexpr int TW = PW - 2 * R;            // output tile width (28)
+  constexpr int TH = PH - 2 * R;            // output tile height
+  constexpr int OPT = (TH + 7) / 8;         // outputs per thread (rows ty, ty+8, ty+16)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RoleSmem<PPT>& sm = *reinterpret_cast<RoleSmem<PPT>*>(smem_raw);
+
+  const int b = blockIdx.z;
+  const int ox0 = blockIdx.x * TW;
+  const int oy0 = L.out_row0 + blockIdx.y * TH;
+  const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;
+
+  // ---- stage the region --------------------------------------------------------------
+  uint32_t my_pk[PPT];
+  float my_nn[PPT], my_nrm[PPT];
+  bool has_zero = false;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int p = tid + NTHR * k;
+    const uint8_t* q = pixel_ptr(L, in, oy0 - R + (p >> 5), ox0 - R + (p & 31));
+    const uint32_t r = q[0], g = q[1], bl = q[2];
+    const float nn = (float)(r * r + g * g + bl * bl);          // exact
+    float nrm;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(nrm) : "f"(nn));
+    my_pk[k] = pack_rgb(r, g, bl);
+    my_nn[k] = nn;
+    my_nrm[k] = nrm;
+    has_zero |= (nn == 0.0f);
+    sm.u.a.px[p] = make_uint4(my_pk[k], __float_as_uint(nn), __float_as_uint(nrm), 0u);
+    sm.pk[p] = my_pk[k];
+  }
+  if (tid < shared::PAD) sm.u.a.px[NP + tid] = make_uint4(0u, 0u, 0u, 0u);
+  const bool blk_zero = __syncthreads_or(has_zero) != 0;
+
+  float Rs[PPT][25];
+#pragma unroll
+  for (int k = 0; k < PPT; ++k)
+#pragma unroll
+    for (int i = 0; i < 25; ++i) Rs[k][i] = -0.0f;   // -0 + v == v: the first add folds away
+  role_groups<VAR, PPT>(std::make_integer_sequence<int, 5>{}, sm, my_pk, my_nn, my_nrm, Rs, tid, blk_zero);
+
+  // ---- role sums replace the maps ------------------------------------------------------
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < PPT; ++k)
+#pragma unroll
+    for (int i = 0; i < 25; ++i) sm.u.S[i][tid + NTHR * k] = Rs[k][i];
+  __syncthreads();
+
+  // ---- outputs: 25 aggregates per window, argmin, store ---------------------------------
+#pragma unroll
+  for (int k = 0; k < OPT; ++k) {
+    const int oy = ty + 8 * k;
+    const int gy = oy0 + oy, gx = ox0 + tx;
+    if ((TH % 8 == 0 || oy < TH) && tx < TW && gx < L.W && gy < L.out_row0 + L.out_rows) {
+      const int t = oy * PW + tx;                             // region index of window sample (0, 0)
+      float Ra[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) Ra[i] = sm.u.S[i][t + (i / WIN) * PW + (i % WIN)];
+      float bv = Ra[0];
+      int so = 0;
+#pragma unroll
+      for (int i = 1; i < N; ++i) {
+        const bool lt = Ra[i] < bv;
+        bv = lt ? Ra[i] : bv;
+        so = lt ? (i / WIN) * PW + (i % WIN) : so;
+      }
+      store_result<N>(L, b, gx, gy, Ra, sm.pk[t + so]);
+    }
+  }
+}
+
+template <int PPT>
+inline const void* role_kernel_fn_t(int var) {
+  return var == EXACT ? (const void*)vf_angular_role_kernel<EXACT, PPT> : (const void*)vf_angular_role_kernel<MINIMAX, PPT>;
+}
+inline const void* role_kernel_fn(int var, int ppt) {
+  return ppt == 1 ? role_kernel_fn_t<1>(var) : (ppt == 2 ? role_kernel_fn_t<2>(var) : role_kernel_fn_t<3>(var));
+}
+inline size_t role_smem_bytes(int ppt) {
+  return ppt == 1 ? sizeof(RoleSmem<1>) : (ppt == 2 ? sizeof(RoleSmem<2>) : sizeof(RoleSmem<3>));
+}
+inline cudaError_t role_set_attributes() {
+  for (int ppt = 1; ppt <= 3; ++ppt)
+    for (int v = 0; v < 2; ++v) {
+      cudaError_t e = cudaFuncSetAttribute(role_kernel_fn(v, ppt), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)role_smem_bytes(ppt));
+      if (e != cudaSuccess) return e;
+    }
+  return cudaSuccess;
+}
+
+}  // namespace vf
