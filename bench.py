@@ -524,7 +524,9 @@ def main():
         ms = statistics.mean(kev[r][i][0].elapsed_time(kev[r][i][1]) for r in range(kreps))
         mpix = npix / (ms / 1e3) / 1e6
         tfl = FLOPS_PER_PAIR[c] * pairs * npix / (ms / 1e3) / 1e12
-        kern[f"{c[0]}/{c[1]}"] = {"kernel": KERNEL_NAMES[c[0]].format(w=w, v=c[1]), "ms": ms, "mpix_s": mpix,
+        kname = "vf_angular_role_kernel<{v}>".format(v=c[1]) if (c[0] == "angular" and w == 5) else \
+            KERNEL_NAMES[c[0]].format(w=w, v=c[1])
+        kern[f"{c[0]}/{c[1]}"] = {"kernel": kname, "ms": ms, "mpix_s": mpix,
                                   "alg_tflops": tfl, "frac_fp32_at_max_clock": tfl / NOMINAL_FP32_TFLOPS_AT_MAX}
         if clocks.get("sm_mhz"):
             kern[f"{c[0]}/{c[1]}"]["frac_fp32_at_measured_clock"] = \

@@ -17,5 +17,7 @@ if [ $rc -eq 0 ]; then
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:vf_ -s 7 -c 7 -o gpurun_out/prof_C2 python tools/prof_driver.py --config C2 > gpurun_out/ncu_C2.log 2>&1
   python tools/prof_driver.py --config C4 > /dev/null && \
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:vf_ -s 7 -c 7 -o gpurun_out/prof_C4 python tools/prof_driver.py --config C4 > gpurun_out/ncu_C4.log 2>&1
+  python tools/prof_driver.py --config C3 --rounds 1 > /dev/null && \
+  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:vf_ -s 7 -c 7 -o gpurun_out/prof_C3 python tools/prof_driver.py --config C3 > gpurun_out/ncu_C3.log 2>&1
 fi
 tail -2 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; tail -1 gpurun_out/bench.err; tail -1 gpurun_out/ncu_launch.log

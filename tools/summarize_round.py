@@ -20,15 +20,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 CRIT = {0: "angular", 1: "exp", 2: "log"}
-VAR = {0: "exact", 1: "minimax", 2: "poly4"}
+VAR = {0: "exact", 1: "minimax", 2: "poly4", 3: "reach"}
 
 
 def kernel_key(name):
     name = name.replace("(int)", "")
+    m = re.search(r"vf_angular_role_kernel<(\d), \d>", name)
+    if m:
+        return f"angular/{VAR[int(m.group(1))]}", 5
     m = re.search(r"vf_angular_(shared|window)_kernel<(\d), (\d)(?:, \d)?>", name)
     if m:
         return f"angular/{VAR[int(m.group(3))]}", int(m.group(2))
-    m = re.search(r"vf_el_kernel<(\d), (\d), (\d)(?:, \d)?>", name)
+    m = re.search(r"vf_el(?:_tma)?_kernel<(\d), (\d), (\d)(?:, \d)?>", name)
     if m:
         return f"{CRIT[int(m.group(2))]}/{VAR[int(m.group(3))]}", int(m.group(1))
     return None, None
@@ -131,6 +134,7 @@ def main():
                        "algorithmic bytes = 3 B in + 3 B out per pixel"}
     ncu_full(tag, "C2", 512 * 512, summary)
     ncu_full(tag, "C4", 16 * 512 * 768, summary)
+    ncu_full(tag, "C3", 8 * 2048 * 2048, summary)
     with open(os.path.join(PROF, "ncu_summary.json"), "w") as fh:
         json.dump(summary, fh, indent=1)
     for cfg, src in (("C2", "bench.json"), ("C3", "bench_C3.json"), ("C4", "bench_C4.json")):
