@@ -94,3 +94,25 @@ def test_c1_rectangles_only_and_smooth_background():
     d = np.abs(np.diff(c.astype(int), axis=1)).max(-1)
     assert np.median(d) <= 4
     assert all(o[0] == "rect" for o in vfsynth._objects(s, 0))
+
+
+def test_mixed_model_gaussian_then_correlated():
+    """P:263 mixed model: Gaussian (sigma per channel, rounded, clamped) then
+    correlated impulsive with phi_k.  sigma = 0 equals the correlated_phik
+    image bit for bit; without impulses the residual of a
+    mid-grey image is N(0, sigma^2) rounded (mean ~0, std ~sigma, symmetric)."""
+    base = dict(H=256, W=256, batch=1, window=(3,), n_objects=0, rects_only=True, p=0.1, seed=9)
+    s0 = vfsynth.ImageSpec("t", noise="mixed", sigma=0.0, **base)
+    sc = vfsynth.ImageSpec("t", noise="correlated_phik", **base)
+    assert np.array_equal(vfsynth.make_image(s0, 0)[1], vfsynth.make_image(sc, 0)[1])
+    sg = vfsynth.ImageSpec("t", noise="mixed", sigma=10.0, **dict(base, p=0.0))
+    c, x = vfsynth.make_image(sg, 0)
+    interior = (c > 40) & (c < 215)             # away from the clamps
+    r = (x.astype(np.float64) - c)[interior]
+    assert abs(r.mean()) < 0.1
+    assert abs(r.std() - math.sqrt(100.0 + 1.0 / 12.0)) < 0.15   # rounding adds 1/12
+    assert abs(np.mean(r > 0) - np.mean(r < 0)) < 0.01
+    # row bands of the mixed model equal the full image (counter-based RNG)
+    sm = vfsynth.ImageSpec("t", noise="mixed", **base)
+    full = vfsynth.make_image(sm, 0)[1]
+    assert np.array_equal(vfsynth.make_image(sm, 0, 100, 180)[1], full[100:180])
