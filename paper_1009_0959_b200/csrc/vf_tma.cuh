@@ -89,8 +89,11 @@ struct Smem {
 // loop otherwise keeps loop-invariant values in registers at the cost of
 // occupancy): 5 (<= 48 registers) for the 3x3 polynomial variants with 1-2
 // rows per thread, 4 with 4 rows, 3 (<= 80) for the libm variants and 5x5.
+#ifndef VF_TMA_MINB_OPT4
+#define VF_TMA_MINB_OPT4 4   // tuning knob (tools/dev experiments)
+#endif
 template <int WIN, int VAR, int OPT>
-constexpr int el_tma_min_blocks() { return (WIN == 3 && VAR != EXACT) ? (OPT <= 2 ? 5 : 4) : 3; }
+constexpr int el_tma_min_blocks() { return (WIN == 3 && VAR != EXACT) ? (OPT <= 2 ? 5 : VF_TMA_MINB_OPT4) : 3; }
 
 template <int WIN, int CRIT, int VAR, int OPT>
 __global__ void __launch_bounds__(TX * TY, el_tma_min_blocks<WIN, VAR, OPT>()) vf_el_tma_kernel(const __grid_constant__ CUtensorMap map, const Launch L,

@@ -18,7 +18,7 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-PROF = os.path.join(ROOT, "profiles")
+PROF = os.environ.get("VF_PROF_DIR", os.path.join(ROOT, "profiles"))
 CRIT = {0: "angular", 1: "exp", 2: "log"}
 VAR = {0: "exact", 1: "minimax", 2: "poly4", 3: "reach"}
 
