@@ -192,10 +192,11 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
     // 5x5: per-pixel role sums (vf_role.cuh) unless the per-window
     // accumulation is asked for explicitly
     if (window == 5 && algo != VF_ALGO_SHARED) {
-      kd->fn = vf::role_kernel_fn(var, ppt);
-      kd->grid = vf::shared_grid(L, B, window, ppt);
-      kd->block = dim3(vf::shared::NTHR);
-      kd->smem = vf::role_smem_bytes(ppt);
+      const int cfg = tile ? tile : (ppt_env >= 1 && ppt_env <= 3 ? ppt_env : 4);   // 4: 384 threads x 2 px
+      kd->fn = vf::role_kernel_fn(var, cfg);
+      kd->grid = vf::role_grid(L, B, cfg);
+      kd->block = dim3(vf::role_threads(cfg));
+      kd->smem = vf::role_smem_bytes(cfg);
       const cudaError_t e = ensure_attributes();
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
       return VF_OK;

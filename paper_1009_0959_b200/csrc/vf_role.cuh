@@ -36,16 +36,17 @@ namespace vf {
 
 namespace role {
 constexpr int PW = shared::PW;          // region width (32)
-constexpr int NTHR = shared::NTHR;      // 256
 constexpr int PRE = 5 * PW;             // map padding before the region: reverse reads reach 4 rows + 4 px back
 constexpr int POST = 5 * PW;            // and after it
 __host__ __device__ constexpr int nslots(int g) { return g == 0 ? 4 : 9; }
 __host__ __device__ constexpr int slot_dx(int g, int s) { return g == 0 ? s + 1 : s - 4; }
 }  // namespace role
 
-template <int PPT>
+// Block of NT threads (256 or 384) over a 32 x (NT PPT / 32) region, PPT
+// region pixels per thread.
+template <int NT, int PPT>
 struct RoleSmem {
-  static constexpr int NP = shared::region_np(PPT);
+  static constexpr int NP = NT * PPT;
   static constexpr int MS = role::PRE + NP + role::POST;   // map stride (floats)
   static constexpr int QCAP = 64;
   struct Maps {
@@ -57,13 +58,13 @@ struct RoleSmem {
     float S[25][NP];              // role sums, after the last group
   } u;
   uint32_t pk[NP];                // packed RGB of the region (output store)
-  uint32_t queue[role::NTHR / 32][QCAP];
+  uint32_t queue[NT / 32][QCAP];
 };
 
 // Exact re-decision of a flagged pair (p, p + (g, dx)) of slot s: as
 // angular_fix in vf_shared.cuh, on this kernel's map layout.
-template <int VAR, int PPT>
-__device__ __forceinline__ void role_fix(RoleSmem<PPT>& sm, int p, int s, int off) {
+template <int VAR, int NT, int PPT>
+__device__ __forceinline__ void role_fix(RoleSmem<NT, PPT>& sm, int p, int s, int off) {
   const uint4 pv = sm.u.a.px[p], qv = sm.u.a.px[p + off];
   const float D = __uint_as_float(__dp4a(pv.x, qv.x, F2P23_BITS)) - F2P23;   // exact dot
   const float nna = __uint_as_float(pv.y), nnb = __uint_as_float(qv.y);
@@ -88,12 +89,13 @@ __device__ __forceinline__ void row_sums5(const float (&v)[9], float (&H)[5]) {
   H[4] = (v[0] + a12) + (v[3] + v[4]);
 }
 
-template <int VAR, int PPT, int G>
-__device__ __forceinline__ void role_group(RoleSmem<PPT>& sm, const uint32_t (&my_pk)[PPT], const float (&my_nn)[PPT],
+template <int VAR, int NT, int PPT, int G>
+__device__ __forceinline__ void role_group(RoleSmem<NT, PPT>& sm, const uint32_t (&my_pk)[PPT], const float (&my_nn)[PPT],
                                            const float (&my_nrm)[PPT], float (&Rs)[PPT][25], int tid, bool blk_zero) {
   using namespace role;
   constexpr int NS = nslots(G);
-  constexpr int QCAP = RoleSmem<PPT>::QCAP;
+  constexpr int QCAP = RoleSmem<NT, PPT>::QCAP;
+  constexpr int NPL = RoleSmem<NT, PPT>::NP;
   const int lane = tid & 31, warp = tid >> 5;
   if (G > 0) __syncthreads();   // previous phase B done with the maps (G = 0: the staging barrier)
   // ---- phase A: maps of the offsets (G, dx) ----------------------------------------
@@ -105,8 +107,8 @@ __device__ __forceinline__ void role_group(RoleSmem<PPT>& sm, const uint32_t (&m
     const int off = G * PW + slot_dx(G, s);
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
-      const int p = tid + NTHR * k;
-      VF_CHECK(p + off >= 0 && p + off < RoleSmem<PPT>::NP + shared::PAD);
+      const int p = tid + NT * k;
+      VF_CHECK(p + off >= 0 && p + off < NPL + shared::PAD);
       const uint4 qv = sm.u.a.px[p + off];
       const float D = __uint_as_float(__dp4a(my_pk[k], qv.x, F2P23_BITS)) - F2P23;   // exact dot
       const float nnq = __uint_as_float(qv.y);
@@ -137,7 +139,7 @@ __device__ __forceinline__ void role_group(RoleSmem<PPT>& sm, const uint32_t (&m
       uint32_t* q = sm.queue[warp];
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        const uint32_t p = tid + NTHR * k;
+        const uint32_t p = tid + NT * k;
         while (flags[k] && pos < QCAP) {
           const uint32_t s = __ffs(flags[k]) - 1;
           flags[k] &= flags[k] - 1;
@@ -156,7 +158,7 @@ __device__ __forceinline__ void role_group(RoleSmem<PPT>& sm, const uint32_t (&m
         while (flags[k]) {
           const int s = __ffs(flags[k]) - 1;
           flags[k] &= flags[k] - 1;
-          role_fix<VAR>(sm, tid + NTHR * k, s, G * PW + slot_dx(G, s));
+          role_fix<VAR>(sm, tid + NT * k, s, G * PW + slot_dx(G, s));
         }
       }
       __syncwarp();
@@ -168,7 +170,7 @@ __device__ __forceinline__ void role_group(RoleSmem<PPT>& sm, const uint32_t (&m
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       if (my_nn[k] == 0.0f) {
-        const int p = tid + NTHR * k;
+        const int p = tid + NT * k;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
           const int off = G * PW + slot_dx(G, s);
@@ -182,7 +184,7 @@ __device__ __forceinline__ void role_group(RoleSmem<PPT>& sm, const uint32_t (&m
   // ---- phase B: rows +G and -G of every pixel's neighbourhood into its role sums -----
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
-    const int q = PRE + tid + NTHR * k;
+    const int q = PRE + tid + NT * k;
     float vf[9], H[5];
     if (G == 0) {   // row 0: (0, dx) for dx > 0 from the maps, dx < 0 from the neighbour's map
 #pragma unroll
@@ -215,24 +217,25 @@ __device__ __forceinline__ void role_group(RoleSmem<PPT>& sm, const uint32_t (&m
   }
 }
 
-template <int VAR, int PPT, int... Gs>
-__device__ __forceinline__ void role_groups(std::integer_sequence<int, Gs...>, RoleSmem<PPT>& sm,
+template <int VAR, int NT, int PPT, int... Gs>
+__device__ __forceinline__ void role_groups(std::integer_sequence<int, Gs...>, RoleSmem<NT, PPT>& sm,
                                             const uint32_t (&my_pk)[PPT], const float (&my_nn)[PPT],
                                             const float (&my_nrm)[PPT], float (&Rs)[PPT][25], int tid, bool blk_zero) {
-  (role_group<VAR, PPT, Gs>(sm, my_pk, my_nn, my_nrm, Rs, tid, blk_zero), ...);
+  (role_group<VAR, NT, PPT, Gs>(sm, my_pk, my_nn, my_nrm, Rs, tid, blk_zero), ...);
 }
 
-template <int VAR, int PPT>
-__global__ void __launch_bounds__(role::NTHR, 2) vf_angular_role_kernel(const Launch L) {
+template <int VAR, int NT, int PPT>
+__global__ void __launch_bounds__(NT, 2) vf_angular_role_kernel(const Launch L) {
   using namespace role;
   constexpr int WIN = 5, R = 2, N = 25;
-  constexpr int NP = RoleSmem<PPT>::NP;
-  constexpr int PH = shared::region_h(PPT);
+  constexpr int NW = NT / 32;               // warps = region rows per pixel slab
+  constexpr int NP = RoleSmem<NT, PPT>::NP;
+  constexpr int PH = NP / PW;               // region height
   constexpr int TW = PW - 2 * R;            // output tile width (28)
   constexpr int TH = PH - 2 * R;            // output tile height
-  constexpr int OPT = (TH + 7) / 8;         // outputs per thread (rows ty, ty+8, ty+16)
+  constexpr int OPT = (TH + NW - 1) / NW;   // outputs per thread (rows ty, ty + NW, ...)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  RoleSmem<PPT>& sm = *reinterpret_cast<RoleSmem<PPT>*>(smem_raw);
+  RoleSmem<NT, PPT>& sm = *reinterpret_cast<RoleSmem<NT, PPT>*>(smem_raw);
 
   const int b = blockIdx.z;
   const int ox0 = blockIdx.x * TW;
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(role::NTHR, 2) vf_angular_role_kernel(const La
   bool has_zero = false;
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
-    const int p = tid + NTHR * k;
+    const int p = tid + NT * k;
     const uint8_t* q = pixel_ptr(L, in, oy0 - R + (p >> 5), ox0 - R + (p & 31));
     const uint32_t r = q[0], g = q[1], bl = q[2];
     const float nn = (float)(r * r + g * g + bl * bl);          // exact
@@ -268,22 +271,22 @@ __global__ void __launch_bounds__(role::NTHR, 2) vf_angular_role_kernel(const La
   for (int k = 0; k < PPT; ++k)
 #pragma unroll
     for (int i = 0; i < 25; ++i) Rs[k][i] = -0.0f;   // -0 + v == v: the first add folds away
-  role_groups<VAR, PPT>(std::make_integer_sequence<int, 5>{}, sm, my_pk, my_nn, my_nrm, Rs, tid, blk_zero);
+  role_groups<VAR, NT, PPT>(std::make_integer_sequence<int, 5>{}, sm, my_pk, my_nn, my_nrm, Rs, tid, blk_zero);
 
   // ---- role sums replace the maps ------------------------------------------------------
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < PPT; ++k)
 #pragma unroll
-    for (int i = 0; i < 25; ++i) sm.u.S[i][tid + NTHR * k] = Rs[k][i];
+    for (int i = 0; i < 25; ++i) sm.u.S[i][tid + NT * k] = Rs[k][i];
   __syncthreads();
 
   // ---- outputs: 25 aggregates per window, argmin, store ---------------------------------
 #pragma unroll
   for (int k = 0; k < OPT; ++k) {
-    const int oy = ty + 8 * k;
+    const int oy = ty + NW * k;
     const int gy = oy0 + oy, gx = ox0 + tx;
-    if ((TH % 8 == 0 || oy < TH) && tx < TW && gx < L.W && gy < L.out_row0 + L.out_rows) {
+    if ((TH % NW == 0 || oy < TH) && tx < TW && gx < L.W && gy < L.out_row0 + L.out_rows) {
       const int t = oy * PW + tx;                             // region index of window sample (0, 0)
       float Ra[N];
 #pragma unroll
@@ -301,24 +304,45 @@ __global__ void __launch_bounds__(role::NTHR, 2) vf_angular_role_kernel(const La
   }
 }
 
-template <int PPT>
+// Launch configurations: cfg 1..3 = 256 threads with 1..3 pixels each; cfg 4
+// (default) = 384 threads with 2 pixels each: the same 32 x 24 region as cfg 3
+// (halo overhead 1.37) with 50 instead of 75 role accumulators per thread,
+// so two blocks of 12 warps fit per SM instead of two of 8.
+template <int NT, int PPT>
 inline const void* role_kernel_fn_t(int var) {
-  return var == EXACT ? (const void*)vf_angular_role_kernel<EXACT, PPT> : (const void*)vf_angular_role_kernel<MINIMAX, PPT>;
+  return var == EXACT ? (const void*)vf_angular_role_kernel<EXACT, NT, PPT>
+                      : (const void*)vf_angular_role_kernel<MINIMAX, NT, PPT>;
 }
-inline const void* role_kernel_fn(int var, int ppt) {
-  return ppt == 1 ? role_kernel_fn_t<1>(var) : (ppt == 2 ? role_kernel_fn_t<2>(var) : role_kernel_fn_t<3>(var));
+inline const void* role_kernel_fn(int var, int cfg) {
+  switch (cfg) {
+    case 1: return role_kernel_fn_t<256, 1>(var);
+    case 2: return role_kernel_fn_t<256, 2>(var);
+    case 3: return role_kernel_fn_t<256, 3>(var);
+    default: return role_kernel_fn_t<384, 2>(var);
+  }
 }
-inline size_t role_smem_bytes(int ppt) {
-  return ppt == 1 ? sizeof(RoleSmem<1>) : (ppt == 2 ? sizeof(RoleSmem<2>) : sizeof(RoleSmem<3>));
+inline int role_threads(int cfg) { return (cfg >= 1 && cfg <= 3) ? 256 : 384; }
+inline int role_region_h(int cfg) { return (cfg >= 1 && cfg <= 3) ? 8 * cfg : 24; }
+inline size_t role_smem_bytes(int cfg) {
+  switch (cfg) {
+    case 1: return sizeof(RoleSmem<256, 1>);
+    case 2: return sizeof(RoleSmem<256, 2>);
+    case 3: return sizeof(RoleSmem<256, 3>);
+    default: return sizeof(RoleSmem<384, 2>);
+  }
 }
 inline cudaError_t role_set_attributes() {
-  for (int ppt = 1; ppt <= 3; ++ppt)
+  for (int cfg = 1; cfg <= 4; ++cfg)
     for (int v = 0; v < 2; ++v) {
-      cudaError_t e = cudaFuncSetAttribute(role_kernel_fn(v, ppt), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)role_smem_bytes(ppt));
+      cudaError_t e = cudaFuncSetAttribute(role_kernel_fn(v, cfg), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)role_smem_bytes(cfg));
       if (e != cudaSuccess) return e;
     }
   return cudaSuccess;
+}
+inline dim3 role_grid(const Launch& L, int B, int cfg) {
+  const int TW = shared::PW - 4, TH = role_region_h(cfg) - 4;
+  return dim3((L.W + TW - 1) / TW, (L.out_rows + TH - 1) / TH, B);
 }
 
 }  // namespace vf
