@@ -182,17 +182,19 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
   const bool no_tma = (algo & VF_ALGO_NO_TMA) != 0;
   algo &= 3;
   if (crit == VF_ANGULAR && algo != VF_ALGO_WINDOW) {
-    // region height: 3 pixels per thread measured fastest at every size
-    // (C2 262 K px, C4 6.3 M px, C3 33.5 M px; tools/tune_tiles.sh).
-    // VF_SHARED_PPT=1..3 or the algo tile bits override, for tuning and tests.
-    int ppt = 3;
+    // launch configuration (vf_shared.cuh: 1..3 = 256 threads x 1..3 region
+    // pixels, 4 = 384 threads x 2 in a 32 x 24 region): 4 measured fastest
+    // for the 3x3 sharing kernel (40 registers, 48 warps per SM: C2 -7%, C4
+    // -1.5% vs 256 x 3) and for the 5x5 role-sum kernel (C3 -15%;
+    // tools/tune_tiles.sh).  VF_SHARED_PPT=1..4 or the algo tile bits (1..3)
+    // override, for tuning and tests.
     static const int ppt_env = [] { const char* e = std::getenv("VF_SHARED_PPT"); return e ? std::atoi(e) : 0; }();
-    if (ppt_env >= 1 && ppt_env <= 3) ppt = ppt_env;
+    int ppt = (ppt_env >= 1 && ppt_env <= 4) ? ppt_env : 4;
     if (tile) ppt = tile;
     // 5x5: per-pixel role sums (vf_role.cuh) unless the per-window
     // accumulation is asked for explicitly
     if (window == 5 && algo != VF_ALGO_SHARED) {
-      const int cfg = tile ? tile : (ppt_env >= 1 && ppt_env <= 3 ? ppt_env : 4);   // 4: 384 threads x 2 px
+      const int cfg = tile ? tile : (ppt_env >= 1 && ppt_env <= 4 ? ppt_env : 4);   // 4: 384 threads x 2 px
       kd->fn = vf::role_kernel_fn(var, cfg);
       kd->grid = vf::role_grid(L, B, cfg);
       kd->block = dim3(vf::role_threads(cfg));
@@ -203,7 +205,7 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
     }
     kd->fn = vf::shared_kernel_fn(window, var, ppt);
     kd->grid = vf::shared_grid(L, B, window, ppt);
-    kd->block = dim3(vf::shared::NTHR);
+    kd->block = dim3(vf::shared::cfg_nt(ppt));
     kd->smem = vf::shared_smem_bytes(window, ppt);
     const cudaError_t e = ensure_attributes();
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");

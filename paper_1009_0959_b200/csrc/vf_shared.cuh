@@ -32,6 +32,10 @@
 
 #include "vf_window.cuh"
 
+#ifndef SHARED_MINB_CFG4
+#define SHARED_MINB_CFG4 4   // 384-thread blocks: <= 40 registers, 48 warps per SM (tuning knob)
+#endif
+
 namespace vf {
 
 namespace shared {
@@ -39,10 +43,14 @@ namespace shared {
 constexpr int PW = 32;              // region width  (= warp width)
 constexpr int PAD = 5 * PW;         // reads past the region stay in bounds
 constexpr int NTHR = 256;
+// Launch configurations (CFG): 1..3 = 256 threads with CFG region pixels each
+// (region 32 x 8 CFG); 4 = 384 threads with 2 pixels each (region 32 x 24).
+__host__ __device__ constexpr int cfg_nt(int cfg) { return cfg == 4 ? 384 : 256; }
+__host__ __device__ constexpr int cfg_ppt(int cfg) { return cfg == 4 ? 2 : cfg; }
 // PPT = region pixels per thread (1..3): region 32 x 8 PPT.  Large images use
 // PPT = 3 (least halo overhead), small ones fewer so more blocks fill the GPU.
-__host__ __device__ constexpr int region_h(int ppt) { return 8 * ppt; }
-__host__ __device__ constexpr int region_np(int ppt) { return PW * 8 * ppt; }
+__host__ __device__ constexpr int region_np(int cfg) { return cfg_nt(cfg) * cfg_ppt(cfg); }
+__host__ __device__ constexpr int region_h(int cfg) { return region_np(cfg) / PW; }
 
 __host__ __device__ constexpr int n_delta(int r) { return 4 * r * (2 * r + 1); }
 // offset index d -> (dy, dx): d < 2r: (0, d+1); else dy = 1 + (d-2r)/(4r+1), dx = -2r + (d-2r)%(4r+1)
@@ -55,12 +63,12 @@ __host__ __device__ constexpr int delta_index(int r, int dy, int dx) {
 }  // namespace shared
 
 // Per-block shared-memory state of the pair-sharing kernel.
-template <int GD, int PPT>
+template <int GD, int CFG>
 struct SharedSmem {
   static constexpr int QCAP = 64;                   // rare-pair queue entries per warp
-  uint4 px[shared::region_np(PPT) + shared::PAD];   // (packed RGB0, |x|^2 bits, |x| bits, 0): one LDS.128 per neighbour
-  float M[GD][shared::region_np(PPT)];
-  uint32_t queue[shared::NTHR / 32][QCAP];          // flagged pairs of one warp: p | dl << 16
+  uint4 px[shared::region_np(CFG) + shared::PAD];   // (packed RGB0, |x|^2 bits, |x| bits, 0): one LDS.128 per neighbour
+  float M[GD][shared::region_np(CFG)];
+  uint32_t queue[shared::cfg_nt(CFG) / 32][QCAP];   // flagged pairs of one warp: p | dl << 16
   int off[40];                                      // region offset of pair offset d (d < n_delta(r) <= 40)
 };
 
@@ -69,8 +77,8 @@ struct SharedSmem {
 // arccos branch (cos < 0.5), its map entry is replaced by the ARCCOS row /
 // acosf of cos = D / (|x_p||x_q|).  Zero vectors never get here (tau = 0 is
 // never flagged) and are handled by the block-uniform path anyway.
-template <int VAR, int GD, int PPT>
-__device__ __forceinline__ void angular_fix(SharedSmem<GD, PPT>& sm, int p, int dl, int d) {
+template <int VAR, int GD, int CFG>
+__device__ __forceinline__ void angular_fix(SharedSmem<GD, CFG>& sm, int p, int dl, int d) {
   const uint4 pv = sm.px[p], qv = sm.px[p + sm.off[d]];
   const float D = __uint_as_float(__dp4a(pv.x, qv.x, F2P23_BITS)) - F2P23;   // exact dot
   const float nna = __uint_as_float(pv.y), nnb = __uint_as_float(qv.y);
@@ -85,17 +93,21 @@ __device__ __forceinline__ void angular_fix(SharedSmem<GD, PPT>& sm, int p, int 
 
 // One group of GD offsets: phase A (pair maps) + rare fix-ups + phase C.
 // G is a template parameter so that every register index stays static.
-template <int WIN, int VAR, int GD, int OPT, int PPT, int G>
-__device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint32_t (&my_pk)[PPT],
-                                             const float (&my_nn)[PPT], const float (&my_nrm)[PPT],
+template <int WIN, int VAR, int GD, int OPT, int CFG, int G>
+__device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint32_t (&my_pk)[shared::cfg_ppt(CFG)],
+                                             const float (&my_nn)[shared::cfg_ppt(CFG)],
+                                             const float (&my_nrm)[shared::cfg_ppt(CFG)],
                                              float (&Ra)[OPT][WIN * WIN], int tid, bool blk_zero) {
   using namespace shared;
-  constexpr int PH = region_h(PPT);
+  constexpr int PPT = cfg_ppt(CFG);
+  constexpr int NT = cfg_nt(CFG);
+  constexpr int NW = NT / 32;
+  constexpr int PH = region_h(CFG);
   constexpr int R = WIN / 2;
   constexpr int N = WIN * WIN;
   constexpr int TW = PW - 2 * R;
   constexpr int TH = PH - 2 * R;
-  constexpr int QCAP = SharedSmem<GD, PPT>::QCAP;
+  constexpr int QCAP = SharedSmem<GD, CFG>::QCAP;
   const int tx = tid & 31, ty = tid >> 5;
   if (G > 0) __syncthreads();   // previous phase C done with M (G = 0: the staging barrier)
   // ---- phase A: pair maps for offsets [G*GD, G*GD + GD) ------------------------------
@@ -108,9 +120,9 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
     const int off = delta_dy(R, d) * PW + delta_dx(R, d);
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
-      const int p = tid + NTHR * k;
+      const int p = tid + NT * k;
       const int q = p + off;                                  // in bounds (PAD); garbage if outside P
-      VF_CHECK(q >= 0 && q < region_np(PPT) + PAD);
+      VF_CHECK(q >= 0 && q < region_np(CFG) + PAD);
       const uint4 qv = sm.px[q];
       const uint32_t qk = qv.x;
       const float2 qn = make_float2(__uint_as_float(qv.y), __uint_as_float(qv.z));
@@ -155,7 +167,7 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
       uint32_t* q = sm.queue[ty];
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        const uint32_t p = tid + NTHR * k;
+        const uint32_t p = tid + NT * k;
         while (flags[k] && pos < QCAP) {
           const uint32_t dl = __ffs(flags[k]) - 1;
           flags[k] &= flags[k] - 1;
@@ -173,7 +185,7 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
         while (flags[k]) {
           const int dl = __ffs(flags[k]) - 1;
           flags[k] &= flags[k] - 1;
-          angular_fix<VAR>(sm, tid + NTHR * k, dl, G * GD + dl);
+          angular_fix<VAR>(sm, tid + NT * k, dl, G * GD + dl);
         }
       }
       __syncwarp();                                           // queue reusable by the next group
@@ -187,7 +199,7 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       if (my_nn[k] == 0.0f) {
-        const int p = tid + NTHR * k;
+        const int p = tid + NT * k;
 #pragma unroll
         for (int dl = 0; dl < GD; ++dl) {
           const int d = G * GD + dl;
@@ -205,8 +217,8 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
   // addition of each folds away.
 #pragma unroll
   for (int k = 0; k < OPT; ++k) {
-    const int oy = ty + 8 * k;
-    if ((TH % 8 == 0 || oy < TH) && tx < TW) {
+    const int oy = ty + NW * k;
+    if ((TH % NW == 0 || oy < TH) && tx < TW) {
       const int base = oy * PW + tx;                          // P index of window sample (0,0)
 #pragma unroll
       for (int i = 0; i < N; ++i) {
@@ -214,7 +226,7 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
         for (int j = i + 1; j < N; ++j) {
           const int d = delta_index(R, j / WIN - i / WIN, j % WIN - i % WIN);
           if (d / GD == G) {
-            VF_CHECK(base + (i / WIN) * PW + (i % WIN) < region_np(PPT));
+            VF_CHECK(base + (i / WIN) * PW + (i % WIN) < region_np(CFG));
             const float v = sm.M[d - G * GD][base + (i / WIN) * PW + (i % WIN)];
             Ra[k][i] += v;
             Ra[k][j] += v;
@@ -225,19 +237,28 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, PPT>& sm, const uint
   }
 }
 
-template <int WIN, int VAR, int GD, int OPT, int PPT, int... Gs>
-__device__ __forceinline__ void shared_groups(std::integer_sequence<int, Gs...>, SharedSmem<GD, PPT>& sm,
-                                              const uint32_t (&my_pk)[PPT], const float (&my_nn)[PPT],
-                                              const float (&my_nrm)[PPT], float (&Ra)[OPT][WIN * WIN], int tid,
-                                              bool blk_zero) {
-  (shared_group<WIN, VAR, GD, OPT, PPT, Gs>(sm, my_pk, my_nn, my_nrm, Ra, tid, blk_zero), ...);
+template <int WIN, int VAR, int GD, int OPT, int CFG, int... Gs>
+__device__ __forceinline__ void shared_groups(std::integer_sequence<int, Gs...>, SharedSmem<GD, CFG>& sm,
+                                              const uint32_t (&my_pk)[shared::cfg_ppt(CFG)],
+                                              const float (&my_nn)[shared::cfg_ppt(CFG)],
+                                              const float (&my_nrm)[shared::cfg_ppt(CFG)], float (&Ra)[OPT][WIN * WIN],
+                                              int tid, bool blk_zero) {
+  (shared_group<WIN, VAR, GD, OPT, CFG, Gs>(sm, my_pk, my_nn, my_nrm, Ra, tid, blk_zero), ...);
 }
 
-template <int WIN, int VAR, int PPT>
-__global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_shared_kernel(const Launch L) {
+// Resident blocks per SM the register allocation is held to.
+__host__ __device__ constexpr int shared_min_blocks(int win, int cfg) {
+  return win == 5 ? 2 : (cfg == 4 ? SHARED_MINB_CFG4 : 4);
+}
+
+template <int WIN, int VAR, int CFG>
+__global__ void __launch_bounds__(shared::cfg_nt(CFG), shared_min_blocks(WIN, CFG)) vf_angular_shared_kernel(const Launch L) {
   using namespace shared;
-  constexpr int PH = region_h(PPT);
-  constexpr int NP = region_np(PPT);
+  constexpr int NT = cfg_nt(CFG);
+  constexpr int NW = NT / 32;
+  constexpr int PPT = cfg_ppt(CFG);
+  constexpr int PH = region_h(CFG);
+  constexpr int NP = region_np(CFG);
   constexpr int R = WIN / 2;
   constexpr int N = WIN * WIN;
   constexpr int TW = PW - 2 * R;            // output tile width
@@ -245,10 +266,10 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
   constexpr int ND = n_delta(R);            // 12 or 40
   constexpr int GD = (WIN == 3) ? 12 : 10;  // offsets per group
   constexpr int NG = ND / GD;
-  constexpr int OPT = (TH + 7) / 8;         // outputs per thread (rows ty, ty+8, ty+16)
+  constexpr int OPT = (TH + NW - 1) / NW;   // outputs per thread (rows ty, ty + NW, ...)
   static_assert(ND % GD == 0, "groups must tile the offsets");
-  extern __shared__ __align__(16) unsigned char smem_raw[];   // sizeof(SharedSmem<GD, PPT>), dynamic (> 48 KB)
-  SharedSmem<GD, PPT>& sm = *reinterpret_cast<SharedSmem<GD, PPT>*>(smem_raw);
+  extern __shared__ __align__(16) unsigned char smem_raw[];   // sizeof(SharedSmem<GD, CFG>), dynamic (> 48 KB)
+  SharedSmem<GD, CFG>& sm = *reinterpret_cast<SharedSmem<GD, CFG>*>(smem_raw);
 
   const int b = blockIdx.z;
   const int ox0 = blockIdx.x * TW;                        // output tile origin (global)
@@ -263,7 +284,7 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
   bool has_zero = false;
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
-    const int p = tid + NTHR * k;
+    const int p = tid + NT * k;
     const int py = p >> 5, px = p & 31;
     const uint8_t* q = pixel_ptr(L, in, oy0 - R + py, ox0 - R + px);
     const uint32_t r = q[0], g = q[1], bl = q[2];
@@ -286,15 +307,15 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
 #pragma unroll
     for (int i = 0; i < N; ++i) Ra[k][i] = -0.0f;
 
-  shared_groups<WIN, VAR, GD, OPT, PPT>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, Ra, tid,
+  shared_groups<WIN, VAR, GD, OPT, CFG>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, Ra, tid,
                                         blk_zero);
 
   // ---- argmin + store ------------------------------------------------------------------
 #pragma unroll
   for (int k = 0; k < OPT; ++k) {
-    const int oy = ty + 8 * k;
+    const int oy = ty + NW * k;
     const int gy = oy0 + oy, gx = ox0 + tx;
-    if ((TH % 8 == 0 || oy < TH) && tx < TW && gx < L.W && gy < L.out_row0 + L.out_rows) {
+    if ((TH % NW == 0 || oy < TH) && tx < TW && gx < L.W && gy < L.out_row0 + L.out_rows) {
       // argmin over the window (lowest index on ties), tracking the region
       // offset of the selected sample, then one load of its packed RGB
       const int base = oy * PW + tx;
@@ -311,41 +332,58 @@ __global__ void __launch_bounds__(shared::NTHR, WIN == 3 ? 4 : 2) vf_angular_sha
   }
 }
 
-// Kernel + grid of the pair-sharing kernel for a launch (see vf_api.cu).
-template <int WIN, int PPT>
+// Kernel + grid of the pair-sharing kernel for a launch (see vf_api.cu);
+// cfg = launch configuration (shared::cfg_nt / cfg_ppt).
+template <int WIN, int CFG>
 inline const void* shared_kernel_fn_t(int var) {
-  return var == EXACT ? (const void*)vf_angular_shared_kernel<WIN, EXACT, PPT>
-                      : (const void*)vf_angular_shared_kernel<WIN, MINIMAX, PPT>;
+  return var == EXACT ? (const void*)vf_angular_shared_kernel<WIN, EXACT, CFG>
+                      : (const void*)vf_angular_shared_kernel<WIN, MINIMAX, CFG>;
 }
 
-inline const void* shared_kernel_fn(int window, int var, int ppt) {
-  if (window == 3) return ppt == 1 ? shared_kernel_fn_t<3, 1>(var) : (ppt == 2 ? shared_kernel_fn_t<3, 2>(var)
-                                                                               : shared_kernel_fn_t<3, 3>(var));
-  return ppt == 1 ? shared_kernel_fn_t<5, 1>(var) : (ppt == 2 ? shared_kernel_fn_t<5, 2>(var) : shared_kernel_fn_t<5, 3>(var));
+template <int WIN>
+inline const void* shared_kernel_fn_w(int var, int cfg) {
+  switch (cfg) {
+    case 1: return shared_kernel_fn_t<WIN, 1>(var);
+    case 2: return shared_kernel_fn_t<WIN, 2>(var);
+    case 3: return shared_kernel_fn_t<WIN, 3>(var);
+    default: return shared_kernel_fn_t<WIN, 4>(var);
+  }
+}
+inline const void* shared_kernel_fn(int window, int var, int cfg) {
+  return window == 3 ? shared_kernel_fn_w<3>(var, cfg) : shared_kernel_fn_w<5>(var, cfg);
 }
 
-inline size_t shared_smem_bytes(int window, int ppt) {
-  if (window == 3) return ppt == 1 ? sizeof(SharedSmem<12, 1>) : (ppt == 2 ? sizeof(SharedSmem<12, 2>) : sizeof(SharedSmem<12, 3>));
-  return ppt == 1 ? sizeof(SharedSmem<10, 1>) : (ppt == 2 ? sizeof(SharedSmem<10, 2>) : sizeof(SharedSmem<10, 3>));
+template <int WIN>
+inline size_t shared_smem_bytes_w(int cfg) {
+  constexpr int GD = (WIN == 3) ? 12 : 10;
+  switch (cfg) {
+    case 1: return sizeof(SharedSmem<GD, 1>);
+    case 2: return sizeof(SharedSmem<GD, 2>);
+    case 3: return sizeof(SharedSmem<GD, 3>);
+    default: return sizeof(SharedSmem<GD, 4>);
+  }
+}
+inline size_t shared_smem_bytes(int window, int cfg) {
+  return window == 3 ? shared_smem_bytes_w<3>(cfg) : shared_smem_bytes_w<5>(cfg);
 }
 
 // Opt the kernels in to > 48 KB of dynamic shared memory (once per process).
 inline cudaError_t shared_set_attributes() {
   const int ws[2] = {3, 5};
   for (int w : ws)
-    for (int ppt = 1; ppt <= 3; ++ppt)
+    for (int cfg = 1; cfg <= 4; ++cfg)
       for (int v = 0; v < 2; ++v) {
-        cudaError_t e = cudaFuncSetAttribute(shared_kernel_fn(w, v, ppt), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)shared_smem_bytes(w, ppt));
+        cudaError_t e = cudaFuncSetAttribute(shared_kernel_fn(w, v, cfg), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)shared_smem_bytes(w, cfg));
         if (e != cudaSuccess) return e;
       }
   return cudaSuccess;
 }
 
-inline dim3 shared_grid(const Launch& L, int B, int window, int ppt) {
+inline dim3 shared_grid(const Launch& L, int B, int window, int cfg) {
   using namespace shared;
   const int R = window / 2;
-  const int TW = PW - 2 * R, TH = region_h(ppt) - 2 * R;
+  const int TW = PW - 2 * R, TH = region_h(cfg) - 2 * R;
   return dim3((L.W + TW - 1) / TW, (L.out_rows + TH - 1) / TH, B);
 }
 

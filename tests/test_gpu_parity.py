@@ -38,7 +38,7 @@ def full_parity(img_np, w, crit, var, algo=None):
     if algo:
         algos = [algo]
     elif crit == "angular":
-        algos = ["window", "shared:1", "shared:2", "shared:3"]
+        algos = ["window", "shared", "shared:1", "shared:2", "shared:3"]
         if w == 5:
             algos += ["role", "role:1", "role:2", "role:3"]
     else:
