@@ -191,14 +191,15 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
     static const int ppt_env = [] { const char* e = std::getenv("VF_SHARED_PPT"); return e ? std::atoi(e) : 0; }();
     int ppt = (ppt_env >= 1 && ppt_env <= 4) ? ppt_env : 4;
     if (tile) ppt = tile;
-    // 5x5: per-pixel role sums (vf_role.cuh) unless the per-window
-    // accumulation is asked for explicitly
-    if (window == 5 && algo != VF_ALGO_SHARED) {
-      const int cfg = tile ? tile : (ppt_env >= 1 && ppt_env <= 4 ? ppt_env : 4);   // 4: 384 threads x 2 px
-      kd->fn = vf::role_kernel_fn(var, cfg);
-      kd->grid = vf::role_grid(L, B, cfg);
-      kd->block = dim3(vf::role_threads(cfg));
-      kd->smem = vf::role_smem_bytes(cfg);
+    // per-pixel role sums (vf_role.cuh): the 5x5 default (C3 -33% vs the
+    // per-window accumulation); at 3x3 only on request (VF_ALGO_ROLE): there
+    // the 36-pair accumulation is cheaper than the extra barriers and row
+    // sums (C4 angular minimax 151 vs 133 us)
+    if (algo == VF_ALGO_ROLE || (window == 5 && algo != VF_ALGO_SHARED)) {
+      kd->fn = vf::role_kernel_fn(window, var, ppt);
+      kd->grid = vf::shared_grid(L, B, window, ppt);
+      kd->block = dim3(vf::shared::cfg_nt(ppt));
+      kd->smem = vf::role_smem_bytes(window, ppt);
       const cudaError_t e = ensure_attributes();
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
       return VF_OK;

@@ -36,26 +36,29 @@ namespace vf {
 
 namespace role {
 constexpr int PW = shared::PW;          // region width (32)
-constexpr int PRE = 5 * PW;             // map padding before the region: reverse reads reach 4 rows + 4 px back
+constexpr int PRE = 5 * PW;             // map padding before the region: reverse reads reach 2r rows + 2r px back
 constexpr int POST = 5 * PW;            // and after it
-__host__ __device__ constexpr int nslots(int g) { return g == 0 ? 4 : 9; }
-__host__ __device__ constexpr int slot_dx(int g, int s) { return g == 0 ? s + 1 : s - 4; }
+// group g = the offsets (g, dx): dx = 1..2r for g = 0, dx = -2r..2r for g = 1..2r
+__host__ __device__ constexpr int nslots(int r, int g) { return g == 0 ? 2 * r : 4 * r + 1; }
+__host__ __device__ constexpr int slot_dx(int r, int g, int s) { return g == 0 ? s + 1 : s - 2 * r; }
 }  // namespace role
 
 // Block of NT threads (256 or 384) over a 32 x (NT PPT / 32) region, PPT
-// region pixels per thread.
-template <int NT, int PPT>
+// region pixels per thread; window side WIN (3 or 5).
+template <int WIN, int NT, int PPT>
 struct RoleSmem {
+  static constexpr int N = WIN * WIN;
+  static constexpr int NSM = 2 * WIN - 1;   // maps of one group (4r + 1)
   static constexpr int NP = NT * PPT;
   static constexpr int MS = role::PRE + NP + role::POST;   // map stride (floats)
   static constexpr int QCAP = 64;
   struct Maps {
     uint4 px[NP + shared::PAD];   // (packed RGB0, |x|^2 bits, |x| bits, 0)
-    float M[9][MS];               // pair maps of one neighbourhood row g
+    float M[NSM][MS];             // pair maps of one neighbourhood row g
   };
   union U {
     Maps a;
-    float S[25][NP];              // role sums, after the last group
+    float S[N][NP];               // role sums, after the last group
   } u;
   uint32_t pk[NP];                // packed RGB of the region (output store)
   uint32_t queue[NT / 32][QCAP];
@@ -63,8 +66,8 @@ struct RoleSmem {
 
 // Exact re-decision of a flagged pair (p, p + (g, dx)) of slot s: as
 // angular_fix in vf_shared.cuh, on this kernel's map layout.
-template <int VAR, int NT, int PPT>
-__device__ __forceinline__ void role_fix(RoleSmem<NT, PPT>& sm, int p, int s, int off) {
+template <int VAR, int WIN, int NT, int PPT>
+__device__ __forceinline__ void role_fix(RoleSmem<WIN, NT, PPT>& sm, int p, int s, int off) {
   const uint4 pv = sm.u.a.px[p], qv = sm.u.a.px[p + off];
   const float D = __uint_as_float(__dp4a(pv.x, qv.x, F2P23_BITS)) - F2P23;   // exact dot
   const float nna = __uint_as_float(pv.y), nnb = __uint_as_float(qv.y);
@@ -77,8 +80,15 @@ __device__ __forceinline__ void role_fix(RoleSmem<NT, PPT>& sm, int p, int s, in
   }
 }
 
+// H_b = sum_{dx=-b}^{2-b} v[2 + dx], b = 0..2, without subtractions.
+__device__ __forceinline__ void row_sums(const float (&v)[5], float (&H)[3]) {
+  const float e = v[2] + v[3];
+  H[0] = e + v[4];
+  H[1] = e + v[1];
+  H[2] = (v[0] + v[1]) + v[2];
+}
 // H_b = sum_{dx=-b}^{4-b} v[4 + dx], b = 0..4, without subtractions.
-__device__ __forceinline__ void row_sums5(const float (&v)[9], float (&H)[5]) {
+__device__ __forceinline__ void row_sums(const float (&v)[9], float (&H)[5]) {
   const float e = v[4] + v[5];
   const float c = e + v[6];
   H[0] = c + (v[7] + v[8]);
@@ -89,13 +99,15 @@ __device__ __forceinline__ void row_sums5(const float (&v)[9], float (&H)[5]) {
   H[4] = (v[0] + a12) + (v[3] + v[4]);
 }
 
-template <int VAR, int NT, int PPT, int G>
-__device__ __forceinline__ void role_group(RoleSmem<NT, PPT>& sm, const uint32_t (&my_pk)[PPT], const float (&my_nn)[PPT],
-                                           const float (&my_nrm)[PPT], float (&Rs)[PPT][25], int tid, bool blk_zero) {
+template <int WIN, int VAR, int NT, int PPT, int G>
+__device__ __forceinline__ void role_group(RoleSmem<WIN, NT, PPT>& sm, const uint32_t (&my_pk)[PPT],
+                                           const float (&my_nn)[PPT], const float (&my_nrm)[PPT],
+                                           float (&Rs)[PPT][WIN * WIN], int tid, bool blk_zero) {
   using namespace role;
-  constexpr int NS = nslots(G);
-  constexpr int QCAP = RoleSmem<NT, PPT>::QCAP;
-  constexpr int NPL = RoleSmem<NT, PPT>::NP;
+  constexpr int R = WIN / 2;
+  constexpr int NS = nslots(R, G);
+  constexpr int QCAP = RoleSmem<WIN, NT, PPT>::QCAP;
+  constexpr int NPL = RoleSmem<WIN, NT, PPT>::NP;
   const int lane = tid & 31, warp = tid >> 5;
   if (G > 0) __syncthreads();   // previous phase B done with the maps (G = 0: the staging barrier)
   // ---- phase A: maps of the offsets (G, dx) ----------------------------------------
@@ -104,7 +116,7 @@ __device__ __forceinline__ void role_group(RoleSmem<NT, PPT>& sm, const uint32_t
   for (int k = 0; k < PPT; ++k) flags[k] = 0u;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
-    const int off = G * PW + slot_dx(G, s);
+    const int off = G * PW + slot_dx(R, G, s);
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       const int p = tid + NT * k;
@@ -151,14 +163,14 @@ __device__ __forceinline__ void role_group(RoleSmem<NT, PPT>& sm, const uint32_t
       for (int e = lane; e < nq; e += 32) {
         const uint32_t en = q[e];
         const int s = (int)(en >> 16);
-        role_fix<VAR>(sm, (int)(en & 0xffffu), s, G * PW + slot_dx(G, s));
+        role_fix<VAR>(sm, (int)(en & 0xffffu), s, G * PW + slot_dx(R, G, s));
       }
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         while (flags[k]) {
           const int s = __ffs(flags[k]) - 1;
           flags[k] &= flags[k] - 1;
-          role_fix<VAR>(sm, tid + NT * k, s, G * PW + slot_dx(G, s));
+          role_fix<VAR>(sm, tid + NT * k, s, G * PW + slot_dx(R, G, s));
         }
       }
       __syncwarp();
@@ -173,7 +185,7 @@ __device__ __forceinline__ void role_group(RoleSmem<NT, PPT>& sm, const uint32_t
         const int p = tid + NT * k;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-          const int off = G * PW + slot_dx(G, s);
+          const int off = G * PW + slot_dx(R, G, s);
           sm.u.a.M[s][PRE + p] = 0.0f;
           if (p - off >= 0) sm.u.a.M[s][PRE + p - off] = 0.0f;
         }
@@ -185,57 +197,63 @@ __device__ __forceinline__ void role_group(RoleSmem<NT, PPT>& sm, const uint32_t
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     const int q = PRE + tid + NT * k;
-    float vf[9], H[5];
+    constexpr int D2 = 2 * R;                 // 2r: neighbourhood half-width
+    float vf[2 * D2 + 1], H[WIN];
     if (G == 0) {   // row 0: (0, dx) for dx > 0 from the maps, dx < 0 from the neighbour's map
 #pragma unroll
-      for (int dx = 1; dx <= 4; ++dx) {
-        vf[4 + dx] = sm.u.a.M[dx - 1][q];
-        vf[4 - dx] = sm.u.a.M[dx - 1][q - dx];
+      for (int dx = 1; dx <= D2; ++dx) {
+        vf[D2 + dx] = sm.u.a.M[dx - 1][q];
+        vf[D2 - dx] = sm.u.a.M[dx - 1][q - dx];
       }
-      vf[4] = -0.0f;   // the sample itself (-0 + x == x: folds away)
+      vf[D2] = -0.0f;   // the sample itself (-0 + x == x: folds away)
     } else {
 #pragma unroll
-      for (int dx = -4; dx <= 4; ++dx) vf[4 + dx] = sm.u.a.M[dx + 4][q];
+      for (int dx = -D2; dx <= D2; ++dx) vf[D2 + dx] = sm.u.a.M[dx + D2][q];
     }
-    row_sums5(vf, H);
+    row_sums(vf, H);
 #pragma unroll
-    for (int b = 0; b < 5; ++b)
+    for (int b = 0; b < WIN; ++b)
 #pragma unroll
-      for (int a = 0; a < 5; ++a)
-        if (-a <= G && G <= 4 - a) Rs[k][a * 5 + b] += H[b];
+      for (int a = 0; a < WIN; ++a)
+        if (-a <= G && G <= D2 - a) Rs[k][a * WIN + b] += H[b];
     if (G > 0) {    // row -G: A(q, q + (-G, dx)) = map of offset (G, -dx) at q + (-G, dx)
-      float vr[9];
+      float vr[2 * D2 + 1];
 #pragma unroll
-      for (int dx = -4; dx <= 4; ++dx) vr[4 + dx] = sm.u.a.M[4 - dx][q - G * PW + dx];
-      row_sums5(vr, H);
+      for (int dx = -D2; dx <= D2; ++dx) vr[D2 + dx] = sm.u.a.M[D2 - dx][q - G * PW + dx];
+      row_sums(vr, H);
 #pragma unroll
-      for (int b = 0; b < 5; ++b)
+      for (int b = 0; b < WIN; ++b)
 #pragma unroll
-        for (int a = 0; a < 5; ++a)
-          if (-a <= -G && -G <= 4 - a) Rs[k][a * 5 + b] += H[b];
+        for (int a = 0; a < WIN; ++a)
+          if (-a <= -G && -G <= D2 - a) Rs[k][a * WIN + b] += H[b];
     }
   }
 }
 
-template <int VAR, int NT, int PPT, int... Gs>
-__device__ __forceinline__ void role_groups(std::integer_sequence<int, Gs...>, RoleSmem<NT, PPT>& sm,
+template <int WIN, int VAR, int NT, int PPT, int... Gs>
+__device__ __forceinline__ void role_groups(std::integer_sequence<int, Gs...>, RoleSmem<WIN, NT, PPT>& sm,
                                             const uint32_t (&my_pk)[PPT], const float (&my_nn)[PPT],
-                                            const float (&my_nrm)[PPT], float (&Rs)[PPT][25], int tid, bool blk_zero) {
-  (role_group<VAR, NT, PPT, Gs>(sm, my_pk, my_nn, my_nrm, Rs, tid, blk_zero), ...);
+                                            const float (&my_nrm)[PPT], float (&Rs)[PPT][WIN * WIN], int tid,
+                                            bool blk_zero) {
+  (role_group<WIN, VAR, NT, PPT, Gs>(sm, my_pk, my_nn, my_nrm, Rs, tid, blk_zero), ...);
 }
 
-template <int VAR, int NT, int PPT>
-__global__ void __launch_bounds__(NT, 2) vf_angular_role_kernel(const Launch L) {
+// Resident blocks per SM the register allocation is held to: 5x5: 2 (<= 80
+// registers at 384 threads); 3x3 (384 threads): 4 (<= 40).
+__host__ __device__ constexpr int role_min_blocks(int win, int nt) { return win == 5 ? 2 : (nt == 384 ? 4 : 4); }
+
+template <int WIN, int VAR, int NT, int PPT>
+__global__ void __launch_bounds__(NT, role_min_blocks(WIN, NT)) vf_angular_role_kernel(const Launch L) {
   using namespace role;
-  constexpr int WIN = 5, R = 2, N = 25;
+  constexpr int R = WIN / 2, N = WIN * WIN;
   constexpr int NW = NT / 32;               // warps = region rows per pixel slab
-  constexpr int NP = RoleSmem<NT, PPT>::NP;
+  constexpr int NP = RoleSmem<WIN, NT, PPT>::NP;
   constexpr int PH = NP / PW;               // region height
-  constexpr int TW = PW - 2 * R;            // output tile width (28)
+  constexpr int TW = PW - 2 * R;            // output tile width (30 / 28)
   constexpr int TH = PH - 2 * R;            // output tile height
   constexpr int OPT = (TH + NW - 1) / NW;   // outputs per thread (rows ty, ty + NW, ...)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  RoleSmem<NT, PPT>& sm = *reinterpret_cast<RoleSmem<NT, PPT>*>(smem_raw);
+  RoleSmem<WIN, NT, PPT>& sm = *reinterpret_cast<RoleSmem<WIN, NT, PPT>*>(smem_raw);
 
   const int b = blockIdx.z;
   const int ox0 = blockIdx.x * TW;
@@ -266,19 +284,20 @@ __global__ void __launch_bounds__(NT, 2) vf_angular_role_kernel(const Launch L) 
   if (tid < shared::PAD) sm.u.a.px[NP + tid] = make_uint4(0u, 0u, 0u, 0u);
   const bool blk_zero = __syncthreads_or(has_zero) != 0;
 
-  float Rs[PPT][25];
+  float Rs[PPT][N];
 #pragma unroll
   for (int k = 0; k < PPT; ++k)
 #pragma unroll
-    for (int i = 0; i < 25; ++i) Rs[k][i] = -0.0f;   // -0 + v == v: the first add folds away
-  role_groups<VAR, NT, PPT>(std::make_integer_sequence<int, 5>{}, sm, my_pk, my_nn, my_nrm, Rs, tid, blk_zero);
+    for (int i = 0; i < N; ++i) Rs[k][i] = -0.0f;   // -0 + v == v: the first add folds away
+  role_groups<WIN, VAR, NT, PPT>(std::make_integer_sequence<int, 2 * R + 1>{}, sm, my_pk, my_nn, my_nrm, Rs, tid,
+                                 blk_zero);
 
   // ---- role sums replace the maps ------------------------------------------------------
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < PPT; ++k)
 #pragma unroll
-    for (int i = 0; i < 25; ++i) sm.u.S[i][tid + NT * k] = Rs[k][i];
+    for (int i = 0; i < N; ++i) sm.u.S[i][tid + NT * k] = Rs[k][i];
   __syncthreads();
 
   // ---- outputs: 25 aggregates per window, argmin, store ---------------------------------
@@ -304,45 +323,50 @@ __global__ void __launch_bounds__(NT, 2) vf_angular_role_kernel(const Launch L) 
   }
 }
 
-// Launch configurations: cfg 1..3 = 256 threads with 1..3 pixels each; cfg 4
-// (default) = 384 threads with 2 pixels each: the same 32 x 24 region as cfg 3
-// (halo overhead 1.37) with 50 instead of 75 role accumulators per thread,
-// so two blocks of 12 warps fit per SM instead of two of 8.
-template <int NT, int PPT>
+// Launch configurations (as shared::cfg_nt / cfg_ppt): cfg 1..3 = 256
+// threads with 1..3 pixels each; cfg 4 (default) = 384 threads with 2 pixels
+// each: the same 32 x 24 region as cfg 3 with two thirds of the role
+// accumulators per thread, so more warps fit per SM (5x5: 24 instead of 16).
+template <int WIN, int CFG>
 inline const void* role_kernel_fn_t(int var) {
-  return var == EXACT ? (const void*)vf_angular_role_kernel<EXACT, NT, PPT>
-                      : (const void*)vf_angular_role_kernel<MINIMAX, NT, PPT>;
+  constexpr int NT = shared::cfg_nt(CFG), PPT = shared::cfg_ppt(CFG);
+  return var == EXACT ? (const void*)vf_angular_role_kernel<WIN, EXACT, NT, PPT>
+                      : (const void*)vf_angular_role_kernel<WIN, MINIMAX, NT, PPT>;
 }
-inline const void* role_kernel_fn(int var, int cfg) {
+template <int WIN>
+inline const void* role_kernel_fn_w(int var, int cfg) {
   switch (cfg) {
-    case 1: return role_kernel_fn_t<256, 1>(var);
-    case 2: return role_kernel_fn_t<256, 2>(var);
-    case 3: return role_kernel_fn_t<256, 3>(var);
-    default: return role_kernel_fn_t<384, 2>(var);
+    case 1: return role_kernel_fn_t<WIN, 1>(var);
+    case 2: return role_kernel_fn_t<WIN, 2>(var);
+    case 3: return role_kernel_fn_t<WIN, 3>(var);
+    default: return role_kernel_fn_t<WIN, 4>(var);
   }
 }
-inline int role_threads(int cfg) { return (cfg >= 1 && cfg <= 3) ? 256 : 384; }
-inline int role_region_h(int cfg) { return (cfg >= 1 && cfg <= 3) ? 8 * cfg : 24; }
-inline size_t role_smem_bytes(int cfg) {
+inline const void* role_kernel_fn(int window, int var, int cfg) {
+  return window == 3 ? role_kernel_fn_w<3>(var, cfg) : role_kernel_fn_w<5>(var, cfg);
+}
+template <int WIN>
+inline size_t role_smem_bytes_w(int cfg) {
   switch (cfg) {
-    case 1: return sizeof(RoleSmem<256, 1>);
-    case 2: return sizeof(RoleSmem<256, 2>);
-    case 3: return sizeof(RoleSmem<256, 3>);
-    default: return sizeof(RoleSmem<384, 2>);
+    case 1: return sizeof(RoleSmem<WIN, 256, 1>);
+    case 2: return sizeof(RoleSmem<WIN, 256, 2>);
+    case 3: return sizeof(RoleSmem<WIN, 256, 3>);
+    default: return sizeof(RoleSmem<WIN, 384, 2>);
   }
+}
+inline size_t role_smem_bytes(int window, int cfg) {
+  return window == 3 ? role_smem_bytes_w<3>(cfg) : role_smem_bytes_w<5>(cfg);
 }
 inline cudaError_t role_set_attributes() {
-  for (int cfg = 1; cfg <= 4; ++cfg)
-    for (int v = 0; v < 2; ++v) {
-      cudaError_t e = cudaFuncSetAttribute(role_kernel_fn(v, cfg), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)role_smem_bytes(cfg));
-      if (e != cudaSuccess) return e;
-    }
+  const int ws[2] = {3, 5};
+  for (int w : ws)
+    for (int cfg = 1; cfg <= 4; ++cfg)
+      for (int v = 0; v < 2; ++v) {
+        cudaError_t e = cudaFuncSetAttribute(role_kernel_fn(w, v, cfg), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)role_smem_bytes(w, cfg));
+        if (e != cudaSuccess) return e;
+      }
   return cudaSuccess;
-}
-inline dim3 role_grid(const Launch& L, int B, int cfg) {
-  const int TW = shared::PW - 4, TH = role_region_h(cfg) - 4;
-  return dim3((L.W + TW - 1) / TW, (L.out_rows + TH - 1) / TH, B);
 }
 
 }  // namespace vf

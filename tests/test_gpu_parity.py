@@ -38,9 +38,7 @@ def full_parity(img_np, w, crit, var, algo=None):
     if algo:
         algos = [algo]
     elif crit == "angular":
-        algos = ["window", "shared", "shared:1", "shared:2", "shared:3"]
-        if w == 5:
-            algos += ["role", "role:1", "role:2", "role:3"]
+        algos = ["window", "shared", "shared:1", "shared:2", "shared:3", "role", "role:1", "role:2", "role:3"]
     else:
         # tile bits force the TMA-staged kernel where the rows allow it (3W % 16 == 0);
         # "+notma" the plain-load one
