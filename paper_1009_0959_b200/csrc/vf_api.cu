@@ -93,12 +93,21 @@ int persistent_blocks(const void* fn, int threads, size_t smem) {
 }
 
 // One-time per-process kernel attribute setup (thread-safe).
+// Kernel attributes (> 48 KB dynamic shared memory) are per device: set once
+// for each device the process launches on (thread-safe).
 cudaError_t ensure_attributes() {
-  static cudaError_t status = [] {
-    cudaError_t e = vf::shared_set_attributes();
-    return e != cudaSuccess ? e : vf::role_set_attributes();
-  }();
-  return status;
+  static std::mutex mu;
+  static std::vector<int> done;   // devices already set up
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  for (int d : done)
+    if (d == dev) return cudaSuccess;
+  e = vf::shared_set_attributes();
+  if (e == cudaSuccess) e = vf::role_set_attributes();
+  if (e == cudaSuccess) done.push_back(dev);
+  return e;
 }
 
 template <int WIN, int OPT>
