@@ -114,6 +114,19 @@ def ncu_full(tag, cfg, npix, summary):
                 else:
                     vals.append(v[:6])
             fh.write(f"| {label} | " + " | ".join(vals) + " |\n")
+        # executed FP32 flops (ncu): 2 FFMA + FMUL + FADD thread instructions
+        # (predicated on) per elapsed cycle, over the FP32 peak 2 x 128 x SMs
+        ex = [("smsp__sass_thread_inst_executed_op_ffma_pred_on.sum.per_cycle_elapsed", 2),
+              ("smsp__sass_thread_inst_executed_op_fmul_pred_on.sum.per_cycle_elapsed", 1),
+              ("smsp__sass_thread_inst_executed_op_fadd_pred_on.sum.per_cycle_elapsed", 1)]
+        if all(m in col for m, _ in ex):
+            vals = []
+            for r in data:
+                fl = sum(w * float(r[col[m]].replace(",", "")) for m, w in ex)
+                vals.append(f"{100 * fl / (2 * 128 * 148):.1f}%")
+                summary.setdefault("executed_fp32_frac", {})[f"{cfg}/{kernel_key(r[col['Kernel Name']])[0]}"] = \
+                    fl / (2 * 128 * 148)
+            fh.write("| executed FP32 flops (2 FFMA + FMUL + FADD) % of peak | " + " | ".join(vals) + " |\n")
         fh.write("\nKernel names: " + "; ".join(f"`{n[:80]}`" for n in names) + "\n")
     for r in data:
         key, w = kernel_key(r[col["Kernel Name"]])
