@@ -198,4 +198,71 @@ __device__ __forceinline__ void crit_accumulate(float zu, float& Ri, float& Rj) 
   }
 }
 
+// ---- packed FP32 pairs (sm_100: FFMA2 / FADD2 / FMUL2) ---------------------------
+// fma.rn.f32x2 computes two independent fp32 FMAs, each rounded exactly like
+// fmaf, in one instruction: same FMA-pipe throughput per element as FFMA
+// (tools/fp32_peak.cu: 17-18 T FFMA2/s = 34-36 T FMA/s) at half the issue
+// slots.  Two pairs of a window are evaluated together so that the Horner
+// chains and the argument scaling issue once for both; results are
+// bit-identical to the scalar path.
+using f32x2 = unsigned long long;
+__device__ __forceinline__ f32x2 pack2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack2(f32x2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 horner4x2(const coef::P4f p, f32x2 x) {
+  f32x2 r = fma2(pack2(p.a4, p.a4), x, pack2(p.a3, p.a3));
+  r = fma2(r, x, pack2(p.a2, p.a2));
+  r = fma2(r, x, pack2(p.a1, p.a1));
+  return fma2(r, x, pack2(p.a0, p.a0));
+}
+template <typename T, int K>
+__device__ __forceinline__ f32x2 horner_rec2(f32x2 x) {
+  constexpr float a = (float)T::c(K);
+  if constexpr (K == T::DEG) return pack2(a, a);
+  else return fma2(horner_rec2<T, K + 1>(x), x, pack2(a, a));
+}
+
+// Two pairs at once: zu2 = (z or u of pair 0, of pair 1); accumulates into
+// (Ri0, Rj0) and (Ri1, Rj1) with the roundings of crit_accumulate.
+template <int CRIT, int VAR>
+__device__ __forceinline__ void crit_accumulate2(f32x2 zu2, float& Ri0, float& Rj0, float& Ri1, float& Rj1) {
+  if (VAR == MINIMAX) {
+    float n0, n1, q0, q1;
+    unpack2(CRIT == EXPC ? horner4x2(coef::EXP_DELTA(), zu2) : horner4x2(coef::ENT_NEGN_U(), zu2), n0, n1);
+    unpack2(CRIT == EXPC ? horner4x2(coef::EXP_Q(), zu2) : horner4x2(coef::ENT_Q_U(), zu2), q0, q1);
+    const float r0 = rcp_approx(q0), r1 = rcp_approx(q1);
+    Ri0 = fmaf(n0, r0, Ri0);
+    Rj0 = fmaf(n0, r0, Rj0);
+    Ri1 = fmaf(n1, r1, Ri1);
+    Rj1 = fmaf(n1, r1, Rj1);
+  } else if (VAR == REACH || VAR == POLY4) {
+    float v0, v1;
+    if (VAR == POLY4)
+      unpack2(horner4x2(coef::EXP_1MP4(), zu2), v0, v1);
+    else if (CRIT == EXPC)
+      unpack2(horner_rec2<coef::R_EXP, 0>(zu2), v0, v1);
+    else
+      unpack2(horner_rec2<coef::R_LOG, 0>(zu2), v0, v1);
+    Ri0 = __fadd_rn(Ri0, v0);
+    Rj0 = __fadd_rn(Rj0, v0);
+    Ri1 = __fadd_rn(Ri1, v1);
+    Rj1 = __fadd_rn(Rj1, v1);
+  } else {   // libm variants: scalar
+    float z0, z1;
+    unpack2(zu2, z0, z1);
+    crit_accumulate<CRIT, VAR>(z0, Ri0, Rj0);
+    crit_accumulate<CRIT, VAR>(z1, Ri1, Rj1);
+  }
+}
+
 }  // namespace vf

@@ -196,12 +196,25 @@ __device__ __forceinline__ void el_window_s1(const Launch& L, int b, int ox, int
   float Ra[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) Ra[k] = -0.0f;   // -0 + v == v: the first add folds away
-  static_for<N * (N - 1) / 2>([&](auto pc) {
-    constexpr int i = pair_i<N>(decltype(pc)::value), j = pair_j<N>(decltype(pc)::value);
-    const float fb = __uint_as_float(sad4(w[i], w[j], F2P23_BITS));   // 2^23 + d1
-    const float zu = fmaf(sc, fb, bias);                               // c * d1, one rounding
-    crit_accumulate<CRIT, VAR>(zu, Ra[i], Ra[j]);
-  });
+  if constexpr (VAR == EXACT) {
+    static_for<N * (N - 1) / 2>([&](auto pc) {
+      constexpr int i = pair_i<N>(decltype(pc)::value), j = pair_j<N>(decltype(pc)::value);
+      const float fb = __uint_as_float(sad4(w[i], w[j], F2P23_BITS));   // 2^23 + d1
+      const float zu = fmaf(sc, fb, bias);                               // c * d1, one rounding
+      crit_accumulate<CRIT, VAR>(zu, Ra[i], Ra[j]);
+    });
+  } else {
+    // polynomial variants: pairs 2q and 2q + 1 together in packed FP32
+    // (FFMA2), one Horner chain issue for both (n(n-1)/2 is even for n = 9, 25)
+    const f32x2 sc2 = pack2(sc, sc), bias2 = pack2(bias, bias);
+    static_for<N * (N - 1) / 4>([&](auto qc) {
+      constexpr int p0 = 2 * decltype(qc)::value, p1 = p0 + 1;
+      constexpr int i0 = pair_i<N>(p0), j0 = pair_j<N>(p0), i1 = pair_i<N>(p1), j1 = pair_j<N>(p1);
+      const f32x2 fb2 = pack2(__uint_as_float(sad4(w[i0], w[j0], F2P23_BITS)),
+                              __uint_as_float(sad4(w[i1], w[j1], F2P23_BITS)));   // 2^23 + d1, two pairs
+      crit_accumulate2<CRIT, VAR>(fma2(sc2, fb2, bias2), Ra[i0], Ra[j0], Ra[i1], Ra[j1]);
+    });
+  }
   float bv = Ra[0];
   uint32_t o = w[0];
 #pragma unroll

@@ -53,6 +53,36 @@ KERNEL(k_ffma4_rsq, asm volatile("fma.rn.f32 %0, %0, %1, 0f3F000000;" : "+f"(a[k
        asm volatile("fma.rn.f32 %0, %0, %1, 0f3F000000;" : "+f"(a[k]) : "f"(bb[k]));
        asm volatile("rsqrt.approx.ftz.f32 %0, %0;" : "+f"(cc[k])))
 
+// packed FP32 pairs (sm_100: fma/add/mul.rn.f32x2 -> FFMA2 / FADD2 / FMUL2)
+#define K2KERNEL(NAME, BODY)                                                 \
+  __global__ void NAME(float* out, float b, float c) {                      \
+    unsigned long long a[ACC], bb[ACC], cc[ACC];                             \
+    _Pragma("unroll") for (int k = 0; k < ACC; ++k) {                        \
+      float2 x = make_float2(threadIdx.x * 1e-3f + k, k);                    \
+      float2 y = make_float2(b + k * 1e-3f, b);                              \
+      float2 z = make_float2(c + k, c);                                      \
+      a[k] = *(unsigned long long*)&x; bb[k] = *(unsigned long long*)&y;     \
+      cc[k] = *(unsigned long long*)&z;                                      \
+    }                                                                        \
+    for (int i = 0; i < ITERS; ++i) {                                        \
+      _Pragma("unroll") for (int k = 0; k < ACC; ++k) { BODY; }              \
+    }                                                                        \
+    float s = 0;                                                             \
+    _Pragma("unroll") for (int k = 0; k < ACC; ++k) {                        \
+      float2 x = *(float2*)&a[k]; s += x.x + x.y; }                          \
+    if (s == 12345.f) out[threadIdx.x] = s;                                  \
+  }
+K2KERNEL(k_ffma2, asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[k]) : "l"(bb[k]), "l"(cc[k])))
+// Horner-like: a = a * x + c with x, c shared by all chains (register reuse)
+K2KERNEL(k_ffma2_shared, asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[k]) : "l"(bb[0]), "l"(cc[0])))
+// a = a * a + c_shared
+K2KERNEL(k_ffma2_sq, asm volatile("fma.rn.f32x2 %0, %0, %0, %1;" : "+l"(a[k]) : "l"(cc[0])))
+K2KERNEL(k_fadd2, asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(a[k]) : "l"(bb[k])))
+K2KERNEL(k_fmul2, asm volatile("mul.rn.f32x2 %0, %0, %1;" : "+l"(a[k]) : "l"(bb[k])))
+// 1 FFMA2 + 1 FFMA interleaved
+K2KERNEL(k_ffma2_ffma, asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[k]) : "l"(bb[k]), "l"(cc[k]));
+         asm volatile("{.reg .f32 lo, hi; mov.b64 {lo, hi}, %0; fma.rn.f32 lo, lo, lo, 0f3F000000; mov.b64 %0, {lo, hi};}" : "+l"(cc[k])))
+
 // integer kernels on packed bytes
 #define IKERNEL(NAME, BODY)                                                  \
   __global__ void NAME(float* out, float b, float c) {                      \
@@ -110,11 +140,17 @@ int main() {
   RUN(k_ffma_fadd, "ffma_plus_fadd_Tinst_per_s", 2)
   RUN(k_ffma_fmax, "ffma_plus_fmnmx_Tinst_per_s", 2)
   RUN(k_ffma4_rsq, "4ffma_plus_rsq_Tinst_per_s", 5)
+  RUN(k_ffma2, "ffma2_Tinst_per_s", 1)
+  RUN(k_ffma2_shared, "ffma2_shared_xc_Tinst_per_s", 1)
+  RUN(k_ffma2_sq, "ffma2_sq_Tinst_per_s", 1)
+  RUN(k_fadd2, "fadd2_Tinst_per_s", 1)
+  RUN(k_fmul2, "fmul2_Tinst_per_s", 1)
+  RUN(k_ffma2_ffma, "ffma2_plus_ffma_Tinst_per_s", 2)
   RUN(k_vabsdiff4, "vabsdiff4_Tinst_per_s", 1)
   RUN(k_dp4a, "idp4a_Tinst_per_s", 1)
   RUN(k_iadd, "iadd_Tinst_per_s", 1)
   int clk;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-  printf(", \"clock_khz_attr\": %d, \"note\": \"thread-instructions per second; FFMA flops = 2x\"}\n", clk);
+  printf(", \"clock_khz_attr\": %d, \"note\": \"thread-instructions per second; FFMA flops = 2x, FFMA2 flops = 4x\"}\n", clk);
   return 0;
 }
