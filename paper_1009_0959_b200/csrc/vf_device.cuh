@@ -219,6 +219,16 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
 }
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 __device__ __forceinline__ f32x2 horner4x2(const coef::P4f p, f32x2 x) {
   f32x2 r = fma2(pack2(p.a4, p.a4), x, pack2(p.a3, p.a3));
   r = fma2(r, x, pack2(p.a2, p.a2));
@@ -230,6 +240,36 @@ __device__ __forceinline__ f32x2 horner_rec2(f32x2 x) {
   constexpr float a = (float)T::c(K);
   if constexpr (K == T::DEG) return pack2(a, a);
   else return fma2(horner_rec2<T, K + 1>(x), x, pack2(a, a));
+}
+
+// Two angular pair evaluations on the tau branch (Eqs. 6-7) in packed FP32:
+// pixel p (packed RGB pk, nn2 = (|p|^2, |p|^2), nnn2 = -nn2, nrm2 = (|p|, |p|))
+// against the neighbour records q0, q1 (packed RGB, |q|^2 bits, |q| bits).
+// Every element is computed with exactly the roundings of the scalar path
+// (angular_geo / vf_shared.cuh phase A): D exact; -Pl = fl(Ph - nn nnq) is the
+// negated exact residual, so X = fl(fl(Ph - D^2) + Pl); tau = X rsqrt(X w).
+template <int VAR>
+__device__ __forceinline__ void angular_tau2(uint32_t pk, f32x2 nn2, f32x2 nnn2, f32x2 nrm2, uint4 q0, uint4 q1,
+                                             float& tau0, float& tau1, float& v0, float& v1) {
+  const f32x2 C = pack2(F2P23, F2P23);
+  const f32x2 Db = pack2(__uint_as_float(__dp4a(pk, q0.x, F2P23_BITS)), __uint_as_float(__dp4a(pk, q1.x, F2P23_BITS)));
+  const f32x2 D = sub2(Db, C);                            // exact dot products
+  const f32x2 nD = sub2(C, Db);                           // -D, exact
+  const f32x2 nnq = pack2(__uint_as_float(q0.y), __uint_as_float(q1.y));
+  const f32x2 Ph = mul2(nn2, nnq);
+  const f32x2 nPl = fma2(nnn2, nnq, Ph);                  // -(exact residual of nn nnq)
+  const f32x2 X = sub2(fma2(nD, D, Ph), nPl);             // |p x q|^2
+  const f32x2 w = fma2(mul2(nrm2, pack2(__uint_as_float(q0.z), __uint_as_float(q1.z))), D, Ph);   // s (s + D)
+  float xw0, xw1;
+  unpack2(fma2(X, w, pack2(1e-30f, 1e-30f)), xw0, xw1);
+  const f32x2 t = mul2(X, pack2(rsqrt_approx(xw0), rsqrt_approx(xw1)));   // sqrt(1 - cos)
+  unpack2(t, tau0, tau1);
+  if (VAR == EXACT) {
+    v0 = 2.0f * asinf(tau0 * 0.70710678118654752f);
+    v1 = 2.0f * asinf(tau1 * 0.70710678118654752f);
+  } else {
+    unpack2(horner4x2(coef::ASIN(), t), v0, v1);
+  }
 }
 
 // Two pairs at once: zu2 = (z or u of pair 0, of pair 1); accumulates into

@@ -114,12 +114,26 @@ __device__ __forceinline__ void role_group(RoleSmem<WIN, NT, PPT>& sm, const uin
   uint32_t flags[PPT];
 #pragma unroll
   for (int k = 0; k < PPT; ++k) flags[k] = 0u;
+  // slots in pairs in packed FP32 (FFMA2 / FADD2 / FMUL2), an odd last slot scalar
 #pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    const int off = G * PW + slot_dx(R, G, s);
+  for (int k = 0; k < PPT; ++k) {
+    const int p = tid + NT * k;
+    const f32x2 nn2 = pack2(my_nn[k], my_nn[k]), nnn2 = pack2(-my_nn[k], -my_nn[k]);
+    const f32x2 nrm2 = pack2(my_nrm[k], my_nrm[k]);
 #pragma unroll
-    for (int k = 0; k < PPT; ++k) {
-      const int p = tid + NT * k;
+    for (int s = 0; s + 1 < NS; s += 2) {
+      const int q0 = p + G * PW + slot_dx(R, G, s), q1 = p + G * PW + slot_dx(R, G, s + 1);
+      VF_CHECK(q0 >= 0 && q0 < NPL + shared::PAD && q1 >= 0 && q1 < NPL + shared::PAD);
+      float tau0, tau1, v0, v1;
+      angular_tau2<VAR>(my_pk[k], nn2, nnn2, nrm2, sm.u.a.px[q0], sm.u.a.px[q1], tau0, tau1, v0, v1);
+      sm.u.a.M[s][PRE + p] = v0;
+      sm.u.a.M[s + 1][PRE + p] = v1;
+      if (tau0 > 0.70641626f) flags[k] |= 1u << s;          // possible cos < 0.5 (see vf_shared.cuh)
+      if (tau1 > 0.70641626f) flags[k] |= 1u << (s + 1);
+    }
+    if (NS % 2) {
+      constexpr int s = NS - 1;
+      const int off = G * PW + slot_dx(R, G, s);
       VF_CHECK(p + off >= 0 && p + off < NPL + shared::PAD);
       const uint4 qv = sm.u.a.px[p + off];
       const float D = __uint_as_float(__dp4a(my_pk[k], qv.x, F2P23_BITS)) - F2P23;   // exact dot
@@ -131,7 +145,7 @@ __device__ __forceinline__ void role_group(RoleSmem<WIN, NT, PPT>& sm, const uin
       const float tau = __fmul_rn(X, rsqrt_approx(fmaf(X, w, 1e-30f)));          // sqrt(1 - cos)
       const float v = (VAR == EXACT) ? 2.0f * asinf(tau * 0.70710678118654752f) : horner4(coef::ASIN(), tau);
       sm.u.a.M[s][PRE + p] = v;
-      if (tau > 0.70641626f) flags[k] |= 1u << s;            // possible cos < 0.5 (see vf_shared.cuh)
+      if (tau > 0.70641626f) flags[k] |= 1u << s;
     }
   }
   // ---- flagged pairs, warp-cooperative (as in vf_shared.cuh) --------------------------

@@ -114,35 +114,27 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint
   uint32_t flags[PPT];                                      // bit dl: pair (p_k, p_k + delta) flagged
 #pragma unroll
   for (int k = 0; k < PPT; ++k) flags[k] = 0u;
+  // two offsets per step in packed FP32 (FFMA2 / FADD2 / FMUL2, GD is even)
 #pragma unroll
-  for (int dl = 0; dl < GD; ++dl) {
-    const int d = G * GD + dl;
-    const int off = delta_dy(R, d) * PW + delta_dx(R, d);
+  for (int k = 0; k < PPT; ++k) {
+    const int p = tid + NT * k;
+    const f32x2 nn2 = pack2(my_nn[k], my_nn[k]), nnn2 = pack2(-my_nn[k], -my_nn[k]);
+    const f32x2 nrm2 = pack2(my_nrm[k], my_nrm[k]);
 #pragma unroll
-    for (int k = 0; k < PPT; ++k) {
-      const int p = tid + NT * k;
-      const int q = p + off;                                  // in bounds (PAD); garbage if outside P
-      VF_CHECK(q >= 0 && q < region_np(CFG) + PAD);
-      const uint4 qv = sm.px[q];
-      const uint32_t qk = qv.x;
-      const float2 qn = make_float2(__uint_as_float(qv.y), __uint_as_float(qv.z));
-      const float D = __uint_as_float(__dp4a(my_pk[k], qk, F2P23_BITS)) - F2P23;   // exact dot
-      const float Ph = __fmul_rn(my_nn[k], qn.x);
-      const float Pl = fmaf(my_nn[k], qn.x, -Ph);
-      const float X = __fadd_rn(fmaf(-D, D, Ph), Pl);         // |x_p x x_q|^2
-      const float s = __fmul_rn(my_nrm[k], qn.y);
-      const float w = fmaf(s, D, Ph);
-      const float tau = __fmul_rn(X, rsqrt_approx(fmaf(X, w, 1e-30f)));   // sqrt(1 - cos)
-      float v;
-      if (VAR == EXACT)
-        v = 2.0f * asinf(tau * 0.70710678118654752f);
-      else
-        v = horner4(coef::ASIN(), tau);
-      sm.M[dl][p] = v;
+    for (int dl = 0; dl < GD; dl += 2) {
+      const int d0 = G * GD + dl, d1 = d0 + 1;
+      const int q0 = p + delta_dy(R, d0) * PW + delta_dx(R, d0);   // in bounds (PAD); garbage if outside P
+      const int q1 = p + delta_dy(R, d1) * PW + delta_dx(R, d1);
+      VF_CHECK(q0 >= 0 && q0 < region_np(CFG) + PAD && q1 >= 0 && q1 < region_np(CFG) + PAD);
+      float tau0, tau1, v0, v1;
+      angular_tau2<VAR>(my_pk[k], nn2, nnn2, nrm2, sm.px[q0], sm.px[q1], tau0, tau1, v0, v1);
+      sm.M[dl][p] = v0;
+      sm.M[dl + 1][p] = v1;
       // cos < 0.5 <=> tau > 1/sqrt2: flag a superset (margin 2^-10 >> the
       // ~5e-7 relative error of tau) for the exact decision below.  Offsets
       // reaching below the region read the zero padding: tau = 0, never flagged.
-      if (tau > 0.70641626f) flags[k] |= 1u << dl;           // (1/sqrt2) (1 - 2^-10)
+      if (tau0 > 0.70641626f) flags[k] |= 1u << dl;           // (1/sqrt2) (1 - 2^-10)
+      if (tau1 > 0.70641626f) flags[k] |= 1u << (dl + 1);
     }
   }
   // ---- rare pairs: exact branch decision, warp-cooperative ---------------------------
