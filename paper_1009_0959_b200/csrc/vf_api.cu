@@ -222,12 +222,13 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
   } else {
     int th = vf::TY;
     if (crit == VF_EXP || crit == VF_LOG) {
-      // 3x3: 4 output rows per thread for large launches (staging and the S1
-      // row sums shared by 4 windows; exact variants 2, whose kept distances
-      // need the registers), 1 for small ones (more blocks); 5x5: 1.
+      // 3x3: 2 output rows per thread for large launches (staging and the S1
+      // row sums shared by 2 windows; measured best with the packed-FP32 pair
+      // loop: C4 exp minimax 130 us vs 135 with 4 rows), 1 for small ones
+      // (more blocks); 5x5: 1.
       // VF_EL_OPT=1|2|4 or the algo tile bits (1, 2, 3 -> 1, 2, 4) override.
       const long long npix = (long long)B * out_rows * W;
-      int opt = (window == 3 && npix >= (1LL << 21)) ? (var == VF_EXACT ? 2 : 4) : 1;
+      int opt = (window == 3 && npix >= (1LL << 21)) ? 2 : 1;
       static const int opt_env = [] { const char* e = std::getenv("VF_EL_OPT"); return e ? std::atoi(e) : 0; }();
       if (window == 3 && (opt_env == 1 || opt_env == 2 || opt_env == 4)) opt = opt_env;
       if (window == 3 && tile) opt = tile == 3 ? 4 : tile;
@@ -238,11 +239,13 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
       static const bool env_no_tma = [] { const char* e = std::getenv("VF_NO_TMA"); return e && e[0] == '1'; }();
       const unsigned long long row_bytes = (unsigned long long)W * 3;
       PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
-      // (measured on C3/C4: a few % faster for the 3x3 polynomial variants
-      // with 4 rows per thread; slower for the libm variants and 5x5, whose
-      // register budget the persistent loop tightens -- those stay on the
-      // plain-load kernel unless the caller forces it, for tests, with algo tile bits)
-      const bool tma_pays = window == 3 && var != VF_EXACT && opt == 4;
+      // (measured on C3/C4: with the scalar pair loop it was a few % faster for
+      // the 3x3 polynomial variants; since the packed-FP32 pair loop the
+      // plain-load kernel with 2 rows per thread is faster everywhere -- C4
+      // exp minimax 131 vs 143 us -- because the persistent loop costs
+      // registers and occupancy.  It stays available, bit-identical, through
+      // the algo tile bits or VF_FORCE_TMA=1, and is tested that way.)
+      const bool tma_pays = false;
       static const bool env_force_tma = [] { const char* e = std::getenv("VF_FORCE_TMA"); return e && e[0] == '1'; }();
       if ((tma_pays || env_force_tma || tile) && !no_tma && !env_no_tma && enc && row_bytes % 16 == 0 && ((uintptr_t)in % 16) == 0 &&
           (B == 1 || in_stride % 16 == 0) && row_bytes < (1ULL << 32)) {

@@ -107,7 +107,7 @@ __device__ __forceinline__ void role_group(RoleSmem<WIN, NT, PPT>& sm, const uin
   constexpr int R = WIN / 2;
   constexpr int NS = nslots(R, G);
   constexpr int QCAP = RoleSmem<WIN, NT, PPT>::QCAP;
-  constexpr int NPL = RoleSmem<WIN, NT, PPT>::NP;
+  [[maybe_unused]] constexpr int NPL = RoleSmem<WIN, NT, PPT>::NP;   // (VF_CHECK)
   const int lane = tid & 31, warp = tid >> 5;
   if (G > 0) __syncthreads();   // previous phase B done with the maps (G = 0: the staging barrier)
   // ---- phase A: maps of the offsets (G, dx) ----------------------------------------
