@@ -222,13 +222,14 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
   } else {
     int th = vf::TY;
     if (crit == VF_EXP || crit == VF_LOG) {
-      // 3x3: 2 output rows per thread for large launches (staging and the S1
-      // row sums shared by 2 windows; measured best with the packed-FP32 pair
-      // loop: C4 exp minimax 130 us vs 135 with 4 rows), 1 for small ones
-      // (more blocks); 5x5: 1.
+      // 3x3: 2 output rows per thread for large launches (4 for the cheap
+      // polynomial variants, whose per-window overheads weigh more: staging
+      // and the S1 row sums are shared by the stacked windows; measured on C4
+      // with the packed-FP32 pair loop), 1 for small ones (more blocks); 5x5: 1.
       // VF_EL_OPT=1|2|4 or the algo tile bits (1, 2, 3 -> 1, 2, 4) override.
       const long long npix = (long long)B * out_rows * W;
-      int opt = (window == 3 && npix >= (1LL << 21)) ? 2 : 1;
+      int opt = (window == 3 && npix >= (1LL << 21))
+                    ? ((var == VF_MINIMAX_POLY4 || var == VF_MINIMAX_REACH) ? 4 : 2) : 1;
       static const int opt_env = [] { const char* e = std::getenv("VF_EL_OPT"); return e ? std::atoi(e) : 0; }();
       if (window == 3 && (opt_env == 1 || opt_env == 2 || opt_env == 4)) opt = opt_env;
       if (window == 3 && tile) opt = tile == 3 ? 4 : tile;
