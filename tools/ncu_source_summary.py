@@ -29,12 +29,17 @@ def load(rep):
     return kernels
 
 
+FLOP_WEIGHTS = {"FFMA": 2, "FADD": 1, "FMUL": 1, "FFMA2": 4, "FADD2": 2, "FMUL2": 2}
+
+
 def main():
     rep = sys.argv[1]
     sel = sys.argv[2] if len(sys.argv) > 2 else ""
+    seen = set()
     for k in load(rep):
-        if sel not in k["name"]:
+        if sel not in k["name"] or k["name"] in seen:   # the source page lists each kernel twice
             continue
+        seen.add(k["name"])
         inst = Counter()
         stall = Counter()
         total_i = 0
@@ -52,6 +57,11 @@ def main():
         print(f"== {k['name'][:90]}  warp-inst {total_i}")
         for op, n in inst.most_common(16):
             print(f"   {op:12s} {n:12d} {100*n/total_i:6.1f}%   stall-samples {100*stall[op]/max(ts,1):5.1f}%")
+        # FP32 flops executed, counting the packed sm_100 forms (FFMA2 = 2 FMAs
+        # = 4 flops per lane); warp instructions x 32 lanes (an upper bound:
+        # partial warps are counted full)
+        fl = 32 * sum(inst[o] * w for o, w in FLOP_WEIGHTS.items())
+        print(f"   exec-fp32-flops {fl}")
 
 
 if __name__ == "__main__":

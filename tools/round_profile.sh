@@ -21,10 +21,11 @@ if [ $rc -eq 0 ]; then
   timeout 1200 ncu --set full --import-source on --clock-control none -k regex:vf_ -s 7 -c 7 -o gpurun_out/prof_C3 python tools/prof_driver.py --config C3 > gpurun_out/ncu_C3.log 2>&1
 fi
 # summarise on the box (the .ncu-rep files exceed gpurun's 64 MiB copy-back limit), keep the C4 report only
-VF_PROF_DIR=gpurun_out/prof_summary python tools/summarize_round.py ${TAG:-r01} > /dev/null 2>&1
+mkdir -p gpurun_out/prof_summary
 for c in C2 C3 C4; do
   [ -f gpurun_out/prof_$c.ncu-rep ] && python tools/ncu_source_summary.py gpurun_out/prof_$c.ncu-rep > gpurun_out/prof_summary/${TAG:-r01}_sass_mix_$c.txt 2>&1
 done
+VF_PROF_DIR=gpurun_out/prof_summary python tools/summarize_round.py ${TAG:-r01} > /dev/null 2>&1
 rm -f gpurun_out/prof_C2.ncu-rep gpurun_out/prof_C3.ncu-rep
 du -sh gpurun_out
 tail -2 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; tail -1 gpurun_out/bench.err; tail -1 gpurun_out/ncu_launch.log

@@ -83,6 +83,19 @@ def to_bytes(v, unit):
     return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
 
 
+def sass_mix_flops(path):
+    """kernel name (normalised, 60 chars) -> executed FP32 flops, from a SASS mix file."""
+    if not os.path.exists(path):
+        return {}
+    res, cur = {}, None
+    for line in open(path):
+        if line.startswith("== "):
+            cur = line[3:].split("  warp-inst")[0].replace("(int)", "").replace("vf::", "")[:60]
+        elif "exec-fp32-flops" in line and cur:
+            res[cur] = float(line.split()[-1])
+    return res
+
+
 def ncu_full(tag, cfg, npix, summary):
     rep = os.path.join(OUT, f"prof_{cfg}.ncu-rep")
     if not os.path.exists(rep):
@@ -114,19 +127,25 @@ def ncu_full(tag, cfg, npix, summary):
                 else:
                     vals.append(v[:6])
             fh.write(f"| {label} | " + " | ".join(vals) + " |\n")
-        # executed FP32 flops (ncu): 2 FFMA + FMUL + FADD thread instructions
-        # (predicated on) per elapsed cycle, over the FP32 peak 2 x 128 x SMs
-        ex = [("smsp__sass_thread_inst_executed_op_ffma_pred_on.sum.per_cycle_elapsed", 2),
-              ("smsp__sass_thread_inst_executed_op_fmul_pred_on.sum.per_cycle_elapsed", 1),
-              ("smsp__sass_thread_inst_executed_op_fadd_pred_on.sum.per_cycle_elapsed", 1)]
-        if all(m in col for m, _ in ex):
+        # executed FP32 flops per elapsed second over the FP32 peak (2 x 128 x
+        # SMs x clock), from the SASS mix (tools/ncu_source_summary.py: FFMA 2,
+        # FADD/FMUL 1, packed FFMA2 4, FADD2/FMUL2 2 flops per lane; ncu's
+        # op_ffma metrics do not count the packed sm_100 forms)
+        mix = sass_mix_flops(os.path.join(PROF, f"{tag}_sass_mix_{cfg}.txt"))
+        if mix and "gpu__time_duration.sum" in col:
             vals = []
             for r in data:
-                fl = sum(w * float(r[col[m]].replace(",", "")) for m, w in ex)
-                vals.append(f"{100 * fl / (2 * 128 * 148):.1f}%")
-                summary.setdefault("executed_fp32_frac", {})[f"{cfg}/{kernel_key(r[col['Kernel Name']])[0]}"] = \
-                    fl / (2 * 128 * 148)
-            fh.write("| executed FP32 flops (2 FFMA + FMUL + FADD) % of peak | " + " | ".join(vals) + " |\n")
+                fl = mix.get(r[col["Kernel Name"]].replace("(int)", "").replace("vf::", "")[:60])
+                t = to_bytes(r[col["gpu__time_duration.sum"]], "x") * (
+                    1e-9 if units[col["gpu__time_duration.sum"]] == "nsecond" else 1e-6)
+                if fl is None:
+                    vals.append("-")
+                    continue
+                frac = fl / t / (2 * 128 * 148 * 1.965e9)
+                vals.append(f"{100 * frac:.1f}%")
+                summary.setdefault("executed_fp32_frac", {})[f"{cfg}/{kernel_key(r[col['Kernel Name']])[0]}"] = frac
+            fh.write("| executed FP32 flops (FFMA/FFMA2/FADD/FADD2/FMUL/FMUL2, SASS mix) % of peak at 1965 MHz | "
+                     + " | ".join(vals) + " |\n")
         fh.write("\nKernel names: " + "; ".join(f"`{n[:80]}`" for n in names) + "\n")
     for r in data:
         key, w = kernel_key(r[col["Kernel Name"]])
