@@ -32,6 +32,9 @@
 
 #include "vf_window.cuh"
 
+#ifndef SHARED_PACKED_C
+#define SHARED_PACKED_C 0    // 1: phase C of two outputs per thread in packed FP32 (FADD2; measured slower, DESIGN 5.3.2)
+#endif
 #ifndef SHARED_MINB_CFG4
 #define SHARED_MINB_CFG4 4   // 384-thread blocks: <= 40 registers, 48 warps per SM (tuning knob)
 #endif
@@ -97,7 +100,8 @@ template <int WIN, int VAR, int GD, int OPT, int CFG, int G>
 __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint32_t (&my_pk)[shared::cfg_ppt(CFG)],
                                              const float (&my_nn)[shared::cfg_ppt(CFG)],
                                              const float (&my_nrm)[shared::cfg_ppt(CFG)],
-                                             float (&Ra)[OPT][WIN * WIN], int tid, bool blk_zero) {
+                                             float (&Ra)[OPT][WIN * WIN], f32x2 (&Rp)[WIN * WIN], int tid,
+                                             bool blk_zero) {
   using namespace shared;
   constexpr int PPT = cfg_ppt(CFG);
   constexpr int NT = cfg_nt(CFG);
@@ -204,6 +208,32 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint
   }
   __syncthreads();
   // ---- phase C: accumulate the window aggregates ------------------------------------
+  // Two outputs per thread (rows ty and ty + NW): their aggregates R_i are one
+  // packed pair and each pair value pair (v_row0, v_row1) is added with one
+  // FADD2 (per-element rounding = __fadd_rn, same order: bit-identical to the
+  // scalar loop).  Warps whose second row is past the tile accumulate a copy
+  // of the first window and discard it (warp-uniform, no divergence).
+  if constexpr (OPT == 2 && SHARED_PACKED_C) {
+    const int oy1 = ty + NW;
+    if (tx < TW) {
+      const int base0 = ty * PW + tx;
+      const int base1 = (TH % NW == 0 || oy1 < TH) ? oy1 * PW + tx : base0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int j = i + 1; j < N; ++j) {
+          const int d = delta_index(R, j / WIN - i / WIN, j % WIN - i % WIN);
+          if (d / GD == G) {
+            const int oi = (i / WIN) * PW + (i % WIN);
+            VF_CHECK(base1 + oi < region_np(CFG) && base0 + oi < region_np(CFG));
+            const f32x2 v = pack2(sm.M[d - G * GD][base0 + oi], sm.M[d - G * GD][base1 + oi]);
+            Rp[i] = add2(Rp[i], v);
+            Rp[j] = add2(Rp[j], v);
+          }
+        }
+      }
+    }
+  } else {
   // Rows past the output tile (TH not a multiple of 8) are skipped warp-
   // uniformly; the aggregates start at -0 inside the branch so that the first
   // addition of each folds away.
@@ -227,6 +257,7 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint
       }
     }
   }
+  }
 }
 
 template <int WIN, int VAR, int GD, int OPT, int CFG, int... Gs>
@@ -234,8 +265,8 @@ __device__ __forceinline__ void shared_groups(std::integer_sequence<int, Gs...>,
                                               const uint32_t (&my_pk)[shared::cfg_ppt(CFG)],
                                               const float (&my_nn)[shared::cfg_ppt(CFG)],
                                               const float (&my_nrm)[shared::cfg_ppt(CFG)], float (&Ra)[OPT][WIN * WIN],
-                                              int tid, bool blk_zero) {
-  (shared_group<WIN, VAR, GD, OPT, CFG, Gs>(sm, my_pk, my_nn, my_nrm, Ra, tid, blk_zero), ...);
+                                              f32x2 (&Rp)[WIN * WIN], int tid, bool blk_zero) {
+  (shared_group<WIN, VAR, GD, OPT, CFG, Gs>(sm, my_pk, my_nn, my_nrm, Ra, Rp, tid, blk_zero), ...);
 }
 
 // Resident blocks per SM the register allocation is held to.
@@ -298,9 +329,16 @@ __global__ void __launch_bounds__(shared::cfg_nt(CFG), shared_min_blocks(WIN, CF
   for (int k = 0; k < OPT; ++k)
 #pragma unroll
     for (int i = 0; i < N; ++i) Ra[k][i] = -0.0f;
+  f32x2 Rp[N];   // packed (row ty, row ty + NW) aggregates (OPT == 2, SHARED_PACKED_C)
+#pragma unroll
+  for (int i = 0; i < N; ++i) Rp[i] = pack2(-0.0f, -0.0f);
 
-  shared_groups<WIN, VAR, GD, OPT, CFG>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, Ra, tid,
+  shared_groups<WIN, VAR, GD, OPT, CFG>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, Ra, Rp, tid,
                                         blk_zero);
+  if constexpr (OPT == 2 && SHARED_PACKED_C) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) unpack2(Rp[i], Ra[0][i], Ra[1][i]);
+  }
 
   // ---- argmin + store ------------------------------------------------------------------
 #pragma unroll
