@@ -35,6 +35,9 @@
 #ifndef SHARED_PACKED_C
 #define SHARED_PACKED_C 0    // 1: phase C of two outputs per thread in packed FP32 (FADD2; measured slower, DESIGN 5.3.2)
 #endif
+#ifndef SHARED_REC8
+#define SHARED_REC8 1        // 8-byte neighbour records (packed RGB0, |x|^2): half the phase-A smem wavefronts, s = sqrt(Ph) by MUFU
+#endif
 #ifndef SHARED_MINB_CFG4
 #define SHARED_MINB_CFG4 4   // 384-thread blocks: <= 40 registers, 48 warps per SM (tuning knob)
 #endif
@@ -69,7 +72,11 @@ __host__ __device__ constexpr int delta_index(int r, int dy, int dx) {
 template <int GD, int CFG>
 struct SharedSmem {
   static constexpr int QCAP = 64;                   // rare-pair queue entries per warp
+#if SHARED_REC8
+  uint2 px[shared::region_np(CFG) + shared::PAD];   // (packed RGB0, |x|^2 bits): one LDS.64 per neighbour
+#else
   uint4 px[shared::region_np(CFG) + shared::PAD];   // (packed RGB0, |x|^2 bits, |x| bits, 0): one LDS.128 per neighbour
+#endif
   float M[GD][shared::region_np(CFG)];
   uint32_t queue[shared::cfg_nt(CFG) / 32][QCAP];   // flagged pairs of one warp: p | dl << 16
   int off[40];                                      // region offset of pair offset d (d < n_delta(r) <= 40)
@@ -82,14 +89,18 @@ struct SharedSmem {
 // never flagged) and are handled by the block-uniform path anyway.
 template <int VAR, int GD, int CFG>
 __device__ __forceinline__ void angular_fix(SharedSmem<GD, CFG>& sm, int p, int dl, int d) {
-  const uint4 pv = sm.px[p], qv = sm.px[p + sm.off[d]];
+  const auto pv = sm.px[p], qv = sm.px[p + sm.off[d]];
   const float D = __uint_as_float(__dp4a(pv.x, qv.x, F2P23_BITS)) - F2P23;   // exact dot
   const float nna = __uint_as_float(pv.y), nnb = __uint_as_float(qv.y);
   const float Ph = __fmul_rn(nna, nnb);
   const float Pl = fmaf(nna, nnb, -Ph);                     // exact residual
   const float t = fmaf(__fmul_rn(4.0f, D), D, -Ph);         // fl(4D^2 - Ph)
   if (t < Pl) {                                             // 4D^2 < P, exact
+#if SHARED_REC8
+    const float c = D * rsqrt_approx(Ph);                   // cos = D / sqrt(|x_p|^2 |x_q|^2)
+#else
     const float c = D * rcp_approx(__fmul_rn(__uint_as_float(pv.z), __uint_as_float(qv.z)));
+#endif
     sm.M[dl][p] = (VAR == EXACT) ? acosf(c) : horner4(coef::ACOS(), c);
   }
 }
@@ -131,7 +142,11 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint
       const int q1 = p + delta_dy(R, d1) * PW + delta_dx(R, d1);
       VF_CHECK(q0 >= 0 && q0 < region_np(CFG) + PAD && q1 >= 0 && q1 < region_np(CFG) + PAD);
       float tau0, tau1, v0, v1;
+#if SHARED_REC8
+      angular_tau2_r8<VAR>(my_pk[k], nn2, nnn2, sm.px[q0], sm.px[q1], tau0, tau1, v0, v1);
+#else
       angular_tau2<VAR>(my_pk[k], nn2, nnn2, nrm2, sm.px[q0], sm.px[q1], tau0, tau1, v0, v1);
+#endif
       sm.M[dl][p] = v0;
       sm.M[dl + 1][p] = v1;
       // cos < 0.5 <=> tau > 1/sqrt2: flag a superset (margin 2^-10 >> the
@@ -318,9 +333,17 @@ __global__ void __launch_bounds__(shared::cfg_nt(CFG), shared_min_blocks(WIN, CF
     my_nn[k] = nn;
     my_nrm[k] = nrm;
     has_zero |= (nn == 0.0f);
+#if SHARED_REC8
+    sm.px[p] = make_uint2(my_pk[k], __float_as_uint(nn));
+#else
     sm.px[p] = make_uint4(my_pk[k], __float_as_uint(nn), __float_as_uint(nrm), 0u);
+#endif
   }
+#if SHARED_REC8
+  if (tid < PAD) sm.px[NP + tid] = make_uint2(0u, 0u);
+#else
   if (tid < PAD) sm.px[NP + tid] = make_uint4(0u, 0u, 0u, 0u);
+#endif
   if (tid < ND) sm.off[tid] = delta_dy(R, tid) * PW + delta_dx(R, tid);
   const bool blk_zero = __syncthreads_or(has_zero) != 0;       // staging barrier
 

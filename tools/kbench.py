@@ -29,22 +29,29 @@ for cfg in cfgs:
     n = w * w
     pairs = n * (n - 1) // 2
     line = [f"{cfg}({w}x{w},{npix/1e6:.1f}Mpx)"]
-    for c in bench.COMBOS + bench.REACH_COMBOS:
-        if only and only not in f"{c[0]}/{c[1]}":
-            continue
-        for _ in range(3):
-            vfb.vf_filter_batch_algo(x, w, *c, algo, out=out)
-        ts = []
-        for _ in range(9):
-            flush.fill_(1)
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record()
-            vfb.vf_filter_batch_algo(x, w, *c, algo, out=out)
-            b.record()
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        ms = statistics.median(ts)
+    combos = [c for c in bench.COMBOS + bench.REACH_COMBOS if not only or only in f"{c[0]}/{c[1]}"]
+    outs = [torch.empty_like(x) for _ in combos]
+    if algo == "auto":
+        # average launch duration over back-to-back launches (bench.steady_kernel_ms)
+        sms, R = bench.steady_kernel_ms(vfb, torch, torch.device("cuda"), torch.cuda.current_stream(), flush, x, w,
+                                        combos, outs)
+    for c in combos:
+        if algo == "auto":
+            ms = sms[c]
+        else:
+            for _ in range(3):
+                vfb.vf_filter_batch_algo(x, w, *c, algo, out=out)
+            ts = []
+            for _ in range(9):
+                flush.fill_(1)
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record()
+                vfb.vf_filter_batch_algo(x, w, *c, algo, out=out)
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            ms = statistics.median(ts)
         frac = bench.FLOPS_PER_PAIR[c] * pairs * npix / (ms / 1e3) / 1e12 / bench.NOMINAL_FP32_TFLOPS_AT_MAX
         line.append(f"{c[0][:3]}/{c[1][:3]} {ms*1e3:8.1f}us {frac*100:4.1f}%")
     print(" | ".join(line), flush=True)
