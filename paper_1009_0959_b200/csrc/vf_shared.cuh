@@ -38,6 +38,9 @@
 #ifndef SHARED_REC8
 #define SHARED_REC8 1        // 8-byte neighbour records (packed RGB0, |x|^2): half the phase-A smem wavefronts, s = sqrt(Ph) by MUFU
 #endif
+#ifndef SHARED_ZLAYOUT
+#define SHARED_ZLAYOUT 1     // 3x3, 384 x 2 configuration: region rows r and r + 12 interleaved in the pair maps
+#endif
 #ifndef SHARED_MINB_CFG4
 #define SHARED_MINB_CFG4 4   // 384-thread blocks: <= 40 registers, 48 warps per SM (tuning knob)
 #endif
@@ -68,6 +71,19 @@ __host__ __device__ constexpr int delta_index(int r, int dy, int dx) {
 
 }  // namespace shared
 
+// Pair-map layout.  Default: M[d][p], p = row * 32 + col.  ZL (3x3, CFG 4:
+// 384 threads, region rows 0..23, thread tid owns rows tid/32 and tid/32 + 12):
+// M[d][2 (p mod 384) + p / 384], i.e. rows r and r + 12 are interleaved, so a
+// thread stores its two pixels' values with one STS.64 and reads the values of
+// its two output windows (rows ty and ty + 12) with one LDS.64.
+// Measured (C4): exact 175.5 -> 171.5 us, minimax 120.8 -> 125.0 us, so the
+// interleaved layout is used for the exact variant only.
+template <int WIN, int CFG, int VAR>
+struct MapLayout {
+  static constexpr bool ZL = SHARED_ZLAYOUT && WIN == 3 && CFG == 4 && VAR == EXACT;
+  __device__ __forceinline__ static int idx(int p) { return ZL ? ((p % 384) << 1) + p / 384 : p; }
+};
+
 // Per-block shared-memory state of the pair-sharing kernel.
 template <int GD, int CFG>
 struct SharedSmem {
@@ -87,7 +103,7 @@ struct SharedSmem {
 // arccos branch (cos < 0.5), its map entry is replaced by the ARCCOS row /
 // acosf of cos = D / (|x_p||x_q|).  Zero vectors never get here (tau = 0 is
 // never flagged) and are handled by the block-uniform path anyway.
-template <int VAR, int GD, int CFG>
+template <int VAR, int WIN, int GD, int CFG>
 __device__ __forceinline__ void angular_fix(SharedSmem<GD, CFG>& sm, int p, int dl, int d) {
   const auto pv = sm.px[p], qv = sm.px[p + sm.off[d]];
   const float D = __uint_as_float(__dp4a(pv.x, qv.x, F2P23_BITS)) - F2P23;   // exact dot
@@ -101,7 +117,7 @@ __device__ __forceinline__ void angular_fix(SharedSmem<GD, CFG>& sm, int p, int 
 #else
     const float c = D * rcp_approx(__fmul_rn(__uint_as_float(pv.z), __uint_as_float(qv.z)));
 #endif
-    sm.M[dl][p] = (VAR == EXACT) ? acosf(c) : horner4(coef::ACOS(), c);
+    sm.M[dl][MapLayout<WIN, CFG, VAR>::idx(p)] = (VAR == EXACT) ? acosf(c) : horner4(coef::ACOS(), c);
   }
 }
 
@@ -130,30 +146,40 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint
 #pragma unroll
   for (int k = 0; k < PPT; ++k) flags[k] = 0u;
   // two offsets per step in packed FP32 (FFMA2 / FADD2 / FMUL2, GD is even)
+  using ML = MapLayout<WIN, CFG, VAR>;
 #pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    const int p = tid + NT * k;
-    const f32x2 nn2 = pack2(my_nn[k], my_nn[k]), nnn2 = pack2(-my_nn[k], -my_nn[k]);
-    const f32x2 nrm2 = pack2(my_nrm[k], my_nrm[k]);
+  for (int dl = 0; dl < GD; dl += 2) {
+    const int d0 = G * GD + dl, d1 = d0 + 1;
+    float va[PPT][2];
 #pragma unroll
-    for (int dl = 0; dl < GD; dl += 2) {
-      const int d0 = G * GD + dl, d1 = d0 + 1;
+    for (int k = 0; k < PPT; ++k) {
+      const int p = tid + NT * k;
+      const f32x2 nn2 = pack2(my_nn[k], my_nn[k]), nnn2 = pack2(-my_nn[k], -my_nn[k]);
       const int q0 = p + delta_dy(R, d0) * PW + delta_dx(R, d0);   // in bounds (PAD); garbage if outside P
       const int q1 = p + delta_dy(R, d1) * PW + delta_dx(R, d1);
       VF_CHECK(q0 >= 0 && q0 < region_np(CFG) + PAD && q1 >= 0 && q1 < region_np(CFG) + PAD);
-      float tau0, tau1, v0, v1;
+      float tau0, tau1;
 #if SHARED_REC8
-      angular_tau2_r8<VAR>(my_pk[k], nn2, nnn2, sm.px[q0], sm.px[q1], tau0, tau1, v0, v1);
+      angular_tau2_r8<VAR>(my_pk[k], nn2, nnn2, sm.px[q0], sm.px[q1], tau0, tau1, va[k][0], va[k][1]);
 #else
-      angular_tau2<VAR>(my_pk[k], nn2, nnn2, nrm2, sm.px[q0], sm.px[q1], tau0, tau1, v0, v1);
+      const f32x2 nrm2 = pack2(my_nrm[k], my_nrm[k]);
+      angular_tau2<VAR>(my_pk[k], nn2, nnn2, nrm2, sm.px[q0], sm.px[q1], tau0, tau1, va[k][0], va[k][1]);
 #endif
-      sm.M[dl][p] = v0;
-      sm.M[dl + 1][p] = v1;
       // cos < 0.5 <=> tau > 1/sqrt2: flag a superset (margin 2^-10 >> the
       // ~5e-7 relative error of tau) for the exact decision below.  Offsets
       // reaching below the region read the zero padding: tau = 0, never flagged.
       if (tau0 > 0.70641626f) flags[k] |= 1u << dl;           // (1/sqrt2) (1 - 2^-10)
       if (tau1 > 0.70641626f) flags[k] |= 1u << (dl + 1);
+    }
+    if constexpr (ML::ZL) {
+      *reinterpret_cast<float2*>(&sm.M[dl][2 * tid]) = make_float2(va[0][0], va[1][0]);
+      *reinterpret_cast<float2*>(&sm.M[dl + 1][2 * tid]) = make_float2(va[0][1], va[1][1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        sm.M[dl][tid + NT * k] = va[k][0];
+        sm.M[dl + 1][tid + NT * k] = va[k][1];
+      }
     }
   }
   // ---- rare pairs: exact branch decision, warp-cooperative ---------------------------
@@ -189,14 +215,14 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint
       const int nq = total < QCAP ? total : QCAP;
       for (int e = lane; e < nq; e += 32) {
         const uint32_t en = q[e];
-        angular_fix<VAR>(sm, (int)(en & 0xffffu), (int)(en >> 16), G * GD + (int)(en >> 16));
+        angular_fix<VAR, WIN>(sm, (int)(en & 0xffffu), (int)(en >> 16), G * GD + (int)(en >> 16));
       }
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {                         // overflow only
         while (flags[k]) {
           const int dl = __ffs(flags[k]) - 1;
           flags[k] &= flags[k] - 1;
-          angular_fix<VAR>(sm, tid + NT * k, dl, G * GD + dl);
+          angular_fix<VAR, WIN>(sm, tid + NT * k, dl, G * GD + dl);
         }
       }
       __syncwarp();                                           // queue reusable by the next group
@@ -215,8 +241,8 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint
         for (int dl = 0; dl < GD; ++dl) {
           const int d = G * GD + dl;
           const int off = delta_dy(R, d) * PW + delta_dx(R, d);
-          sm.M[dl][p] = 0.0f;
-          if (p - off >= 0) sm.M[dl][p - off] = 0.0f;
+          sm.M[dl][ML::idx(p)] = 0.0f;
+          if (p - off >= 0) sm.M[dl][ML::idx(p - off)] = 0.0f;
         }
       }
     }
@@ -228,7 +254,42 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint
   // FADD2 (per-element rounding = __fadd_rn, same order: bit-identical to the
   // scalar loop).  Warps whose second row is past the tile accumulate a copy
   // of the first window and discard it (warp-uniform, no divergence).
-  if constexpr (OPT == 2 && SHARED_PACKED_C) {
+  if constexpr (ML::ZL) {
+    // rows ty and ty + 12 of the maps are adjacent: one LDS.64 per pair feeds
+    // both windows of warps 0..9; warps 10, 11 (second row past the 22-row
+    // tile) read their one window's values one by one
+    static_assert(OPT == 2 && NW == 12 && TH == 22 && GD == 12, "ZL layout: 3x3, CFG 4");
+    if (tx < TW) {
+      const int base = ty * PW + tx;                          // P index of window sample (0,0), row ty
+      if (ty + NW < TH) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+#pragma unroll
+          for (int j = i + 1; j < N; ++j) {
+            const int d = delta_index(R, j / WIN - i / WIN, j % WIN - i % WIN);
+            const int q = base + (i / WIN) * PW + (i % WIN);  // row <= 11
+            VF_CHECK(q < 384);
+            const float2 v = *reinterpret_cast<const float2*>(&sm.M[d][2 * q]);
+            Ra[0][i] += v.x;
+            Ra[0][j] += v.x;
+            Ra[1][i] += v.y;
+            Ra[1][j] += v.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+#pragma unroll
+          for (int j = i + 1; j < N; ++j) {
+            const int d = delta_index(R, j / WIN - i / WIN, j % WIN - i % WIN);
+            const float v = sm.M[d][ML::idx(base + (i / WIN) * PW + (i % WIN))];
+            Ra[0][i] += v;
+            Ra[0][j] += v;
+          }
+        }
+      }
+    }
+  } else if constexpr (OPT == 2 && SHARED_PACKED_C) {
     const int oy1 = ty + NW;
     if (tx < TW) {
       const int base0 = ty * PW + tx;
