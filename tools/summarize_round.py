@@ -25,9 +25,9 @@ VAR = {0: "exact", 1: "minimax", 2: "poly4", 3: "reach"}
 
 def kernel_key(name):
     name = name.replace("(int)", "")
-    m = re.search(r"vf_angular_role_kernel<(\d), \d>", name)
+    m = re.search(r"vf_angular_role_kernel<(\d), (\d)", name)   # <WIN, VAR, NT, PPT>
     if m:
-        return f"angular/{VAR[int(m.group(1))]}", 5
+        return f"angular/{VAR[int(m.group(2))]}", int(m.group(1))
     m = re.search(r"vf_angular_(shared|window)_kernel<(\d), (\d)(?:, \d)?>", name)
     if m:
         return f"angular/{VAR[int(m.group(3))]}", int(m.group(2))
@@ -78,6 +78,9 @@ METRICS = [
 ]
 
 
+TIME_TO_US = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
+
+
 def to_bytes(v, unit):
     f = float(v.replace(",", ""))
     return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
@@ -120,8 +123,8 @@ def ncu_full(tag, cfg, npix, summary):
                 v = r[col[m]]
                 if m.startswith("dram__bytes"):
                     vals.append(f"{to_bytes(v, units[col[m]])/1e6:.2f} MB")
-                elif m == "gpu__time_duration.sum":
-                    vals.append(f"{to_bytes(v, 'x') * (1e-3 if units[col[m]] == 'nsecond' else 1):.1f}")
+                elif m == "gpu__time_duration.sum":   # in µs
+                    vals.append(f"{to_bytes(v, 'x') * TIME_TO_US[units[col[m]]]:.1f}")
                 elif m == "smsp__inst_executed.sum":
                     vals.append(f"{float(v.replace(',', ''))*32/npix:.0f} /px")
                 else:
@@ -136,8 +139,7 @@ def ncu_full(tag, cfg, npix, summary):
             vals = []
             for r in data:
                 fl = mix.get(r[col["Kernel Name"]].replace("(int)", "").replace("vf::", "")[:60])
-                t = to_bytes(r[col["gpu__time_duration.sum"]], "x") * (
-                    1e-9 if units[col["gpu__time_duration.sum"]] == "nsecond" else 1e-6)
+                t = to_bytes(r[col["gpu__time_duration.sum"]], "x") * TIME_TO_US[units[col["gpu__time_duration.sum"]]] * 1e-6
                 if fl is None:
                     vals.append("-")
                     continue
