@@ -308,6 +308,38 @@ __device__ __forceinline__ void angular_tau2_r8(uint32_t pk, f32x2 nn2, f32x2 nn
   }
 }
 
+// Two angular pair evaluations on the tau branch for TWO pixels against one
+// neighbour offset (vf_shared.cuh PX2): pk0/pk1 the pixels' packed RGB,
+// nn2 = (|p0|^2, |p1|^2), nnn2 = -nn2, q = (pk(q0), pk(q1), |q0|^2, |q1|^2).
+// Element-wise the same roundings as angular_tau2_r8.
+template <int VAR>
+__device__ __forceinline__ void angular_tau2_px2(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2, uint4 q,
+                                                 float& tau0, float& tau1, float& v0, float& v1) {
+  const f32x2 C = pack2(F2P23, F2P23);
+  const f32x2 Db = pack2(__uint_as_float(__dp4a(pk0, q.x, F2P23_BITS)), __uint_as_float(__dp4a(pk1, q.y, F2P23_BITS)));
+  const f32x2 D = sub2(Db, C);                            // exact dot products
+  const f32x2 nD = sub2(C, Db);                           // -D, exact
+  const f32x2 nnq = pack2(__uint_as_float(q.z), __uint_as_float(q.w));
+  const f32x2 Ph = mul2(nn2, nnq);
+  const f32x2 nPl = fma2(nnn2, nnq, Ph);                  // -(exact residual of nn nnq)
+  const f32x2 X = sub2(fma2(nD, D, Ph), nPl);             // |p x q|^2
+  float ph0, ph1, s0, s1;
+  unpack2(Ph, ph0, ph1);
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(s0) : "f"(ph0));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(s1) : "f"(ph1));
+  const f32x2 w = fma2(pack2(s0, s1), D, Ph);             // s (s + D)
+  float xw0, xw1;
+  unpack2(fma2(X, w, pack2(1e-30f, 1e-30f)), xw0, xw1);
+  const f32x2 t = mul2(X, pack2(rsqrt_approx(xw0), rsqrt_approx(xw1)));   // sqrt(1 - cos)
+  unpack2(t, tau0, tau1);
+  if (VAR == EXACT) {
+    v0 = 2.0f * asinf(tau0 * 0.70710678118654752f);
+    v1 = 2.0f * asinf(tau1 * 0.70710678118654752f);
+  } else {
+    unpack2(horner4x2(coef::ASIN(), t), v0, v1);
+  }
+}
+
 // ---- chunk schedule of the packed accumulation (N = 2M + 1 samples) ----------
 // Aggregates are held as packed pairs A_g = (R_2g, R_2g+1), g < M, plus R_{N-1}.
 // The N(N-1)/2 pairs are grouped into chunks of two whose values V = (v0, v1)

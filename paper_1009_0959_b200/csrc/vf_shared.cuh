@@ -28,6 +28,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <type_traits>
 #include <utility>
 
 #include "vf_window.cuh"
@@ -37,6 +38,9 @@
 #endif
 #ifndef SHARED_REC8
 #define SHARED_REC8 1        // 8-byte neighbour records (packed RGB0, |x|^2): half the phase-A smem wavefronts, s = sqrt(Ph) by MUFU
+#endif
+#ifndef SHARED_PX2
+#define SHARED_PX2 1         // 3x3, CFG 4: phase A packs a thread's two pixels (not two offsets) per FFMA2 chain
 #endif
 #ifndef SHARED_ZLAYOUT
 #define SHARED_ZLAYOUT 1     // 3x3, 384 x 2 configuration: region rows r and r + 12 interleaved in the pair maps
@@ -85,18 +89,37 @@ struct MapLayout {
 };
 
 // Per-block shared-memory state of the pair-sharing kernel.
+// Pixel records.  Default: px[m] per region pixel m.  PX2 (3x3, CFG 4, whose
+// threads own pixels p and p + 384): px[j] = (pk(j), pk(j + 384), |x_j|^2,
+// |x_{j+384}|^2) for j < 384 + PAD (zero past the region), so one LDS.128 of
+// px[p + off] gives the neighbours of BOTH of a thread's pixels for offset
+// off as ready register pairs, and one FFMA2 chain evaluates the two pairs.
 template <int GD, int CFG>
 struct SharedSmem {
   static constexpr int QCAP = 64;                   // rare-pair queue entries per warp
+  static constexpr bool PX2 = SHARED_PX2 && CFG == 4 && GD == 12;   // GD 12 <=> 3x3
 #if SHARED_REC8
-  uint2 px[shared::region_np(CFG) + shared::PAD];   // (packed RGB0, |x|^2 bits): one LDS.64 per neighbour
+  using Rec = typename std::conditional<PX2, uint4, uint2>::type;   // (packed RGB0, |x|^2 bits): one LDS.64 per neighbour
 #else
-  uint4 px[shared::region_np(CFG) + shared::PAD];   // (packed RGB0, |x|^2 bits, |x| bits, 0): one LDS.128 per neighbour
+  using Rec = uint4;   // (packed RGB0, |x|^2 bits, |x| bits, 0): one LDS.128 per neighbour
 #endif
+  Rec px[(PX2 ? 384 : shared::region_np(CFG)) + shared::PAD];
   float M[GD][shared::region_np(CFG)];
   uint32_t queue[shared::cfg_nt(CFG) / 32][QCAP];   // flagged pairs of one warp: p | dl << 16
   int off[40];                                      // region offset of pair offset d (d < n_delta(r) <= 40)
 };
+
+// (packed RGB0, |x|^2 bits) of region pixel m (m < region + PAD: zero past it).
+template <int GD, int CFG>
+__device__ __forceinline__ uint2 rec_get(const SharedSmem<GD, CFG>& sm, int m) {
+  if constexpr (SharedSmem<GD, CFG>::PX2) {
+    const uint4 r = sm.px[m < 384 ? m : m - 384];
+    return m < 384 ? make_uint2(r.x, r.z) : make_uint2(r.y, r.w);
+  } else {
+    const auto r = sm.px[m];
+    return make_uint2(r.x, r.y);
+  }
+}
 
 // Exact re-evaluation of a flagged pair (p, p + off) of offset slot dl: the
 // exact branch predicate 4D^2 < P; if the pair is on the
@@ -105,18 +128,14 @@ struct SharedSmem {
 // never flagged) and are handled by the block-uniform path anyway.
 template <int VAR, int WIN, int GD, int CFG>
 __device__ __forceinline__ void angular_fix(SharedSmem<GD, CFG>& sm, int p, int dl, int d) {
-  const auto pv = sm.px[p], qv = sm.px[p + sm.off[d]];
+  const uint2 pv = rec_get(sm, p), qv = rec_get(sm, p + sm.off[d]);
   const float D = __uint_as_float(__dp4a(pv.x, qv.x, F2P23_BITS)) - F2P23;   // exact dot
   const float nna = __uint_as_float(pv.y), nnb = __uint_as_float(qv.y);
   const float Ph = __fmul_rn(nna, nnb);
   const float Pl = fmaf(nna, nnb, -Ph);                     // exact residual
   const float t = fmaf(__fmul_rn(4.0f, D), D, -Ph);         // fl(4D^2 - Ph)
   if (t < Pl) {                                             // 4D^2 < P, exact
-#if SHARED_REC8
     const float c = D * rsqrt_approx(Ph);                   // cos = D / sqrt(|x_p|^2 |x_q|^2)
-#else
-    const float c = D * rcp_approx(__fmul_rn(__uint_as_float(pv.z), __uint_as_float(qv.z)));
-#endif
     sm.M[dl][MapLayout<WIN, CFG, VAR>::idx(p)] = (VAR == EXACT) ? acosf(c) : horner4(coef::ACOS(), c);
   }
 }
@@ -145,8 +164,28 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint
   uint32_t flags[PPT];                                      // bit dl: pair (p_k, p_k + delta) flagged
 #pragma unroll
   for (int k = 0; k < PPT; ++k) flags[k] = 0u;
-  // two offsets per step in packed FP32 (FFMA2 / FADD2 / FMUL2, GD is even)
   using ML = MapLayout<WIN, CFG, VAR>;
+  if constexpr (SharedSmem<GD, CFG>::PX2) {
+    // one offset per step, the thread's two pixels in packed FP32
+    const f32x2 nn2 = pack2(my_nn[0], my_nn[1]), nnn2 = pack2(-my_nn[0], -my_nn[1]);
+#pragma unroll
+    for (int dl = 0; dl < GD; ++dl) {
+      const int d = G * GD + dl;
+      const int j = tid + delta_dy(R, d) * PW + delta_dx(R, d);
+      VF_CHECK(j >= 0 && j < 384 + PAD);
+      float tau0, tau1, v0, v1;
+      angular_tau2_px2<VAR>(my_pk[0], my_pk[1], nn2, nnn2, sm.px[j], tau0, tau1, v0, v1);
+      if (tau0 > 0.70641626f) flags[0] |= 1u << dl;           // (1/sqrt2) (1 - 2^-10), see below
+      if (tau1 > 0.70641626f) flags[1] |= 1u << dl;
+      if constexpr (ML::ZL) {
+        *reinterpret_cast<float2*>(&sm.M[dl][2 * tid]) = make_float2(v0, v1);
+      } else {
+        sm.M[dl][tid] = v0;
+        sm.M[dl][tid + NT] = v1;
+      }
+    }
+  } else {
+  // two offsets per step in packed FP32 (FFMA2 / FADD2 / FMUL2, GD is even)
 #pragma unroll
   for (int dl = 0; dl < GD; dl += 2) {
     const int d0 = G * GD + dl, d1 = d0 + 1;
@@ -181,6 +220,7 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint
         sm.M[dl + 1][tid + NT * k] = va[k][1];
       }
     }
+  }
   }
   // ---- rare pairs: exact branch decision, warp-cooperative ---------------------------
   // The flagged pairs of the warp (~1% of its pairs, spread over a few lanes)
@@ -394,17 +434,25 @@ __global__ void __launch_bounds__(shared::cfg_nt(CFG), shared_min_blocks(WIN, CF
     my_nn[k] = nn;
     my_nrm[k] = nrm;
     has_zero |= (nn == 0.0f);
+    if constexpr (!SharedSmem<GD, CFG>::PX2) {
 #if SHARED_REC8
-    sm.px[p] = make_uint2(my_pk[k], __float_as_uint(nn));
+      sm.px[p] = make_uint2(my_pk[k], __float_as_uint(nn));
 #else
-    sm.px[p] = make_uint4(my_pk[k], __float_as_uint(nn), __float_as_uint(nrm), 0u);
+      sm.px[p] = make_uint4(my_pk[k], __float_as_uint(nn), __float_as_uint(nrm), 0u);
+#endif
+    }
+  }
+  if constexpr (SharedSmem<GD, CFG>::PX2) {
+    static_assert(PPT == 2 && NT == 384 && PAD <= 384, "PX2: 384 threads x 2 pixels");
+    sm.px[tid] = make_uint4(my_pk[0], my_pk[1], __float_as_uint(my_nn[0]), __float_as_uint(my_nn[1]));
+    if (tid < PAD) sm.px[384 + tid] = make_uint4(my_pk[1], 0u, __float_as_uint(my_nn[1]), 0u);   // rows 12.., zero pad
+  } else {
+#if SHARED_REC8
+    if (tid < PAD) sm.px[NP + tid] = make_uint2(0u, 0u);
+#else
+    if (tid < PAD) sm.px[NP + tid] = make_uint4(0u, 0u, 0u, 0u);
 #endif
   }
-#if SHARED_REC8
-  if (tid < PAD) sm.px[NP + tid] = make_uint2(0u, 0u);
-#else
-  if (tid < PAD) sm.px[NP + tid] = make_uint4(0u, 0u, 0u, 0u);
-#endif
   if (tid < ND) sm.off[tid] = delta_dy(R, tid) * PW + delta_dx(R, tid);
   const bool blk_zero = __syncthreads_or(has_zero) != 0;       // staging barrier
 
@@ -441,7 +489,7 @@ __global__ void __launch_bounds__(shared::cfg_nt(CFG), shared_min_blocks(WIN, CF
         bv = lt ? Ra[k][i] : bv;
         so = lt ? (i / WIN) * PW + (i % WIN) : so;
       }
-      store_result<N>(L, b, gx, gy, Ra[k], sm.px[base + so].x);
+      store_result<N>(L, b, gx, gy, Ra[k], rec_get(sm, base + so).x);
     }
   }
 }
