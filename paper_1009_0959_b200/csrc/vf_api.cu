@@ -123,6 +123,21 @@ const void* el_kernel(int crit, int var) {
   return var == EXACT ? (const void*)vf_el_kernel<WIN, LOGC, EXACT, OPT> : (const void*)vf_el_kernel<WIN, LOGC, MINIMAX, OPT>;
 }
 
+// 3x3 polynomial / rational variants with NTY-warp blocks
+template <int OPT, int NTY>
+const void* el_kernel_ty(int crit, int var) {
+  using namespace vf;
+  if (crit == EXPC) {
+    if (var == MINIMAX) return (const void*)vf_el_kernel<3, EXPC, MINIMAX, OPT, NTY>;
+    if (var == REACH) return (const void*)vf_el_kernel<3, EXPC, REACH, OPT, NTY>;
+    if (var == POLY4) return (const void*)vf_el_kernel<3, EXPC, POLY4, OPT, NTY>;
+    return nullptr;
+  }
+  if (var == REACH) return (const void*)vf_el_kernel<3, LOGC, REACH, OPT, NTY>;
+  if (var == MINIMAX) return (const void*)vf_el_kernel<3, LOGC, MINIMAX, OPT, NTY>;
+  return nullptr;
+}
+
 template <int WIN, int OPT>
 const void* el_tma_kernel(int crit, int var) {
   using namespace vf;
@@ -222,14 +237,18 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
   } else {
     int th = vf::TY;
     if (crit == VF_EXP || crit == VF_LOG) {
-      // 3x3: 2 output rows per thread for large launches (4 for the cheap
-      // polynomial variants, whose per-window overheads weigh more: staging
-      // and the S1 row sums are shared by the stacked windows; measured on C4
-      // with the packed-FP32 pair loop), 1 for small ones (more blocks); 5x5: 1.
+      // 3x3: several output rows per thread for large launches (staging and
+      // the S1 row sums are shared by the stacked windows; the libm variants
+      // 2, the others 4 -- below), 1 for small ones (more blocks); 5x5: 1.
       // VF_EL_OPT=1|2|4 or the algo tile bits (1, 2, 3 -> 1, 2, 4) override.
+      // Large 3x3 launches of the non-libm variants: 4 rows per thread in
+      // 4-warp blocks (32 x 16 outputs; C4: poly4 94.5 -> 92.6 us, exp reach
+      // 101.9 -> 98.6 us, exp/log minimax 125.7 -> 124.4 us vs 8-warp blocks
+      // with 4 / 2 rows); VF_EL_TY=8 restores the 8-warp blocks.
       const long long npix = (long long)B * out_rows * W;
-      int opt = (window == 3 && npix >= (1LL << 21))
-                    ? ((var == VF_MINIMAX_POLY4 || var == VF_MINIMAX_REACH) ? 4 : 2) : 1;
+      const bool big3 = window == 3 && npix >= (1LL << 21);
+      int opt = big3 ? (var == VF_EXACT ? 2 : 4) : 1;
+      int nty = (big3 && var != VF_EXACT) ? 4 : vf::TY;
       static const int opt_env = [] { const char* e = std::getenv("VF_EL_OPT"); return e ? std::atoi(e) : 0; }();
       if (window == 3 && (opt_env == 1 || opt_env == 2 || opt_env == 4)) opt = opt_env;
       if (window == 3 && tile) opt = tile == 3 ? 4 : tile;
@@ -276,6 +295,19 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
         }
       }
       th = vf::TY * opt;
+      static const int ty_env = [] { const char* e = std::getenv("VF_EL_TY"); return e ? std::atoi(e) : 0; }();
+      if (window == 3 && (ty_env == 4 || ty_env == vf::TY)) nty = ty_env;
+      if (window == 3 && nty == 4 && opt >= 2 && var != VF_EXACT) {
+        kd->fn = opt == 4 ? el_kernel_ty<4, 4>(crit, var) : el_kernel_ty<2, 4>(crit, var);
+        th = 4 * opt;
+        kd->grid = dim3((W + vf::TX - 1) / vf::TX, (out_rows + th - 1) / th, B);
+        kd->block = dim3(vf::TX, 4);
+        kd->smem = 0;
+        if (kd->grid.y > 65535 || kd->grid.z > 65535)
+          return fail(VF_EINVAL, "grid too large (%lld blocks in y or z)",
+                      (long long)(kd->grid.y > kd->grid.z ? kd->grid.y : kd->grid.z));
+        return VF_OK;
+      }
     } else {
       kd->fn = window == 3 ? window_kernel<3>(crit, var) : window_kernel<5>(crit, var);
     }

@@ -353,10 +353,11 @@ __device__ __forceinline__ void el_compute_tile(const Launch& L, int b, int x0, 
   }
 }
 
-template <int WIN, int CRIT, int VAR, int OPT>
-__global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
+// NTY = warps per block (block 32 x NTY threads, output tile 32 x NTY*OPT).
+template <int WIN, int CRIT, int VAR, int OPT, int NTY = TY>
+__global__ void __launch_bounds__(TX * NTY) vf_el_kernel(const Launch L) {
   constexpr int R = WIN / 2;
-  constexpr int TYE = TY * OPT;                // output tile height
+  constexpr int TYE = NTY * OPT;               // output tile height
   constexpr int SW = TX + 2 * R;
   constexpr int SH = TYE + 2 * R;
   __shared__ StageSmem<SW, SH> sm;
@@ -365,7 +366,7 @@ __global__ void __launch_bounds__(TX * TY) vf_el_kernel(const Launch L) {
   const int x0 = blockIdx.x * TX;
   const int y0 = L.out_row0 + blockIdx.y * TYE;
   const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
-  stage_packed<SW, SH, TX, TY>(L, in, x0 - R, y0 - R, sm);
+  stage_packed<SW, SH, TX, NTY>(L, in, x0 - R, y0 - R, sm);
 
   el_compute_tile<WIN, CRIT, VAR, OPT>(L, b, x0, y0, sm.pk);
 }
