@@ -31,7 +31,7 @@ def kernel_key(name):
     m = re.search(r"vf_angular_(shared|window)_kernel<(\d), (\d)(?:, \d)?>", name)
     if m:
         return f"angular/{VAR[int(m.group(3))]}", int(m.group(2))
-    m = re.search(r"vf_el(?:_tma)?_kernel<(\d), (\d), (\d)(?:, \d)?>", name)
+    m = re.search(r"vf_el(?:_tma)?_kernel<(\d), (\d), (\d)(?:, \d)*>", name)
     if m:
         return f"{CRIT[int(m.group(2))]}/{VAR[int(m.group(3))]}", int(m.group(1))
     return None, None
