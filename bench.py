@@ -587,6 +587,9 @@ def main():
                                "tools/fp32_peak.cu measures 68.9 TFLOP/s of FFMA",
                 "traffic": ncu_traffic(f"{spec.name}/{dom}"),
                 "algorithmic_flops_per_launch": FLOPS_PER_PAIR[tuple(dom.split("/"))] * pairs * npix,
+                "note": ("libm-bound exact variant (CUDA's expm1f / log1pf / asinf: range reduction, polynomial, "
+                         "special-case selects, ~24-37 SASS instructions per pair); the minimax kernels of the same "
+                         "step are in per_kernel / best_minimax_kernel") if dom.endswith("exact") else None,
                 "timing": f"average launch duration over {R} back-to-back launches (one CUDA graph replay, events on "
                           f"the launching stream) over {R} distinct copies of the step input ({R * in_bytes >> 20} MiB "
                           "> L2), L2 flushed before each replay; the isolated single-launch time is per_kernel."
