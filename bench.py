@@ -242,7 +242,7 @@ def run_reference(args):
                          "sample": f"{args.steps} steps x 7 filters of {x.shape[1]}x{x.shape[2]}x{x.shape[0]} px"},
         "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -358,14 +358,14 @@ def run_partitioned(args):
                 full_ok[w] = bool(full.shape[0] == spec.H)
         extra["gathered_rows_ok"] = full_ok
     if rank == 0:
-        print(json.dumps({
+        emit({
             "metric": "filtered Mpixels/s", "value": units / (ms / 1e3) / 1e6, "unit": "Mpix/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_s, "mode": args.mode, "parallelism": f"dp{world}",
                        "input_generation_s": t_gen},
             "gpu_launches": (2 * len(COMBOS) if args.mode == "shard" else len(spec.window)) * args.steps,
-            **extra}), flush=True)
+            **extra})
     dist.destroy_process_group()
     return 0
 
@@ -448,7 +448,23 @@ KERNEL_NAMES = {"angular": "vf_angular_shared_kernel<{w},{v}>", "exp": "vf_el_ke
                 "log": "vf_el_kernel<{w},log,{v}>"}   # (3x3 polynomial variants of large launches: vf_el_tma_kernel)
 
 
+# The JSON line goes to the original stdout; everything else written to fd 1
+# (NCCL's version banner, library prints) is redirected to stderr so that
+# stdout carries exactly one line.
+_JSON_OUT = None
+
+
+def emit(line: dict):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
@@ -695,7 +711,7 @@ def main():
             "peaks": {"hbm_gbs": measured_peaks().get("hbm_gbs"),
                       "fp32_tflops_nominal_at_max_clock": NOMINAL_FP32_TFLOPS_AT_MAX},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     plan.close()
     if world > 1:
         dist.destroy_process_group()

@@ -175,6 +175,13 @@ VF_API int vf_plan_destroy(vf_plan plan);
  * pixel and summed in double).  Overwrites stats. */
 VF_API int vf_image_stats(const uint8_t *a, const uint8_t *b, int B, int H, int W, double *stats,
                    void *stream);
+/* As vf_image_stats; flags = VF_STATS_NO_REF_NORM (1) skips the reference
+ * norm sum stats[.][4] (written as 0): it depends on `a` only, so a caller
+ * comparing several outputs with one reference computes it once.  Then a's
+ * CIELAB is only evaluated where a != b.  Other flags: VF_EINVAL. */
+#define VF_STATS_NO_REF_NORM 1
+VF_API int vf_image_stats_ex(const uint8_t *a, const uint8_t *b, int B, int H, int W, double *stats, int flags,
+                             void *stream);
 
 VF_API const char *vf_status_string(int status);
 /* Text of the last error on the calling thread ("" if none). */

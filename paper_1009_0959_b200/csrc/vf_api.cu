@@ -496,8 +496,14 @@ int vf_plan_destroy(vf_plan plan) {
 }
 
 int vf_image_stats(const uint8_t* a, const uint8_t* b, int B, int H, int W, double* stats, void* stream) {
+  return vf_image_stats_ex(a, b, B, H, W, stats, 0, stream);
+}
+
+int vf_image_stats_ex(const uint8_t* a, const uint8_t* b, int B, int H, int W, double* stats, int flags,
+                      void* stream) {
   g_err[0] = 0;
   if (!a || !b || !stats) return fail(VF_EINVAL, "NULL pointer");
+  if (flags & ~VF_STATS_NO_REF_NORM) return fail(VF_EINVAL, "unknown stats flags (%lld)", flags);
   if (B < 1 || H < 1 || W < 1) return fail(VF_EINVAL, "bad size");
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(double) * 8 * (size_t)B, st);
@@ -506,7 +512,7 @@ int vf_image_stats(const uint8_t* a, const uint8_t* b, int B, int H, int W, doub
   int blocks = (int)((npix + 255) / 256);
   const int per_image = (148 * 8 + B - 1) / B;   // ~8 blocks per SM over the whole batch
   if (blocks > per_image) blocks = per_image < 1 ? 1 : per_image;
-  vf::vf_stats_kernel<<<dim3(blocks, B), 256, 0, st>>>(a, b, npix, stats);
+  vf::vf_stats_kernel<<<dim3(blocks, B), 256, 0, st>>>(a, b, npix, stats, (flags & VF_STATS_NO_REF_NORM) ? 0 : 1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "vf_stats_kernel launch");
   return VF_OK;

@@ -56,9 +56,9 @@ def _cuda_filter_rows(band, band_row0, H, out_row0, out_rows, window, criterion,
     return vf.vf_filter_rows(band, band_row0, H, out_row0, out_rows, window, criterion, variant)
 
 
-def _cuda_stats(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+def _cuda_stats(a: torch.Tensor, b: torch.Tensor, ref_norm: bool = True) -> torch.Tensor:
     from . import vf
-    return vf.vf_image_stats(a, b)
+    return vf.vf_image_stats(a, b, ref_norm=ref_norm)
 
 
 # ----------------------------------------------------------------- batch sharding
@@ -84,8 +84,14 @@ def gather_batch_stats(outs: dict, B: int, combos, reference: Optional[Tuple] = 
     counts = [shard_range(B, world, r)[1] - shard_range(B, world, r)[0] for r in range(world)]
     ref = tuple(reference) if reference is not None else tuple(combos[0])
     stats = {}
+    ref_norm = None   # column 4 (sum |ref_Lab|) depends on the reference only: computed once
     for c in combos:
-        s = stats_fn(outs[ref], outs[tuple(c)]).to(torch.float64)
+        if ref_norm is None or stats_fn is not _cuda_stats:
+            s = stats_fn(outs[ref], outs[tuple(c)]).to(torch.float64)
+            ref_norm = s[:, 4].clone()
+        else:
+            s = stats_fn(outs[ref], outs[tuple(c)], ref_norm=False).to(torch.float64)
+            s[:, 4] = ref_norm
         stats[tuple(c)] = all_gather_rows(s, counts, group)
     return stats
 

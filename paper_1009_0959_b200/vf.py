@@ -27,7 +27,8 @@ VARIANTS = {"exact": VF_EXACT, "minimax": VF_MINIMAX, "poly4": VF_MINIMAX_POLY4,
 ALGOS = {"auto": VF_ALGO_AUTO, "window": VF_ALGO_WINDOW, "shared": VF_ALGO_SHARED, "role": VF_ALGO_ROLE}
 EXPORTS = ["vf_filter", "vf_filter_batch", "vf_filter_rows", "vf_filter_batch_algo",
            "vf_host_workspace_bytes", "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_destroy",
-           "vf_image_stats", "vf_status_string", "vf_last_error", "vf_version"]
+           "vf_image_stats", "vf_image_stats_ex", "vf_status_string", "vf_last_error", "vf_version"]
+VF_STATS_NO_REF_NORM = 1
 
 
 class VFError(RuntimeError):
@@ -60,6 +61,7 @@ def load_library(path: str = LIB_PATH):
     L.vf_plan_launch.argtypes = [P, P]
     L.vf_plan_destroy.argtypes = [P]
     L.vf_image_stats.argtypes = [P, P, I, I, I, P, P]
+    L.vf_image_stats_ex.argtypes = [P, P, I, I, I, P, I, P]
     L.vf_status_string.argtypes = [I]
     L.vf_status_string.restype = ctypes.c_char_p
     L.vf_last_error.argtypes = []
@@ -67,7 +69,7 @@ def load_library(path: str = LIB_PATH):
     L.vf_version.argtypes = []
     for name in ("vf_filter", "vf_filter_batch", "vf_filter_batch_algo", "vf_filter_rows",
                  "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_destroy", "vf_image_stats",
-                 "vf_version"):
+                 "vf_image_stats_ex", "vf_version"):
         getattr(L, name).restype = I
     _lib = L
     return L
@@ -239,14 +241,20 @@ class Plan:
 
 
 def vf_image_stats(a: torch.Tensor, b: torch.Tensor, stats: Optional[torch.Tensor] = None,
-                   stream=None) -> torch.Tensor:
-    """Per-image [B, 8] float64 statistics (see include/vf.h)."""
+                   stream=None, ref_norm: bool = True) -> torch.Tensor:
+    """Per-image [B, 8] float64 statistics (see include/vf.h).  ref_norm=False
+    (vf_image_stats_ex, VF_STATS_NO_REF_NORM) skips column 4 (sum |a_Lab|,
+    a function of `a` alone), which is then 0."""
     L = load_library()
     x = a.unsqueeze(0) if a.dim() == 3 else a
     B, H, W, _ = x.shape
     if stats is None:
         stats = torch.empty((B, 8), dtype=torch.float64, device=a.device)
-    rc = L.vf_image_stats(_dev_u8(a, "a"), _dev_u8(b, "b"), B, H, W, stats.data_ptr(), _stream(stream))
+    if ref_norm:
+        rc = L.vf_image_stats(_dev_u8(a, "a"), _dev_u8(b, "b"), B, H, W, stats.data_ptr(), _stream(stream))
+    else:
+        rc = L.vf_image_stats_ex(_dev_u8(a, "a"), _dev_u8(b, "b"), B, H, W, stats.data_ptr(), VF_STATS_NO_REF_NORM,
+                                 _stream(stream))
     _check(rc, "vf_image_stats")
     return stats
 

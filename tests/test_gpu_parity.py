@@ -275,6 +275,29 @@ def test_image_stats_against_numpy_metrics():
         assert s[i, 5] == np.abs(a[i].astype(int) - b[i]).max()
 
 
+def test_image_stats_without_reference_norm():
+    """vf_image_stats_ex(VF_STATS_NO_REF_NORM): every column but 4 equals the
+    full statistics (bit-exact: same per-pixel fp32 values, same summation),
+    column 4 is 0; unknown flags are rejected."""
+    rng = np.random.default_rng(1)
+    a = rng.integers(0, 256, size=(3, 41, 37, 3)).astype(np.uint8)
+    b = a.copy()
+    m = rng.random(a.shape[:3]) < 0.3
+    b[m] = rng.integers(0, 256, size=(m.sum(), 3))
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    full = vfb.vf_image_stats(ta, tb).cpu().numpy()
+    part = vfb.vf_image_stats(ta, tb, ref_norm=False).cpu().numpy()
+    for k in (0, 1, 2, 5):
+        assert np.array_equal(full[:, k], part[:, k])
+    assert np.allclose(part[:, 3], full[:, 3], rtol=1e-6, atol=0)
+    assert np.all(part[:, 4] == 0) and np.all(full[:, 4] > 0)
+    from paper_1009_0959_b200 import vf as vfm
+    L = vfm.load_library()
+    st = torch.empty((3, 8), dtype=torch.float64, device="cuda")
+    rc = L.vf_image_stats_ex(ta.data_ptr(), tb.data_ptr(), 3, 41, 37, st.data_ptr(), 2, None)
+    assert rc == vfm.VF_EINVAL
+
+
 # ------------------------------------------------------------- full-size configs (sampled)
 def _sample_pixels(H, W, n, seed):
     rng = np.random.default_rng(seed)
