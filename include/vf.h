@@ -186,7 +186,7 @@ VF_API int vf_image_stats_ex(const uint8_t *a, const uint8_t *b, int B, int H, i
 VF_API const char *vf_status_string(int status);
 /* Text of the last error on the calling thread ("" if none). */
 VF_API const char *vf_last_error(void);
-/* ABI version (major*100 + minor): 101. */
+/* ABI version (major*100 + minor): 102 (102: vf_image_stats_ex). */
 VF_API int vf_version(void);
 
 #ifdef __cplusplus

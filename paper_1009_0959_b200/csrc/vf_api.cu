@@ -530,6 +530,6 @@ const char* vf_status_string(int status) {
 
 const char* vf_last_error(void) { return g_err; }
 
-int vf_version(void) { return 101; }
+int vf_version(void) { return 102; }
 
 }  // extern "C"
