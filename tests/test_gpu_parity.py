@@ -150,6 +150,27 @@ def test_tma_path_row_stripes():
     assert r.returncode == 0 and "tma stripes ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+def test_el_block_shapes_bit_identical():
+    """exp/log 3x3 large launches: the default 4-warp x 4-row blocks, the
+    8-warp blocks with 4 or 2 rows and 4-warp x 2-row blocks give bit-identical
+    outputs, indices and aggregates (child processes: the shape knobs are read
+    once per process)."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    import el_blocks_child
+    ref = el_blocks_child.digests()
+    child = os.path.join(here, "el_blocks_child.py")
+    for env in ({"VF_EL_TY": "8", "VF_EL_OPT": "4"}, {"VF_EL_TY": "8", "VF_EL_OPT": "2"},
+                {"VF_EL_TY": "4", "VF_EL_OPT": "2"}):
+        r = subprocess.run([sys.executable, child], env=dict(os.environ, **env), capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        got = dict(line.split() for line in r.stdout.strip().splitlines())
+        assert got == ref, (env, got, ref)
+
+
 @pytest.mark.parametrize("crit,var", CV)
 @pytest.mark.parametrize("w", [3, 5])
 def test_palette_ties_zero_vectors_branch_points(crit, var, w):
