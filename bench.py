@@ -26,6 +26,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -183,6 +185,41 @@ def ncu_traffic(key):
         return d.get("dram_bytes_per_launch", {}).get(key)
     except Exception:
         return None
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_oracle_breakdown(w, x_np, budget_s=1.0, combos=COMBOS):
+    """the oracle's Mpix/s per criterion x variant on all host
+    threads and, for the whole 7-filter set, on one thread (bounded samples)."""
+    import oracle
+    img = x_np[0]
+    npx = img.shape[0] * img.shape[1]
+    per = {}
+    for crit, var in combos:
+        t0 = time.perf_counter()
+        k = 0
+        while True:
+            oracle.filter_image(img, w, crit, var, want_index=False)
+            k += 1
+            if time.perf_counter() - t0 >= budget_s:
+                break
+        per[f"{crit}/{var}"] = k * npx / (time.perf_counter() - t0) / 1e6
+    # one thread: a row band of the image, all 7 filters once
+    band = np.ascontiguousarray(img[: max(w, min(img.shape[0], 64))])
+    t0 = time.perf_counter()
+    for crit, var in combos:
+        oracle.filter_image(band, w, crit, var, want_index=False, nthreads=1)
+    st = len(combos) * band.shape[0] * band.shape[1] / (time.perf_counter() - t0) / 1e6
+    return per, st
 
 
 def cpu_oracle_rate(spec, w, x_np, budget_s=12.0, combos=COMBOS):
@@ -680,8 +717,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         xs = x_np if spec.name in ("C1", "C2") else x_np[:1, :256]
         v, steps_done, dt, cores = cpu_oracle_rate(spec, w, xs)
+        per, single = cpu_oracle_breakdown(w, xs)
         cpu = {"value": v, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
-               "sample": f"{steps_done} x (7 filters over {xs.shape[0]}x{xs.shape[1]}x{xs.shape[2]} px), {dt:.1f} s"}
+               "sample": f"{steps_done} x (7 filters over {xs.shape[0]}x{xs.shape[1]}x{xs.shape[2]} px), {dt:.1f} s",
+               "cpu_model": cpu_model(), "per_filter_mpix_s": per, "single_thread_mpix_s": single}
 
     if rank == 0:
         line = {
