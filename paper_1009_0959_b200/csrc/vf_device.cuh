@@ -224,11 +224,6 @@ __device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
-__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
 __device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
   f32x2 d;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -337,117 +332,6 @@ __device__ __forceinline__ void angular_tau2_px2(uint32_t pk0, uint32_t pk1, f32
     v1 = 2.0f * asinf(tau1 * 0.70710678118654752f);
   } else {
     unpack2(horner4x2(coef::ASIN(), t), v0, v1);
-  }
-}
-
-// ---- chunk schedule of the packed accumulation (N = 2M + 1 samples) ----------
-// Aggregates are held as packed pairs A_g = (R_2g, R_2g+1), g < M, plus R_{N-1}.
-// The N(N-1)/2 pairs are grouped into chunks of two whose values V = (v0, v1)
-// land on whole packed pairs:
-//   AA(g,h): (2g,2h), (2g+1,2h+1)   A_g += V,  A_h += V
-//   AB(g,h): (2g,2h+1), (2g+1,2h)   A_g += V,  A_h += swap(V)
-//   W(g):    (2g,2g+1), (2g+2,2g+3) A_g += (v0,v0), A_{g+1} += (v1,v1)
-//   S(g):    (2g,N-1), (2g+1,N-1)   A_g += V,  R_{N-1} += v0, += v1
-// (M(M-1) + M/2 + M chunks: 18 for N = 9, 150 for N = 25; M must be even).
-enum { CH_AA = 0, CH_AB = 1, CH_W = 2, CH_S = 3 };
-template <int N>
-struct ChunkPlan {
-  static constexpr int M = (N - 1) / 2;
-  static constexpr int NC = M * (M - 1) + M / 2 + M;
-  static_assert(M % 2 == 0 && 2 * NC == N * (N - 1) / 2, "chunk plan must cover every pair once");
-  // chunk c -> (kind, g, h).  The M(M-1) cross-group chunks run in rounds of
-  // a round-robin schedule (circle method): a round holds M/2 disjoint group
-  // pairs, first their AA chunks, then their AB chunks, so consecutive
-  // chunks update different packed aggregates (independent dependency chains).
-  __host__ __device__ static constexpr int kind(int c) {
-    return c < M * (M - 1) ? ((c % M) < M / 2 ? CH_AA : CH_AB) : (c < M * (M - 1) + M / 2 ? CH_W : CH_S);
-  }
-  __host__ __device__ static constexpr int gh(int c, bool want_h) {   // group pair of cross chunk c
-    const int r = c / M, k = (c % M) % (M / 2);
-    const int a = k == 0 ? r : (r + k) % (M - 1);
-    const int b = k == 0 ? M - 1 : (r - k + (M - 1)) % (M - 1);
-    return want_h ? (a > b ? a : b) : (a < b ? a : b);
-  }
-  __host__ __device__ static constexpr int g(int c) {
-    return c < M * (M - 1) ? gh(c, false) : (c < M * (M - 1) + M / 2 ? 2 * (c - M * (M - 1)) : c - M * (M - 1) - M / 2);
-  }
-  __host__ __device__ static constexpr int h(int c) {
-    return c < M * (M - 1) ? gh(c, true) : (c < M * (M - 1) + M / 2 ? g(c) + 1 : M);
-  }
-  __host__ __device__ static constexpr int i0(int c) { return kind(c) == CH_S ? 2 * g(c) : 2 * g(c); }
-  __host__ __device__ static constexpr int j0(int c) {
-    return kind(c) == CH_AA ? 2 * h(c) : kind(c) == CH_AB ? 2 * h(c) + 1 : kind(c) == CH_W ? 2 * g(c) + 1 : N - 1;
-  }
-  __host__ __device__ static constexpr int i1(int c) { return kind(c) == CH_W ? 2 * h(c) : 2 * g(c) + 1; }
-  __host__ __device__ static constexpr int j1(int c) {
-    return kind(c) == CH_AA ? 2 * h(c) + 1 : kind(c) == CH_AB ? 2 * h(c) : kind(c) == CH_W ? 2 * h(c) + 1 : N - 1;
-  }
-};
-
-__device__ __forceinline__ f32x2 swap2(f32x2 v) {
-  float lo, hi;
-  unpack2(v, lo, hi);
-  return pack2(hi, lo);   // folded into the consumer's LO_HI operand form
-}
-__device__ __forceinline__ f32x2 bcast_lo(f32x2 v) {
-  float lo, hi;
-  unpack2(v, lo, hi);
-  return pack2(lo, lo);   // .F32 broadcast operand
-}
-__device__ __forceinline__ f32x2 bcast_hi(f32x2 v) {
-  float lo, hi;
-  unpack2(v, lo, hi);
-  return pack2(hi, hi);
-}
-
-// One chunk (kind KIND) of the packed accumulation: zu2 = the two scaled
-// arguments; Ag / Ah = the chunk's packed aggregates (Ah unused for CH_S),
-// Rl = R_{N-1}.  Per element the roundings are those of crit_accumulate.
-template <int CRIT, int VAR, int KIND>
-__device__ __forceinline__ void crit_chunk(f32x2 zu2, f32x2& Ag, f32x2& Ah, float& Rl) {
-  if constexpr (VAR == MINIMAX) {
-    // exp: Delta(z) / Q(z);  log: -Ntilde(u) / Qtilde(u)
-    const f32x2 n2 = CRIT == EXPC ? horner4x2(coef::EXP_DELTA(), zu2) : horner4x2(coef::ENT_NEGN_U(), zu2);
-    float q0, q1;
-    unpack2(CRIT == EXPC ? horner4x2(coef::EXP_Q(), zu2) : horner4x2(coef::ENT_Q_U(), zu2), q0, q1);
-    const f32x2 r2 = pack2(rcp_approx(q0), rcp_approx(q1));
-    if constexpr (KIND == CH_AA) {
-      Ag = fma2(n2, r2, Ag);
-      Ah = fma2(n2, r2, Ah);
-    } else if constexpr (KIND == CH_AB) {
-      Ag = fma2(n2, r2, Ag);
-      Ah = fma2(swap2(n2), swap2(r2), Ah);
-    } else if constexpr (KIND == CH_W) {
-      Ag = fma2(bcast_lo(n2), bcast_lo(r2), Ag);
-      Ah = fma2(bcast_hi(n2), bcast_hi(r2), Ah);
-    } else {
-      float n0, n1, r0, r1;
-      unpack2(n2, n0, n1);
-      unpack2(r2, r0, r1);
-      Ag = fma2(n2, r2, Ag);
-      Rl = fmaf(n0, r0, Rl);
-      Rl = fmaf(n1, r1, Rl);
-    }
-  } else {
-    static_assert(VAR == REACH || VAR == POLY4, "packed chunks: polynomial and rational variants only");
-    const f32x2 v2 = VAR == POLY4 ? horner4x2(coef::EXP_1MP4(), zu2)
-                                  : (CRIT == EXPC ? horner_rec2<coef::R_EXP, 0>(zu2) : horner_rec2<coef::R_LOG, 0>(zu2));
-    if constexpr (KIND == CH_AA) {
-      Ag = add2(Ag, v2);
-      Ah = add2(Ah, v2);
-    } else if constexpr (KIND == CH_AB) {
-      Ag = add2(Ag, v2);
-      Ah = add2(Ah, swap2(v2));
-    } else if constexpr (KIND == CH_W) {
-      Ag = add2(Ag, bcast_lo(v2));
-      Ah = add2(Ah, bcast_hi(v2));
-    } else {
-      float v0, v1;
-      unpack2(v2, v0, v1);
-      Ag = add2(Ag, v2);
-      Rl = __fadd_rn(Rl, v0);
-      Rl = __fadd_rn(Rl, v1);
-    }
   }
 }
 

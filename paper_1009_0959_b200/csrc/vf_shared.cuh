@@ -33,9 +33,6 @@
 
 #include "vf_window.cuh"
 
-#ifndef SHARED_PACKED_C
-#define SHARED_PACKED_C 0    // 1: phase C of two outputs per thread in packed FP32 (FADD2; measured slower, DESIGN 5.3.2)
-#endif
 #ifndef SHARED_REC8
 #define SHARED_REC8 1        // 8-byte neighbour records (packed RGB0, |x|^2): half the phase-A smem wavefronts, s = sqrt(Ph) by MUFU
 #endif
@@ -146,8 +143,7 @@ template <int WIN, int VAR, int GD, int OPT, int CFG, int G>
 __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint32_t (&my_pk)[shared::cfg_ppt(CFG)],
                                              const float (&my_nn)[shared::cfg_ppt(CFG)],
                                              const float (&my_nrm)[shared::cfg_ppt(CFG)],
-                                             float (&Ra)[OPT][WIN * WIN], f32x2 (&Rp)[WIN * WIN], int tid,
-                                             bool blk_zero) {
+                                             float (&Ra)[OPT][WIN * WIN], int tid, bool blk_zero) {
   using namespace shared;
   constexpr int PPT = cfg_ppt(CFG);
   constexpr int NT = cfg_nt(CFG);
@@ -329,26 +325,6 @@ __device__ __forceinline__ void shared_group(SharedSmem<GD, CFG>& sm, const uint
         }
       }
     }
-  } else if constexpr (OPT == 2 && SHARED_PACKED_C) {
-    const int oy1 = ty + NW;
-    if (tx < TW) {
-      const int base0 = ty * PW + tx;
-      const int base1 = (TH % NW == 0 || oy1 < TH) ? oy1 * PW + tx : base0;
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-#pragma unroll
-        for (int j = i + 1; j < N; ++j) {
-          const int d = delta_index(R, j / WIN - i / WIN, j % WIN - i % WIN);
-          if (d / GD == G) {
-            const int oi = (i / WIN) * PW + (i % WIN);
-            VF_CHECK(base1 + oi < region_np(CFG) && base0 + oi < region_np(CFG));
-            const f32x2 v = pack2(sm.M[d - G * GD][base0 + oi], sm.M[d - G * GD][base1 + oi]);
-            Rp[i] = add2(Rp[i], v);
-            Rp[j] = add2(Rp[j], v);
-          }
-        }
-      }
-    }
   } else {
   // Rows past the output tile (TH not a multiple of 8) are skipped warp-
   // uniformly; the aggregates start at -0 inside the branch so that the first
@@ -381,8 +357,8 @@ __device__ __forceinline__ void shared_groups(std::integer_sequence<int, Gs...>,
                                               const uint32_t (&my_pk)[shared::cfg_ppt(CFG)],
                                               const float (&my_nn)[shared::cfg_ppt(CFG)],
                                               const float (&my_nrm)[shared::cfg_ppt(CFG)], float (&Ra)[OPT][WIN * WIN],
-                                              f32x2 (&Rp)[WIN * WIN], int tid, bool blk_zero) {
-  (shared_group<WIN, VAR, GD, OPT, CFG, Gs>(sm, my_pk, my_nn, my_nrm, Ra, Rp, tid, blk_zero), ...);
+                                              int tid, bool blk_zero) {
+  (shared_group<WIN, VAR, GD, OPT, CFG, Gs>(sm, my_pk, my_nn, my_nrm, Ra, tid, blk_zero), ...);
 }
 
 // Resident blocks per SM the register allocation is held to.
@@ -461,16 +437,8 @@ __global__ void __launch_bounds__(shared::cfg_nt(CFG), shared_min_blocks(WIN, CF
   for (int k = 0; k < OPT; ++k)
 #pragma unroll
     for (int i = 0; i < N; ++i) Ra[k][i] = -0.0f;
-  f32x2 Rp[N];   // packed (row ty, row ty + NW) aggregates (OPT == 2, SHARED_PACKED_C)
-#pragma unroll
-  for (int i = 0; i < N; ++i) Rp[i] = pack2(-0.0f, -0.0f);
-
-  shared_groups<WIN, VAR, GD, OPT, CFG>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, Ra, Rp, tid,
+  shared_groups<WIN, VAR, GD, OPT, CFG>(std::make_integer_sequence<int, NG>{}, sm, my_pk, my_nn, my_nrm, Ra, tid,
                                         blk_zero);
-  if constexpr (OPT == 2 && SHARED_PACKED_C) {
-#pragma unroll
-    for (int i = 0; i < N; ++i) unpack2(Rp[i], Ra[0][i], Ra[1][i]);
-  }
 
   // ---- argmin + store ------------------------------------------------------------------
 #pragma unroll

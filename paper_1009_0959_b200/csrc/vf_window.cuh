@@ -18,10 +18,6 @@
 
 #include "vf_device.cuh"
 
-#ifndef EL_PACKED_ACC
-#define EL_PACKED_ACC 0   // 1: exp/log polynomial variants accumulate into packed aggregates (ChunkPlan; measured slower, DESIGN 5.3.2)
-#endif
-
 namespace vf {
 
 constexpr int TX = 32;   // output tile width  (one warp per tile row)
@@ -207,9 +203,10 @@ __device__ __forceinline__ void el_window_s1(const Launch& L, int b, int ox, int
       const float zu = fmaf(sc, fb, bias);                               // c * d1, one rounding
       crit_accumulate<CRIT, VAR>(zu, Ra[i], Ra[j]);
     });
-  } else if constexpr (!EL_PACKED_ACC) {
+  } else {
     // polynomial variants: pairs 2q and 2q + 1 together in packed FP32
-    // (FFMA2), one Horner chain issue for both, scalar accumulation
+    // (FFMA2), one Horner chain issue for both, scalar accumulation (packed
+    // aggregates were measured slower)
     const f32x2 sc2 = pack2(sc, sc), bias2 = pack2(bias, bias);
     static_for<N * (N - 1) / 4>([&](auto qc) {
       constexpr int p0 = 2 * decltype(qc)::value, p1 = p0 + 1;
@@ -218,34 +215,6 @@ __device__ __forceinline__ void el_window_s1(const Launch& L, int b, int ox, int
                               __uint_as_float(sad4(w[i1], w[j1], F2P23_BITS)));   // 2^23 + d1, two pairs
       crit_accumulate2<CRIT, VAR>(fma2(sc2, fb2, bias2), Ra[i0], Ra[j0], Ra[i1], Ra[j1]);
     });
-  } else {
-    // polynomial variants in packed FP32 (FFMA2): two pairs per Horner chain
-    // issue, and the aggregates held as packed pairs A_g = (R_2g, R_2g+1), so
-    // that one FADD2 / FFMA2 (with its free LO_HI swap and .F32 broadcast
-    // operand forms) adds a chunk's two values to two aggregates: ~1 instead of
-    // 2 accumulating instructions per pair.  Every aggregate receives the same
-    // values with the same per-element rounding as crit_accumulate; only the
-    // (fixed, compile-time) order of the additions differs from the raster
-    // order.  Flat windows: every aggregate adds the same value N - 1 times,
-    // so all tie exactly and the lowest index wins.
-    constexpr int M = (N - 1) / 2;
-    const f32x2 sc2 = pack2(sc, sc), bias2 = pack2(bias, bias);
-    f32x2 A[M];
-#pragma unroll
-    for (int g = 0; g < M; ++g) A[g] = pack2(-0.0f, -0.0f);   // -0 + v == v: the first add folds away
-    float Rl = -0.0f;                                        // R_{N-1}
-    static_for<ChunkPlan<N>::NC>([&](auto kc) {
-      using plan = ChunkPlan<N>;
-      constexpr int c = decltype(kc)::value;
-      constexpr int i0 = plan::i0(c), j0 = plan::j0(c), i1 = plan::i1(c), j1 = plan::j1(c);
-      constexpr int kind = plan::kind(c), g = plan::g(c), h = plan::h(c);
-      const f32x2 fb2 = pack2(__uint_as_float(sad4(w[i0], w[j0], F2P23_BITS)),
-                              __uint_as_float(sad4(w[i1], w[j1], F2P23_BITS)));   // 2^23 + d1, two pairs
-      crit_chunk<CRIT, VAR, kind>(fma2(sc2, fb2, bias2), A[g], A[h < M ? h : g], Rl);
-    });
-#pragma unroll
-    for (int g = 0; g < M; ++g) unpack2(A[g], Ra[2 * g], Ra[2 * g + 1]);
-    Ra[N - 1] = Rl;
   }
   float bv = Ra[0];
   uint32_t o = w[0];
