@@ -52,5 +52,14 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     return target
 
 
+def build_all(verbose: bool = False) -> None:
+    """libvf.so and libvf_debug.so, compiled concurrently (one nvcc each)."""
+    import concurrent.futures as cf
+    with cf.ThreadPoolExecutor(2) as ex:
+        futs = [ex.submit(build, True, verbose, False), ex.submit(build, True, False, True)]
+        for f in futs:
+            f.result()
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))
