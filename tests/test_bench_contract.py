@@ -33,3 +33,27 @@ def test_reference_arm_other_ranks_exit_quietly():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
                         "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == "", (r.stdout, r.stderr[-1000:])
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_gpu_arm_json_line():
+    """Our arm on the GPU (short run): one JSON line with roofline, clocks,
+    gpu_launches and an end-to-end figure that moved host bytes."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3",
+                        "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert KEYS <= set(d), KEYS - set(d)
+    assert d["dtype"] == "f32" and d["scaling"] == "weak" and d["gpu_launches"] == 7 * 3
+    rf = d["roofline"]
+    assert rf["bound"] == "alu" and 0 < rf["frac"] < 1.5 and rf["unit"] == "TFLOP/s" and rf["peak"] > 70
+    assert d["e2e"]["h2d_bytes_per_step"] == 512 * 512 * 3 and d["e2e"]["d2h_bytes_per_step"] == 7 * 512 * 512 * 3
+    assert d["e2e"]["outputs_match_device_path"] is True
+    assert d["clocks"]["sm_mhz"] is None or d["clocks"]["sm_mhz"] > 0
+    for k, v in d["per_kernel"].items():
+        assert v["ms"] > 0 and v["ms_isolated"] > 0, k
