@@ -411,6 +411,8 @@ def run_partitioned(args):
 PAPER_FILTERS = [("amnfe", "exact"), ("amnfe", "minimax"), ("amnfe", "poly4"), ("amnfg", "exact"),
                  ("amnfg", "minimax"), ("evmf", "exact"), ("evmf", "minimax")]
 PAPER_TIME_PCT = {"BVDF": 1371.314, "AMNFE": 143.496, "EVMF": 236.105}   # Table 5, correlated 10%
+# Fig. 5: one 512x512 image, 10% noise, Pentium D 2.66 GHz, gcc 3.4.4, single thread, seconds
+PAPER_FIG5_S = {"BVDF": (10.360, 0.688), "AMNFE": (0.594, 0.422), "EVMF": (0.594, 0.250)}
 
 
 def steady_kernel_ms(vfb, torch, dev, stream, flush, x, w, combos, outs, reps=3):
@@ -711,6 +713,11 @@ def main():
                          ("AMNFE", pk["amnfe/exact"]["ms"], pk["amnfe/minimax"]["ms"]),
                          ("EVMF", pk["evmf/exact"]["ms"], pk["evmf/minimax"]["ms"])):
         paper["time_pct"][name] = {"b200": 100.0 * te / ta, "paper_pentium_d": PAPER_TIME_PCT[name]}
+        if spec.name == "C2":   # same image size as Fig. 5: per-image times side by side (context, not a target)
+            pe, pa = PAPER_FIG5_S[name]
+            paper.setdefault("fig5_context", {})[name] = {
+                "paper_exact_s": pe, "paper_approx_s": pa, "b200_exact_s": te / 1e3, "b200_approx_s": ta / 1e3,
+                "hardware": "paper: Pentium D 2.66 GHz, 1 thread (P:295); b200: one kernel launch (per_kernel timing)"}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
