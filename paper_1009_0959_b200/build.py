@@ -35,8 +35,16 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
+# Per-translation-unit extra flags (ptxas's register-usage
+# level 2 helps the 3x3 exp/log non-libm kernels, hurts the libm ones).
+SOURCE_FLAGS = {"vf_el_ty4.cu": ["-Xptxas", "--register-usage-level=2"]}
+
+
 def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
-    """debug=True builds libvf_debug.so with the VF_CHECK device bounds checks."""
+    """debug=True builds libvf_debug.so with the VF_CHECK device bounds checks.
+    Each .cu is compiled to an object with its own flags (concurrently), then
+    linked into the shared library."""
+    import tempfile
     target = LIB_DEBUG if debug else LIB
     if not force and not debug and up_to_date():
         return LIB
@@ -44,10 +52,21 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
         nvcc = "/usr/local/cuda/bin/nvcc" if nvcc == "nvcc" and subprocess.call(
             ["which", "nvcc"], stdout=subprocess.DEVNULL) != 0 else nvcc
-    tmp = target + ".tmp%d" % os.getpid()
-    cmd = [nvcc] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + (["-DVF_DEBUG"] if debug else []) + \
-        ["-o", tmp] + sources()
-    subprocess.run(cmd, check=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + (["-Xptxas", "-v"] if verbose else []) + \
+        (["-DVF_DEBUG"] if debug else [])
+    with tempfile.TemporaryDirectory(prefix="vfbuild") as tmpd:
+        procs, objs = [], []
+        for src in sources():
+            obj = os.path.join(tmpd, os.path.basename(src) + ".o")
+            cmd = [nvcc] + compile_flags + SOURCE_FLAGS.get(os.path.basename(src), []) + ["-c", "-o", obj, src]
+            procs.append((subprocess.Popen(cmd), cmd))
+            objs.append(obj)
+        rcs = [(p.wait(), cmd) for p, cmd in procs]   # all finished before the directory goes away
+        for rc, cmd in rcs:
+            if rc != 0:
+                raise subprocess.CalledProcessError(rc, cmd)
+        tmp = target + ".tmp%d" % os.getpid()
+        subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs, check=True)
     os.replace(tmp, target)
     return target
 

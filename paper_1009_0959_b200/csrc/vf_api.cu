@@ -23,6 +23,11 @@
 #include "vf_tma.cuh"
 #include "vf_window.cuh"
 
+namespace vf {
+// vf_el_ty4.cu (its own translation unit and ptxas setting)
+const void* el_kernel_ty4(int opt, int crit, int var);
+}  // namespace vf
+
 namespace {
 
 thread_local char g_err[512] = "";
@@ -121,21 +126,6 @@ const void* el_kernel(int crit, int var) {
   }
   if (var == REACH) return (const void*)vf_el_kernel<WIN, LOGC, REACH, OPT>;
   return var == EXACT ? (const void*)vf_el_kernel<WIN, LOGC, EXACT, OPT> : (const void*)vf_el_kernel<WIN, LOGC, MINIMAX, OPT>;
-}
-
-// 3x3 polynomial / rational variants with NTY-warp blocks
-template <int OPT, int NTY>
-const void* el_kernel_ty(int crit, int var) {
-  using namespace vf;
-  if (crit == EXPC) {
-    if (var == MINIMAX) return (const void*)vf_el_kernel<3, EXPC, MINIMAX, OPT, NTY>;
-    if (var == REACH) return (const void*)vf_el_kernel<3, EXPC, REACH, OPT, NTY>;
-    if (var == POLY4) return (const void*)vf_el_kernel<3, EXPC, POLY4, OPT, NTY>;
-    return nullptr;
-  }
-  if (var == REACH) return (const void*)vf_el_kernel<3, LOGC, REACH, OPT, NTY>;
-  if (var == MINIMAX) return (const void*)vf_el_kernel<3, LOGC, MINIMAX, OPT, NTY>;
-  return nullptr;
 }
 
 template <int WIN, int OPT>
@@ -298,7 +288,8 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
       static const int ty_env = [] { const char* e = std::getenv("VF_EL_TY"); return e ? std::atoi(e) : 0; }();
       if (window == 3 && (ty_env == 4 || ty_env == vf::TY)) nty = ty_env;
       if (window == 3 && nty == 4 && opt >= 2 && var != VF_EXACT) {
-        kd->fn = opt == 4 ? el_kernel_ty<4, 4>(crit, var) : el_kernel_ty<2, 4>(crit, var);
+        kd->fn = vf::el_kernel_ty4(opt, crit, var);
+        if (!kd->fn) return fail(VF_EINVAL, "no 4-warp kernel for this variant");
         th = 4 * opt;
         kd->grid = dim3((W + vf::TX - 1) / vf::TX, (out_rows + th - 1) / th, B);
         kd->block = dim3(vf::TX, 4);
