@@ -37,7 +37,8 @@ def up_to_date() -> bool:
 
 # Per-translation-unit extra flags (ptxas's register-usage
 # level 2 helps the 3x3 exp/log non-libm kernels, hurts the libm ones).
-SOURCE_FLAGS = {"vf_el_ty4.cu": ["-Xptxas", "--register-usage-level=2"]}
+SOURCE_FLAGS = {"vf_el_ty4.cu": ["-Xptxas", "--register-usage-level=2"],
+                "vf_ang_mm.cu": ["-Xptxas", "--register-usage-level=2"]}
 
 
 def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:

@@ -15,6 +15,7 @@
 #include <new>
 #include <vector>
 
+#define VF_ANGULAR_MM_EXTERN   // angular minimax kernels: vf_ang_mm.cu
 #include "../../include/vf.h"
 #include "vf_paper.cuh"
 #include "vf_role.cuh"

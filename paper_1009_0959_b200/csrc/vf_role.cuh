@@ -341,11 +341,20 @@ __global__ void __launch_bounds__(NT, role_min_blocks(WIN, NT)) vf_angular_role_
 // threads with 1..3 pixels each; cfg 4 (default) = 384 threads with 2 pixels
 // each: the same 32 x 24 region as cfg 3 with two thirds of the role
 // accumulators per thread, so more warps fit per SM (5x5: 24 instead of 16).
+#ifndef VF_ANGULAR_MM_TU   // kernel selection: vf_api.cu only (vf_ang_mm.cu instantiates the minimax kernels itself)
+#ifdef VF_ANGULAR_MM_EXTERN
+const void* role_kernel_fn_mm(int window, int cfg);
+#endif
 template <int WIN, int CFG>
 inline const void* role_kernel_fn_t(int var) {
   constexpr int NT = shared::cfg_nt(CFG), PPT = shared::cfg_ppt(CFG);
+#ifdef VF_ANGULAR_MM_EXTERN
+  if (var != EXACT) return role_kernel_fn_mm(WIN, CFG);   // vf_ang_mm.cu
+  return (const void*)vf_angular_role_kernel<WIN, EXACT, NT, PPT>;
+#else
   return var == EXACT ? (const void*)vf_angular_role_kernel<WIN, EXACT, NT, PPT>
                       : (const void*)vf_angular_role_kernel<WIN, MINIMAX, NT, PPT>;
+#endif
 }
 template <int WIN>
 inline const void* role_kernel_fn_w(int var, int cfg) {
@@ -382,5 +391,7 @@ inline cudaError_t role_set_attributes() {
       }
   return cudaSuccess;
 }
+
+#endif  // VF_ANGULAR_MM_TU
 
 }  // namespace vf

@@ -464,10 +464,22 @@ __global__ void __launch_bounds__(shared::cfg_nt(CFG), shared_min_blocks(WIN, CF
 
 // Kernel + grid of the pair-sharing kernel for a launch (see vf_api.cu);
 // cfg = launch configuration (shared::cfg_nt / cfg_ppt).
+// VF_ANGULAR_MM_EXTERN (vf_api.cu): the minimax kernels are instantiated in
+// their own translation unit (vf_ang_mm.cu, own ptxas setting) and fetched
+// from there; only the exact ones are instantiated here.
+#ifndef VF_ANGULAR_MM_TU   // kernel selection: vf_api.cu only (vf_ang_mm.cu instantiates the minimax kernels itself)
+#ifdef VF_ANGULAR_MM_EXTERN
+const void* shared_kernel_fn_mm(int window, int cfg);
+#endif
 template <int WIN, int CFG>
 inline const void* shared_kernel_fn_t(int var) {
+#ifdef VF_ANGULAR_MM_EXTERN
+  if (var != EXACT) return shared_kernel_fn_mm(WIN, CFG);
+  return (const void*)vf_angular_shared_kernel<WIN, EXACT, CFG>;
+#else
   return var == EXACT ? (const void*)vf_angular_shared_kernel<WIN, EXACT, CFG>
                       : (const void*)vf_angular_shared_kernel<WIN, MINIMAX, CFG>;
+#endif
 }
 
 template <int WIN>
@@ -516,5 +528,7 @@ inline dim3 shared_grid(const Launch& L, int B, int window, int cfg) {
   const int TW = PW - 2 * R, TH = region_h(cfg) - 2 * R;
   return dim3((L.W + TW - 1) / TW, (L.out_rows + TH - 1) / TH, B);
 }
+
+#endif  // VF_ANGULAR_MM_TU
 
 }  // namespace vf
