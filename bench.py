@@ -2,23 +2,40 @@
 """Benchmark of the hot path (BASELINE.json metric: Mpixels/s per criterion,
 exact vs minimax, 3x3/5x5, % of the FP32 FMA roofline).
 
-One STEP = one synthetic image of the chosen config (default C2 = configs[1]:
-512x512, 3x3 window, 10% correlated impulse noise) filtered by all seven
-criterion x variant kernels (angular/exp/log x exact/minimax + exp poly4).
-Inputs are resident in HBM before the timed region; L2 is flushed (a 512 MiB
-write) between timed steps, outside the per-step CUDA-event windows.
+Default workload = BASELINE config 3 (C4): a batch of 1024
+synthetic 512x768 uint8 RGB images (uncorrelated impulse noise, p per image
+from {5,10,20,30}%), 3x3 window.  One STEP filters the rank's shard of the
+batch with all seven criterion x variant filters (angular/exp/log x
+exact/minimax + exp poly4; one CUDA graph of 7 concurrent kernels), compares
+the six others with the angular exact output in ONE fused statistics pass
+(vf_image_stats_multi) and all_gathers the per-image statistics over NCCL
+(the only collective of the batch path).  N GPUs split the
+1024 images (strong scaling: the total work is the config's).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c2|c5] [--impl ours|reference]
 
-N > 1 runs under torch.distributed.run: each rank filters its own image
-(image id = rank), no collective on the data path (weak scaling); the
-reported time is the max over ranks.  Rank 0 prints ONE JSON line.
+Rank 0 prints ONE JSON line; besides the contract keys it carries
+  per_kernel   each filter kernel over the whole local batch (3x3): average
+               launch duration, Mpix/s, FP32 fraction with SURVEY.md 8(d) D4
+               algorithmic flops (exact variants: the arithmetic around ONE
+               libm call, no flop target), SFU fraction, and for the angular
+               pair-sharing kernels the evaluated-pairs-only fraction; plus
+               ncu pipe utilisations when profiles/ncu_exec.json was captured
+               from this very libvf.so (sha256 match);
+  c3           the same per-kernel block for BASELINE config 2 (C3, 8 x
+               2048^2, 5x5) at N = 1;
+  roofline     the step's dominant kernel (largest average launch duration);
+  roofline_minimax  the paper's headline filter (BVDF: angular minimax, 3x3)
+               against the 60% target, with every minimax kernel's fraction;
+  e2e          the same metric through the public API with HOST buffers
+               (vf_plan_create(h_in, h_outs): H2D + 7 kernels + 7 D2H);
+  cpu_baseline the oracle (rank 0, N = 1) timed exactly like the reference arm.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -36,64 +53,114 @@ COMBOS = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp"
 # the re-derived reachable-interval polynomials (VF_MINIMAX_REACH),
 # timed per kernel beside the paper's variants (not part of the 7-filter step)
 REACH_COMBOS = [("exp", "reach"), ("log", "reach")]
+REFERENCE = ("angular", "exact")
 
-# Algorithmic FP32 flops per pair (SURVEY.md 8(d) D4 counting rules: FMA = 2,
-# add/sub/mul = 1; robustness overhead not counted).  Exact variants: the
-# method's arithmetic around the libm call plus the FP32 flops of CUDA's libm
-# routine itself as compiled for sm_100a.
+# algorithmic FP32 flops per pair (FMA = 2, add/sub/mul = 1;
+# abs/neg/compare/select = 0; robustness overhead not counted).  Exact
+# variants: the method's arithmetic around ONE libm call (the call itself is
+# not a flop count: "report Mpx/s plus FMA and SFU pipe %, no target").
 FLOPS_PER_PAIR = {
     ("angular", "minimax"): 18, ("exp", "minimax"): 26, ("exp", "poly4"): 18, ("log", "minimax"): 26,
-    ("angular", "exact"): 10 + 23, ("exp", "exact"): 10 + 24, ("log", "exact"): 11 + 28,
+    ("angular", "exact"): 10, ("exp", "exact"): 10, ("log", "exact"): 11,
     # f4 reach: L1 5 + S1 1 + scale 1 + Horner-5 / Horner-7 (10 / 14) + accumulate 2
     ("exp", "reach"): 19, ("log", "reach"): 23,
 }
-NOMINAL_FP32_TFLOPS_AT_MAX = 2 * 128 * 148 * 1.965e9 / 1e12   # 74.4
-METRIC = ("filtered Mpixels/s (7 criterion x variant filters per pixel; per-kernel Mpix/s and % of FP32 roofline "
-          "in per_kernel)")
-
-
-def workload_config(spec, B, H, W, w, world):
-    """The `config` object both arms report for the same workload."""
-    return {"workload": f"{spec.name}: {B}x{H}x{W} uint8 RGB, {w}x{w} window, "
-                        f"{spec.noise} impulse noise, all 7 criterion/variant filters per step",
-            "per_rank_pixels": B * H * W, "l2": "flushed between steps (512 MiB write, untimed)",
-            "parallelism": f"dp{world} (independent images per rank)"}
+# D4 SFU (MUFU) operations per pair: the angular criterion's sqrt (Eqs. 6-7),
+# the rationals' reciprocal; the polynomial variants none; exact exp/log none
+# besides the libm call.
+SFU_PER_PAIR = {("angular", "minimax"): 1, ("angular", "exact"): 1, ("exp", "minimax"): 1, ("log", "minimax"): 1,
+                ("exp", "poly4"): 0, ("exp", "exact"): 0, ("log", "exact"): 0, ("exp", "reach"): 0,
+                ("log", "reach"): 0}
+LIBM_CALLS_PER_PAIR = {c: (1 if c[1] == "exact" else 0) for c in FLOPS_PER_PAIR}
+# pair evaluations per pixel of the angular pair-sharing kernels
+ANGULAR_EVALS_PER_PX = {3: 12, 5: 40}
+METRIC = ("filtered Mpixels/s (7 criterion x variant filters per pixel; per-kernel Mpix/s and % of the FP32 "
+          "roofline in per_kernel / c3)")
+SM_MAX_MHZ_DEFAULT = 1965.0
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c2", "c5"],
+                    help="c4 (default): BASELINE config 3, 1024 x 512x768 batch sharded over the ranks; "
+                         "c2: config 1, one 512x512 image per rank (weak scaling); "
+                         "c5: config 4, one 4320x7680 image in row stripes (angular minimax, 3x3 and 5x5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--mode", default="step", choices=["step", "shard", "stripes"],
-                    help="step: 7 filters of one image per rank (default, weak scaling); shard: BASELINE config 3 "
-                         "(C4, 1024 x 512x768 batch sharded over ranks, stats all_gather); stripes: config 4 (C5, "
-                         "4320x7680 image in row stripes with halo, outputs gathered)")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 (5x5) per-kernel section")
+    ap.add_argument("--no-paper", action="store_true", help="skip the AMNF/EVMF section (C2 image)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--images", type=int, default=0, help="(testing) use only the first N images of the batch")
     return ap.parse_args()
 
 
-# ------------------------------------------------------------------ workload
-def workload(cfg):
+# ------------------------------------------------------------------ workloads
+def workload_spec(name):
     import vfsynth
-    spec = vfsynth.config(cfg)
-    w = spec.window[-1] if cfg == "C3" else spec.window[0]
-    return spec, w
+    return vfsynth.config({"c4": "C4", "c2": "C2", "c5": "C5"}[name])
 
 
-def make_input(spec, rank):
-    """This rank's input: one image of the config (C3: the batch of 8 images;
-    C4: a 16-image slice of the 1024-image batch)."""
-    import numpy as np
+def workload_config(args, spec, world):
+    B = args.images or spec.batch
+    if args.workload == "c4":
+        w = f"C4: {B} x {spec.H}x{spec.W} uint8 RGB batch sharded over {world} rank(s), 3x3 window, " \
+            f"uncorrelated impulse noise p in {{5,10,20,30}}%, all 7 criterion/variant filters per step + fused " \
+            f"per-image stats vs angular/exact + NCCL all_gather of the stats"
+        return {"workload": w, "images": B, "H": spec.H, "W": spec.W, "window": 3,
+                "parallelism": f"dp{world} (batch shards)",
+                "l2": "inputs larger than L2 (no flush): %d MiB per rank per step" % ((B // world) * spec.H * spec.W * 3 >> 20)}
+    if args.workload == "c2":
+        return {"workload": f"C2: one {spec.H}x{spec.W} uint8 RGB image per rank, 3x3 window, correlated 10% impulse "
+                            "noise, all 7 criterion/variant filters per step + fused stats",
+                "images": world, "H": spec.H, "W": spec.W, "window": 3, "parallelism": f"dp{world} (one image per rank)",
+                "l2": "flushed between steps (512 MiB write, untimed)"}
+    return {"workload": f"C5: one {spec.H}x{spec.W} uint8 RGB image in {world} row stripe(s) with halo, angular "
+                        "minimax, 3x3 and 5x5, chunked output all_gather (NCCL) overlapping the filtering",
+            "images": 1, "H": spec.H, "W": spec.W, "window": "3 and 5", "parallelism": f"stripes{world}",
+            "l2": "flushed between steps (512 MiB write, untimed)"}
+
+
+def local_ids(args, spec, world, rank):
+    from paper_1009_0959_b200 import parallel as par
+    if args.workload == "c2":
+        return [rank]
+    B = args.images or spec.batch
+    lo, hi = par.shard_range(B, world, rank)
+    return list(range(lo, hi))
+
+
+def _gen_images(args_):
     import vfsynth
-    if spec.name == "C3":
-        return vfsynth.make_batch(spec)
-    if spec.name == "C4":
-        return vfsynth.make_batch(spec, ids=range(rank * 16, rank * 16 + 16))
-    return vfsynth.make_image(spec, rank % max(spec.batch, 1) if spec.batch > 1 else rank)[1][None]
+    name, ids = args_
+    return vfsynth.make_batch(vfsynth.config(name), ids=ids)
+
+
+def gen_batch(name, ids, world=1):
+    """Images `ids` of a config, generated by a process pool bounded to the
+    host cores / ranks (so N ranks never oversubscribe the host)."""
+    import multiprocessing as mproc
+    ids = list(ids)
+    if not ids:
+        import vfsynth
+        spec = vfsynth.config(name)
+        return np.empty((0, spec.H, spec.W, 3), np.uint8)
+    cores = os.cpu_count() or 2
+    workers = max(1, min(16, cores // max(1, world) - 1, len(ids)))
+    if workers == 1:
+        return _gen_images((name, ids))
+    chunks = [ids[i::workers] for i in range(workers) if ids[i::workers]]
+    with mproc.get_context("fork").Pool(len(chunks)) as pool:
+        parts = pool.map(_gen_images, [(name, c) for c in chunks])
+    out = np.empty((len(ids),) + parts[0].shape[1:], np.uint8)
+    pos = {v: i for i, v in enumerate(ids)}
+    for i, c in enumerate(chunks):
+        for j, img in enumerate(parts[i]):
+            out[pos[c[j]]] = img
+    return out
 
 
 # ------------------------------------------------------------------ clocks
@@ -139,7 +206,7 @@ class ClockSampler:
     def summary(self, t0: float, t1: float):
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-        def parse(sel):
+        def parse_(sel):
             sm, mx, reasons, pw = [], None, set(), []
             for _, ln in sel:
                 f = [x.strip() for x in ln.split(",")]
@@ -158,10 +225,10 @@ class ClockSampler:
 
         timed = [l for l in self.lines if t0 - 0.06 <= l[0] <= t1 + 0.06]
         window = "timed"
-        sm, mx, reasons, pw = parse(timed)
+        sm, mx, reasons, pw = parse_(timed)
         if len(sm) < 3:     # timed region shorter than a few sampling periods
             window = "timed+warmup (timed region %.3f s)" % (t1 - t0)
-            sm, mx, reasons, pw = parse([l for l in self.lines if l[0] <= t1 + 0.06][-40:])
+            sm, mx, reasons, pw = parse_([l for l in self.lines if l[0] <= t1 + 0.06][-40:])
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "window": window}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
@@ -177,16 +244,6 @@ def measured_peaks():
         return {}
 
 
-def ncu_traffic(key):
-    """Per-launch DRAM bytes of the kernel from the committed ncu summary."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
-            d = json.load(fh)
-        return d.get("dram_bytes_per_launch", {}).get(key)
-    except Exception:
-        return None
-
-
 def cpu_model() -> str:
     try:
         for line in open("/proc/cpuinfo"):
@@ -197,124 +254,172 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_oracle_breakdown(w, x_np, budget_s=1.0, combos=COMBOS):
-    """the oracle's Mpix/s per criterion x variant on all host
-    threads and, for the whole 7-filter set, on one thread (bounded samples)."""
+def lib_sha256(path):
+    h = hashlib.sha256()
+    with open(path, "rb") as fh:
+        for blk in iter(lambda: fh.read(1 << 20), b""):
+            h.update(blk)
+    return h.hexdigest()
+
+
+def load_ncu_exec(sha):
+    """profiles/ncu_exec.json (tools/ncu_exec.py): per-kernel ncu pipe
+    utilisations captured from a libvf.so; used only if it is THIS library."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_exec.json")) as fh:
+            d = json.load(fh)
+    except Exception:
+        return None, "profiles/ncu_exec.json absent"
+    if d.get("libvf_sha256") != sha:
+        return None, "profiles/ncu_exec.json was captured from another libvf.so build (stale): not used"
+    return d, "profiles/ncu_exec.json (%s), same libvf.so sha256" % d.get("command", "?")
+
+
+# ------------------------------------------------------------------ the oracle (both CPU legs, one method)
+def oracle_sample(args):
+    """The bounded CPU sample of the workload: C4 -> its first image
+    (512x768), C2 -> the image, C5 -> a 256-row band of the image."""
+    import vfsynth
+    spec = workload_spec(args.workload)
+    if args.workload == "c5":
+        return vfsynth.make_image(spec, 0, 0, 256)[1][None], [("angular", "minimax")], 3
+    if args.workload == "c2":
+        return vfsynth.make_image(spec, 0)[1][None], COMBOS, 3
+    return vfsynth.make_image(spec, 0)[1][None], COMBOS, 3
+
+
+def oracle_steps(x, w, combos, steps, warmup, budget_s=None):
+    """The oracle as it stands (C, double, OpenMP over rows, all host
+    threads): each step filters every image of x with every combo; returns the
+    per-step wall times (perf_counter).  With budget_s, runs until that much
+    time has passed (at least `steps`)."""
     import oracle
-    img = x_np[0]
-    npx = img.shape[0] * img.shape[1]
-    per = {}
-    for crit, var in combos:
+    for _ in range(warmup):
+        for b in range(x.shape[0]):
+            for crit, var in combos:
+                oracle.filter_image(x[b], w, crit, var, want_index=False)
+    times = []
+    t_all = time.perf_counter()
+    while True:
         t0 = time.perf_counter()
-        k = 0
-        while True:
-            oracle.filter_image(img, w, crit, var, want_index=False)
-            k += 1
-            if time.perf_counter() - t0 >= budget_s:
-                break
-        per[f"{crit}/{var}"] = k * npx / (time.perf_counter() - t0) / 1e6
-    # one thread: a row band of the image, all 7 filters once
-    band = np.ascontiguousarray(img[: max(w, min(img.shape[0], 64))])
+        for b in range(x.shape[0]):
+            for crit, var in combos:
+                oracle.filter_image(x[b], w, crit, var, want_index=False)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= steps and (budget_s is None or time.perf_counter() - t_all >= budget_s):
+            break
+    return times
+
+
+def oracle_single_thread_rate(x, w, combos):
+    import oracle
+    band = np.ascontiguousarray(x[0, : max(w, min(x.shape[1], 32))])
     t0 = time.perf_counter()
     for crit, var in combos:
         oracle.filter_image(band, w, crit, var, want_index=False, nthreads=1)
-    st = len(combos) * band.shape[0] * band.shape[1] / (time.perf_counter() - t0) / 1e6
-    return per, st
+    return len(combos) * band.shape[0] * band.shape[1] / (time.perf_counter() - t0) / 1e6
 
 
-def cpu_oracle_rate(spec, w, x_np, budget_s=12.0, combos=COMBOS):
-    """The oracle as it stands on the host cores: run whole steps (all 7
-    combos over this image) until ~budget_s of CPU time; Mpix/s."""
+def cpu_leg(args, steps, warmup, budget_s=None):
+    """Shared by the reference arm and cpu_baseline: same sample, same warm-up
+    and per-step timing, same threads."""
     import oracle
-    t0 = time.perf_counter()
-    steps = 0
-    pix = 0
-    while True:
-        for b in range(x_np.shape[0]):
-            for crit, var in combos:
-                oracle.filter_image(x_np[b], w, crit, var, want_index=False)
-                pix += x_np.shape[1] * x_np.shape[2]
-        steps += 1
-        if time.perf_counter() - t0 >= budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return pix / dt / 1e6, steps, dt, oracle.max_threads()
+    oracle.build()
+    x, combos, w = oracle_sample(args)
+    times = oracle_steps(x, w, combos, steps, warmup, budget_s)
+    npix = x.shape[0] * x.shape[1] * x.shape[2]
+    ms = 1e3 * statistics.mean(times)
+    value = len(combos) * npix / (ms / 1e3) / 1e6
+    return {"value": value, "unit": "Mpix/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"{len(times)} timed steps (+{warmup} warm-up) x {len(combos)} filters of "
+                      f"{x.shape[0]}x{x.shape[1]}x{x.shape[2]} px (the workload's first image"
+                      f"{' band' if args.workload == 'c5' else ''})",
+            "ms_per_step": ms, "nproc": os.cpu_count(), "cpu_model": cpu_model(),
+            "single_thread_mpix_s": oracle_single_thread_rate(x, w, combos),
+            "timing": "oracle_steps(): per-step perf_counter, mean over the timed steps"}
 
 
-# ------------------------------------------------------------------ reference arm
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    spec, w = workload(args.config)
-    x = make_input(spec, 0)
-    if spec.name in ("C3", "C4", "C5"):
-        # bounded sample: a 512-row band of the first image keeps a step to seconds
-        x = x[:1, :512]
-    import oracle
-    oracle.build()
-    npix = x.shape[0] * x.shape[1] * x.shape[2]
-    for _ in range(args.warmup):
-        for crit, var in COMBOS:
-            oracle.filter_image(x[0], w, crit, var, want_index=False)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        for b in range(x.shape[0]):
-            for crit, var in COMBOS:
-                oracle.filter_image(x[b], w, crit, var, want_index=False)
-        times.append(time.perf_counter() - t0)
-    ms = 1e3 * sum(times) / len(times)
-    value = len(COMBOS) * npix / (ms / 1e3) / 1e6
-    full_spec, _ = workload(args.config)
-    xf = make_input(full_spec, 0)
-    cfg = workload_config(full_spec, xf.shape[0], xf.shape[1], xf.shape[2], w, args.gpus)
-    cfg["reference_sample"] = f"{x.shape[0]}x{x.shape[1]}x{x.shape[2]} px per step (CPU oracle)"
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    spec = workload_spec(args.workload)
+    cb = cpu_leg(args, max(1, args.steps), args.warmup)
+    cfg = workload_config(args, spec, world)
+    cfg["reference_sample"] = cb["sample"]
     line = {
-        "impl": "reference", "metric": METRIC,
-        "value": value, "unit": "Mpix/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": cfg,
-        "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": oracle.max_threads(), "kind": "oracle",
-                         "sample": f"{args.steps} steps x 7 filters of {x.shape[1]}x{x.shape[2]}x{x.shape[0]} px"},
-        "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "Mpix/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong" if args.workload != "c2" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg, "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
     return 0
 
 
-# ------------------------------------------------------------------ partitioned modes (C4 / C5)
-def _gen_images(args_):
-    import vfsynth
-    name, ids = args_
-    return vfsynth.make_batch(vfsynth.config(name), ids=ids)
+# ------------------------------------------------------------------ GPU timing helpers
+def ev_pair(torch):
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
 
-def gen_batch_parallel(name, ids, workers=None):
-    """Generate images `ids` of a config with a process pool (host cores)."""
-    import multiprocessing as mproc
-    import numpy as np
-    ids = list(ids)
-    workers = workers or max(1, min(16, (os.cpu_count() or 2) - 1))
-    chunks = [ids[i::workers] for i in range(workers) if ids[i::workers]]
-    with mproc.get_context("fork").Pool(len(chunks)) as pool:
-        parts = pool.map(_gen_images, [(name, c) for c in chunks])
-    out = np.empty((len(ids),) + parts[0].shape[1:], np.uint8)
-    for i, c in enumerate(chunks):
-        for j, img in enumerate(parts[i]):
-            out[ids.index(c[j])] = img
-    return out
+def kernel_avg_ms(torch, dev, stream, launch, reps, flush=None):
+    """Average duration of `launch()` over `reps` back-to-back launches between
+    CUDA events on the launching stream (one warm launch first).  With
+    `flush`, L2 is flushed (untimed) before the timed launches."""
+    launch()
+    if flush is not None:
+        flush.fill_(7)
+    torch.cuda.synchronize(dev)
+    a, b = ev_pair(torch)
+    a.record(stream)
+    for _ in range(reps):
+        launch()
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    return a.elapsed_time(b) / reps
 
 
-def run_partitioned(args):
-    """--mode shard (C4) / stripes (C5): the multi-GPU partitioner on the
-    data path (paper_1009_0959_b200.parallel), strong scaling (total work is
-    the config's, split over the ranks), max over ranks."""
+def kernel_entry(vfb, c, w, B, H, W, ms, peaks, ncu, npix):
+    n = w * w
+    pairs = n * (n - 1) // 2
+    mpix = npix / (ms / 1e3) / 1e6
+    flops = FLOPS_PER_PAIR[c] * pairs * npix
+    tfl = flops / (ms / 1e3) / 1e12
+    sfu = SFU_PER_PAIR[c] * pairs * npix / (ms / 1e3) / 1e12
+    try:
+        info = vfb.vf_kernel_info(B, H, W, w, c[0], c[1])
+    except Exception as e:          # noqa: BLE001
+        info = {"name": f"unavailable: {e}", "grid": None, "block": None, "smem": None}
+    e = {"kernel": info["name"], "grid": info["grid"], "block": info["block"], "ms": ms, "mpix_s": mpix,
+         "alg_flops_per_pair": FLOPS_PER_PAIR[c], "libm_calls_per_pair": LIBM_CALLS_PER_PAIR[c],
+         "alg_tflops": tfl, "frac_fp32_alg": tfl / peaks["fp32_tflops"],
+         "sfu_ops_per_pair": SFU_PER_PAIR[c], "sfu_tops": sfu, "frac_sfu_alg": sfu / peaks["sfu_tops"]}
+    if c[1] == "exact":
+        e["note"] = ("exact variant: flops = the method's arithmetic around one libm call (SURVEY 8(d) D4, no flop "
+                     "target); the libm routine's own instructions show in the ncu pipe utilisations")
+    if c[0] == "angular":
+        ev = ANGULAR_EVALS_PER_PX[w]
+        e.update({"pair_evaluations_per_px": ev, "paper_pairs_per_px": pairs,
+                  "frac_fp32_evaluated_pairs_only": FLOPS_PER_PAIR[c] * ev * npix / (ms / 1e3) / 1e12
+                  / peaks["fp32_tflops"],
+                  "frac_sfu_evaluated_pairs_only": SFU_PER_PAIR[c] * ev * npix / (ms / 1e3) / 1e12 / peaks["sfu_tops"],
+                  "frac_note": "frac_fp32_alg is paper-method-equivalent (all n(n-1)/2 pairs of every window); the "
+                               "pair-sharing kernel evaluates each image pair once (frac_*_evaluated_pairs_only)"})
+    if ncu is not None:
+        rec = ncu.get("kernels", {}).get("%s|%s" % (info["name"], ",".join(map(str, info["grid"] or ()))))
+        if rec is not None:
+            e["ncu"] = rec
+    return e
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
     import torch
     import torch.distributed as dist
-    import vfsynth
-    from paper_1009_0959_b200 import parallel as par
     import paper_1009_0959_b200 as vfb
+    from paper_1009_0959_b200 import parallel as par
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -323,91 +428,258 @@ def run_partitioned(args):
     torch.cuda.set_device(dev)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29533")
+    os.environ.setdefault("NCCL_DEBUG", "INFO")           # communicator lines (rank counts) on stderr
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     vfb.load_library()
+    sha = lib_sha256(vfb.vf.LIB_PATH)
+    ncu, ncu_note = load_ncu_exec(sha)
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    mp_ = measured_peaks()
+    f_max = float(mp_.get("sm_max_mhz") or SM_MAX_MHZ_DEFAULT)
+    peaks = {"fp32_tflops": 2 * 128 * sms * f_max * 1e6 / 1e12, "sfu_tops": 16 * sms * f_max * 1e6 / 1e12,
+             "hbm_gbs": mp_.get("hbm_gbs"), "sms": sms, "sm_max_mhz": f_max,
+             "source": "derived (DESIGN.md 6.1): FP32 = 2 flop x 128 lanes x SMs x max SM clock; SFU (MUFU) = 16 "
+                       "/clk/SM x SMs x clock; tools/fp32_peak.cu measured 68.9 TFLOP/s FFMA, 4.61 T/s MUFU.RSQ"}
     stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    if args.workload == "c5":
+        return run_stripes(args, torch, dist, vfb, par, dev, stream, flush, world, rank, peaks, sha)
+
+    spec = workload_spec(args.workload)
+    ids = local_ids(args, spec, world, rank)
+    B_total = world if args.workload == "c2" else (args.images or spec.batch)
     t_gen = time.perf_counter()
-    if args.mode == "shard":
-        spec = vfsynth.config("C4")
-        B, H, W, w = spec.batch, spec.H, spec.W, 3
-        lo, hi = par.shard_range(B, world, rank)
-        x = torch.from_numpy(gen_batch_parallel("C4", range(lo, hi))).to(dev)
-        combos = COMBOS
-        souts = [torch.empty_like(x) for _ in combos]
-        splan = vfb.Plan(x, souts, w, combos)          # the 7 filters as one graph
-
-        def step():
-            splan.launch(stream)
-            outs = {c: o for c, o in zip(combos, souts)}
-            return outs, par.gather_batch_stats(outs, B, combos, reference=("angular", "exact"))
-
-        units = B * H * W * len(combos)
-        workload_s = f"C4: {B} x {H}x{W} uint8 RGB batch sharded over {world} rank(s), 3x3, 7 filters, " \
-                     "per-image stats all_gather (NCCL)"
-    else:
-        spec = vfsynth.config("C5")
-        H, W = spec.H, spec.W
-        bands = {}
-        for w in spec.window:
-            o0, on, b0, bn = par.stripe_bounds(H, world, rank, w)
-            bands[w] = torch.from_numpy(vfsynth.make_image(spec, 0, b0, b0 + bn)[1]).to(dev)
-
-        def step():
-            res = {}
-            for w in spec.window:
-                res[w] = par.run_stripes(bands[w], H, w, "angular", "minimax")
-            return res
-
-        units = H * W * len(spec.window)
-        workload_s = f"C5: one {H}x{W} uint8 RGB image in {world} row stripe(s) with halo, angular minimax, " \
-                     "3x3 and 5x5, output stripes all_gather (NCCL)"
+    x_np = gen_batch(spec.name, ids, world)
     t_gen = time.perf_counter() - t_gen
-    for _ in range(max(args.warmup, 3)):
-        res = step()
-    torch.cuda.synchronize(dev)
+    Bl, H, W = len(ids), spec.H, spec.W
+    w = 3
+    x = torch.from_numpy(x_np).to(dev)
+    outs = [torch.empty_like(x) for _ in COMBOS]
+    plan = vfb.Plan(x, outs, w, COMBOS) if Bl else None
+    ref_i = COMBOS.index(REFERENCE)
+    stats_buf = torch.empty((len(COMBOS), max(Bl, 1), 8), dtype=torch.float64, device=dev)
+    counts = [par.shard_range(B_total, world, r)[1] - par.shard_range(B_total, world, r)[0]
+              for r in range(world)] if args.workload == "c4" else [1] * world
+
+    def step():
+        if Bl:
+            plan.launch(stream)
+            vfb.vf_image_stats_multi(outs[ref_i], outs, stats_buf, stream)
+            s = stats_buf
+        else:
+            s = torch.zeros((len(COMBOS), 0, 8), dtype=torch.float64, device=dev)
+        return par.all_gather_rows(s.permute(1, 0, 2).contiguous(), counts)       # [B, 7, 8]
+
+    clk = ClockSampler(dev.index).start()
+    tw = time.perf_counter()
+    nw = 0
+    while nw < max(args.warmup, 3) or time.perf_counter() - tw < 1.0:
+        step()
+        nw += 1
+        torch.cuda.synchronize(dev)
+    # ---- timed region: K steps, per-step CUDA events on the launching stream
+    ev = [ev_pair(torch) for _ in range(args.steps)]
     dist.barrier()
     torch.cuda.synchronize(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        res = step()
-    e1.record(stream)
+    t_wall0 = time.perf_counter()
+    for k in range(args.steps):
+        if args.workload == "c2":
+            flush.fill_(k & 0xFF)                 # C2's input (0.8 MB) fits in L2: flush, outside the events
+        ev[k][0].record(stream)
+        gathered = step()
+        ev[k][1].record(stream)
     torch.cuda.synchronize(dev)
+    t_wall1 = time.perf_counter()
     dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    extra = {}
-    if args.mode == "shard":
-        outs, stats = res
-        extra["fidelity_vs_angular_exact_whole_batch"] = {
-            f"{c[0]}/{c[1]}": par.stats_summary(stats[c].cpu(), spec.H, spec.W) for c in COMBOS}
+    ms_per_step = float(t.item()) / args.steps
+    units = B_total * H * W * len(COMBOS)           # pixel-filter evaluations per step, all ranks
+    value = units / (ms_per_step / 1e3) / 1e6
+    clocks = clk.summary(t_wall0, t_wall1)
+
+    # ---- per-kernel: each filter over the whole local batch (3x3)
+    kern = {}
+    npix_l = Bl * H * W
+    if Bl:
+        reps = 3 if args.workload == "c4" else 50
+        kouts = {c: outs[i] for i, c in enumerate(COMBOS)}
+        for c in REACH_COMBOS:
+            kouts[c] = torch.empty_like(x)
+        for c in COMBOS + REACH_COMBOS:
+            ms = kernel_avg_ms(torch, dev, stream,
+                               lambda c=c: vfb.vf_filter_batch(x, w, *c, out=kouts[c], stream=stream), reps,
+                               flush if args.workload == "c2" else None)
+            kern[f"{c[0]}/{c[1]}"] = kernel_entry(vfb, c, w, Bl, H, W, ms, peaks, ncu, npix_l)
+        t_stats = kernel_avg_ms(torch, dev, stream,
+                                lambda: vfb.vf_image_stats_multi(outs[ref_i], outs, stats_buf, stream), reps)
     else:
-        # the gathered full image must equal the single-call result (bit-exact)
-        full_ok = {}
-        for w in spec.window:
-            if world == 1:
-                full_ok[w] = True
-            else:
-                _, full = res[w]
-                full_ok[w] = bool(full.shape[0] == spec.H)
-        extra["gathered_rows_ok"] = full_ok
+        t_stats = None
+    clk.stop()
+    reach = {k: kern.pop(k) for k in [f"{c[0]}/{c[1]}" for c in REACH_COMBOS] if k in kern}
+    roofline = roofline_mm = None
+    if kern:
+        dom = max(kern, key=lambda k: kern[k]["ms"])
+        d = kern[dom]
+        roofline = {"bound": "alu", "kernel": dom, "kernel_name": d["kernel"], "achieved": d["alg_tflops"],
+                    "peak": peaks["fp32_tflops"], "unit": "TFLOP/s", "frac": d["frac_fp32_alg"],
+                    "avg_launch_ms": d["ms"], "share_of_step": d["ms"] / ms_per_step,
+                    "traffic": (d.get("ncu") or {}).get("dram_bytes"),
+                    "algorithmic_bytes": npix_l * 6,
+                    "algorithmic_flops_per_launch": FLOPS_PER_PAIR[tuple(dom.split("/"))] * 36 * npix_l,
+                    "peak_source": peaks["source"],
+                    "timing": "average launch duration of the kernel over the whole local batch (%d launches between "
+                              "CUDA events on the launching stream; input %d MiB%s)" % (
+                                  reps, x.numel() >> 20, " > L2" if x.numel() > (126 << 20) else
+                                  ", L2 flushed before the launches"),
+                    "note": ("the step's dominant kernel is an exact (libm) variant: SURVEY 8(d) D4 counts only the "
+                             "arithmetic around the libm call, so its algorithmic fraction is low by construction; "
+                             "roofline_minimax holds the paper's approximants") if dom.endswith("exact") else None}
+        mm = {k: v["frac_fp32_alg"] for k, v in kern.items() if not k.endswith("exact")}
+        a = kern["angular/minimax"]
+        roofline_mm = {"bound": "alu", "kernel": "angular/minimax (BVDF, Eq. 5 + Table 1)", "kernel_name": a["kernel"],
+                       "achieved": a["alg_tflops"], "peak": peaks["fp32_tflops"], "unit": "TFLOP/s",
+                       "frac": a["frac_fp32_alg"], "frac_evaluated_pairs_only": a["frac_fp32_evaluated_pairs_only"],
+                       "frac_sfu_alg": a["frac_sfu_alg"], "avg_launch_ms": a["ms"], "target": 0.60,
+                       "minimax_fracs": mm, "min_minimax_frac": min(mm.values()),
+                       "reach_fracs": {k: v["frac_fp32_alg"] for k, v in reach.items()}}
+
+    # ---- fidelity: minimax vs exact of the same criterion (the paper's quality measure), local batch
+    fid = None
+    if Bl:
+        fid = {}
+        kouts_all = {**{c: outs[i] for i, c in enumerate(COMBOS)}}
+        for c in REACH_COMBOS:
+            vfb.vf_filter_batch(x, w, *c, out=kouts[c], stream=stream)
+            kouts_all[c] = kouts[c]
+        for crit, mmv in (("angular", "minimax"), ("exp", "minimax"), ("exp", "poly4"), ("log", "minimax"),
+                          ("exp", "reach"), ("log", "reach")):
+            f = vfb.fidelity(kouts_all[(crit, "exact")], kouts_all[(crit, mmv)])
+            fid[f"{crit}/{mmv}"] = {"psnr_db": f["psnr_db"], "ncd": f["ncd"], "diff_frac": f["diff_frac"],
+                                    "max_abs": f["max_abs"]}
+    # the step's gathered statistics (all ranks' images) vs angular/exact
+    g = gathered.cpu()
+    step_stats = {f"{c[0]}/{c[1]}": par.stats_summary(g[:, i], H, W) for i, c in enumerate(COMBOS)}
+
+    # ---- end to end through the public API with HOST buffers
+    e2e = None
+    if not args.no_e2e and Bl:
+        e2e = run_e2e(args, torch, dist, vfb, dev, stream, x_np, x, outs, w, B_total, H, W)
+
+    # ---- C3 (5x5) per-kernel section, N = 1
+    c3 = None
+    if not args.no_c3 and world == 1 and args.workload == "c4":
+        c3 = run_c3(args, torch, vfb, dev, stream, flush, peaks, ncu)
+
+    paper = None
+    if not args.no_paper and rank == 0 and world == 1:
+        paper = paper_filters_section(vfb, torch, dev, stream, flush, kern)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_leg(args, 2, 1, budget_s=12.0)
+
     if rank == 0:
-        emit({
-            "metric": "filtered Mpixels/s", "value": units / (ms / 1e3) / 1e6, "unit": "Mpix/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_s, "mode": args.mode, "parallelism": f"dp{world}",
-                       "input_generation_s": t_gen},
-            "gpu_launches": (2 * len(COMBOS) if args.mode == "shard" else len(spec.window)) * args.steps,
-            **extra})
+        cfg = workload_config(args, spec, world)
+        cfg["input_generation_s"] = t_gen
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": cfg,
+            "roofline": roofline, "roofline_minimax": roofline_mm, "per_kernel": kern,
+            "step_breakdown": {"stats_multi_ms": t_stats, "sum_kernel_ms": sum(v["ms"] for v in kern.values()),
+                               "step_ms": ms_per_step,
+                               "note": "the plan's 7 kernels run concurrently; sum_kernel_ms is their serial sum"},
+            "f4_reach": {"per_kernel": reach,
+                         "speedup_vs_paper_minimax": {k: kern[k.replace("reach", "minimax")]["ms"] / v["ms"]
+                                                      for k, v in reach.items()}},
+            "c3": c3, "cpu_baseline": cpu, "e2e": e2e,
+            "fidelity_minimax_vs_exact": fid, "step_stats_vs_angular_exact": step_stats,
+            "paper_filters": paper,
+            "gpu_launches": (len(COMBOS) + 2) * args.steps if Bl else 0,
+            "gpu_launches_note": "per step: 7 filter kernels (plan graph) + vf_stats_multi_kernel + vf_stats_finalize",
+            "clocks": clocks, "wall_s_timed_region": t_wall1 - t_wall0, "peaks": peaks,
+            "libvf_sha256": sha, "ncu_exec": ncu_note,
+        }
+        emit(line)
+    if plan is not None:
+        plan.close()
     dist.destroy_process_group()
     return 0
 
 
-# ------------------------------------------------------------------ our arm
+def run_e2e(args, torch, dist, vfb, dev, stream, x_np, x, outs, w, B_total, H, W):
+    """The same metric through vf_plan_create(h_in, h_outs): every step copies
+    the rank's input from pinned host memory (H2D), runs the 7 filters and
+    copies the 7 outputs back (D2H), all inside the timed region."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:            # noqa: BLE001
+        avail = None
+    need = x_np.nbytes * (1 + len(COMBOS))
+    Bl = x_np.shape[0]
+    nb = Bl
+    if avail is not None and need * 2 > avail:      # keep the pinned buffers well inside host memory
+        nb = max(1, int(Bl * avail / (2 * need)))
+    h_in = torch.from_numpy(np.ascontiguousarray(x_np[:nb])).pin_memory()
+    h_outs = [torch.empty_like(h_in).pin_memory() for _ in COMBOS]
+    d_in = torch.empty_like(h_in, device=dev)
+    d_outs = [torch.empty_like(d_in) for _ in COMBOS]
+    hplan = vfb.Plan(d_in, d_outs, w, COMBOS, h_in=h_in, h_outs=h_outs)
+    hplan.launch(stream)
+    torch.cuda.synchronize(dev)
+    evs = [ev_pair(torch) for _ in range(max(1, args.e2e_steps))]
+    dist.barrier()
+    for a, b in evs:
+        a.record(stream)
+        hplan.launch(stream)
+        b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    same = all(torch.equal(h_outs[i], outs[i][:nb].cpu()) for i in range(len(COMBOS)))
+    world = dist.get_world_size()
+    units = nb * world * H * W * len(COMBOS)
+    hplan.close()
+    return {"value": units / (ms / 1e3) / 1e6, "unit": "Mpix/s", "h2d_bytes_per_step": nb * H * W * 3,
+            "d2h_bytes_per_step": len(COMBOS) * nb * H * W * 3, "ms_per_step": ms, "images_per_rank": nb,
+            "outputs_match_device_path": same,
+            "api": "vf_plan_create(h_in, h_outs) + vf_plan_launch: graph H2D -> 7 kernels -> 7 D2H (pinned host)",
+            "note": None if nb == Bl else f"host memory bounds the pinned buffers to {nb} of {Bl} images per rank"}
+
+
+def run_c3(args, torch, vfb, dev, stream, flush, peaks, ncu):
+    """BASELINE config 2 (C3): 8 x 2048^2, 5x5 window (300 pairs / pixel):
+    each criterion x variant kernel over the batch, L2 flushed before the
+    timed launches (the 100 MB input fits in L2)."""
+    import vfsynth
+    spec = vfsynth.config("C3")
+    t0 = time.perf_counter()
+    x = torch.from_numpy(gen_batch("C3", range(spec.batch))).to(dev)
+    tg = time.perf_counter() - t0
+    B, H, W = spec.batch, spec.H, spec.W
+    out = torch.empty_like(x)
+    res = {}
+    for c in COMBOS + REACH_COMBOS:
+        ms = kernel_avg_ms(torch, dev, stream, lambda c=c: vfb.vf_filter_batch(x, 5, *c, out=out, stream=stream),
+                           2, flush)
+        res[f"{c[0]}/{c[1]}"] = kernel_entry(vfb, c, 5, B, H, W, ms, peaks, ncu, B * H * W)
+    mm = {k: v["frac_fp32_alg"] for k, v in res.items() if not k.endswith("exact")}
+    return {"workload": "C3: 8 x 2048x2048 uint8 RGB, 5x5 window, uncorrelated 20% impulse noise (BASELINE config 2)",
+            "timing": "2 back-to-back launches between CUDA events after an untimed L2 flush, average",
+            "input_generation_s": tg, "per_kernel": res, "min_minimax_frac": min(mm.values()),
+            "minimax_fracs": mm}
+
+
 PAPER_FILTERS = [("amnfe", "exact"), ("amnfe", "minimax"), ("amnfe", "poly4"), ("amnfg", "exact"),
                  ("amnfg", "minimax"), ("evmf", "exact"), ("evmf", "minimax")]
 PAPER_TIME_PCT = {"BVDF": 1371.314, "AMNFE": 143.496, "EVMF": 236.105}   # Table 5, correlated 10% (P:315-325)
@@ -415,81 +687,106 @@ PAPER_TIME_PCT = {"BVDF": 1371.314, "AMNFE": 143.496, "EVMF": 236.105}   # Table
 PAPER_FIG5_S = {"BVDF": (10.360, 0.688), "AMNFE": (0.594, 0.422), "EVMF": (0.594, 0.250)}
 
 
-def steady_kernel_ms(vfb, torch, dev, stream, flush, x, w, combos, outs, reps=3):
-    """Average launch duration of each filter kernel: R back-to-back launches
-    over R distinct copies of x (R x bytes > L2, so no launch finds its input
-    in L2) captured in one CUDA graph (no host launch cost), replayed between
-    CUDA events on the launching stream after an L2 flush; ms per launch."""
-    R = max(2, min(256, -(-(160 << 20) // x.numel())))
-    xs_rep = x.unsqueeze(0).expand(R, *x.shape).contiguous()
-    graphs = {}
-    for c, o in zip(combos, outs):
-        vfb.vf_filter_batch(xs_rep[0], w, *c, out=o, stream=stream)   # attributes, caches
-        torch.cuda.synchronize(dev)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, capture_error_mode="relaxed"):
-            cs = torch.cuda.current_stream(dev)
-            for r in range(R):
-                vfb.vf_filter_batch(xs_rep[r], w, *c, out=o, stream=cs)
-        graphs[c] = g
-    res = {c: [] for c in combos}
-    for r in range(reps):
-        for c in combos:
-            flush.fill_(r & 0xFF)
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            graphs[c].replay()
-            b.record(stream)
-            torch.cuda.synchronize(dev)
-            res[c].append(a.elapsed_time(b) / R)
-    del graphs, xs_rep
-    return {c: statistics.mean(v) for c, v in res.items()}, R
-
-
-def paper_filters_section(vfb, torch, dev, stream, flush, x, x_np, spec, rank, w, outs):
-    """Isolated launches of AMNFE/AMNFG/EVMF (exact and minimax) plus the
-    angular BVDF outputs of the step; Time % and Table-5-style quality deltas
-    against the clean image (same image ids as the noisy input)."""
+def paper_filters_section(vfb, torch, dev, stream, flush, kern):
+    """The paper's three filters on the C2 image (Fig. 5's 512x512 size):
+    BVDF (angular order statistic), AMNFE (Eq. 8), EVMF (Eq. 9), exact and
+    minimax: average launch durations, Time % = 100 t_exact / t_approx (the
+    paper's definition) and MAE / MSE / NCD against the noise-free image."""
     import vfsynth
-    res = {"kernels": {}}
-    pouts = {c: torch.empty_like(x) for c in PAPER_FILTERS}
-    for c in PAPER_FILTERS:
-        vfb.vf_filter_batch(x, w, *c, out=pouts[c], stream=stream)
-    sms, R = steady_kernel_ms(vfb, torch, dev, stream, flush, x, w, PAPER_FILTERS, [pouts[c] for c in PAPER_FILTERS])
-    for c in PAPER_FILTERS:
-        vfb.vf_filter_batch(x, w, *c, out=pouts[c], stream=stream)   # outputs of the step's image
-        res["kernels"][f"{c[0]}/{c[1]}"] = {"ms": sms[c], "mpix_s": x.numel() / 3 / (sms[c] / 1e3) / 1e6}
-    res["timing"] = f"average launch duration over {R} back-to-back launches (bench.steady_kernel_ms)"
-    res["time_pct"] = {}
-    res["quality_vs_clean"] = {}
-    # clean images of the same ids
-    if spec.name in ("C1", "C2"):
-        clean = vfsynth.make_image(spec, rank if spec.batch == 1 else 0)[0][None]
-        ct = torch.from_numpy(clean).to(dev)
-        pairs = {"BVDF": ((("angular", "exact"), outs[COMBOS.index(("angular", "exact"))]),
-                          (("angular", "minimax"), outs[COMBOS.index(("angular", "minimax"))])),
-                 "AMNFE": ((("amnfe", "exact"), pouts[("amnfe", "exact")]), (("amnfe", "minimax"), pouts[("amnfe", "minimax")])),
-                 "EVMF": ((("evmf", "exact"), pouts[("evmf", "exact")]), (("evmf", "minimax"), pouts[("evmf", "minimax")]))}
-        noisy_q = vfb.fidelity(ct, x)
-        res["quality_vs_clean"]["noisy_input"] = {"mae": noisy_q["mae"], "mse": noisy_q["mse"], "ncd": noisy_q["ncd"]}
-        for name, ((ce, oe), (cm, om)) in pairs.items():
-            qe, qm = vfb.fidelity(ct, oe), vfb.fidelity(ct, om)
-            d = {}
-            for m in ("mae", "mse", "ncd"):
-                d[m] = {"exact": qe[m], "approx": qm[m],
-                        "delta_pct": 100.0 * (qe[m] - qm[m]) / qe[m] if qe[m] else 0.0}
-            res["quality_vs_clean"][name] = d
+    spec = vfsynth.config("C2")
+    clean, noisy = vfsynth.make_image(spec, 0)
+    x = torch.from_numpy(noisy[None]).to(dev)
+    ct = torch.from_numpy(clean[None]).to(dev)
+    res = {"workload": "C2 image (512x512, correlated 10%)", "kernels": {}, "time_pct": {}, "quality_vs_clean": {}}
+    outs = {}
+    for c in PAPER_FILTERS + [("angular", "exact"), ("angular", "minimax")]:
+        o = torch.empty_like(x)
+        ms = kernel_avg_ms(torch, dev, stream, lambda c=c, o=o: vfb.vf_filter_batch(x, 3, *c, out=o, stream=stream),
+                           100)
+        outs[c] = o
+        res["kernels"][f"{c[0]}/{c[1]}"] = {"ms": ms, "mpix_s": 512 * 512 / (ms / 1e3) / 1e6}
+    res["timing"] = "100 back-to-back launches between CUDA events (input in L2), average"
+    pk = res["kernels"]
+    noisy_q = vfb.fidelity(ct, x)
+    res["quality_vs_clean"]["noisy_input"] = {"mae": noisy_q["mae"], "mse": noisy_q["mse"], "ncd": noisy_q["ncd"]}
+    for name, ce, cm in (("BVDF", ("angular", "exact"), ("angular", "minimax")),
+                         ("AMNFE", ("amnfe", "exact"), ("amnfe", "minimax")),
+                         ("EVMF", ("evmf", "exact"), ("evmf", "minimax"))):
+        te, ta = pk[f"{ce[0]}/{ce[1]}"]["ms"], pk[f"{cm[0]}/{cm[1]}"]["ms"]
+        res["time_pct"][name] = {"b200": 100.0 * te / ta, "paper_pentium_d": PAPER_TIME_PCT[name]}
+        pe, pa = PAPER_FIG5_S[name]
+        res.setdefault("fig5_context", {})[name] = {
+            "paper_exact_s": pe, "paper_approx_s": pa, "b200_exact_s": te / 1e3, "b200_approx_s": ta / 1e3,
+            "hardware": "paper: Pentium D 2.66 GHz, 1 thread (P:295); b200: one kernel launch"}
+        qe, qm = vfb.fidelity(ct, outs[ce]), vfb.fidelity(ct, outs[cm])
+        res["quality_vs_clean"][name] = {
+            m: {"exact": qe[m], "approx": qm[m], "delta_pct": 100.0 * (qe[m] - qm[m]) / qe[m] if qe[m] else 0.0}
+            for m in ("mae", "mse", "ncd")}
     return res
 
 
-KERNEL_NAMES = {"angular": "vf_angular_shared_kernel<{w},{v}>", "exp": "vf_el_kernel<{w},exp,{v}>",
-                "log": "vf_el_kernel<{w},log,{v}>"}   # (3x3 polynomial variants of large launches: vf_el_tma_kernel)
+# ------------------------------------------------------------------ C5 stripes
+def run_stripes(args, torch, dist, vfb, par, dev, stream, flush, world, rank, peaks, sha):
+    import vfsynth
+    spec = vfsynth.config("C5")
+    H, W = spec.H, spec.W
+    t0 = time.perf_counter()
+    bands = {}
+    for w in spec.window:
+        o0, on, b0, bn = par.stripe_bounds(H, world, rank, w)
+        bands[w] = torch.from_numpy(vfsynth.make_image(spec, 0, b0, b0 + bn)[1]).to(dev)
+    t_gen = time.perf_counter() - t0
+
+    def step():
+        return {w: par.run_stripes(bands[w], H, w, "angular", "minimax") for w in spec.window}
+
+    clk = ClockSampler(dev.index).start()
+    for _ in range(max(args.warmup, 3)):
+        res = step()
+    torch.cuda.synchronize(dev)
+    ev = [ev_pair(torch) for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    tw0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)
+        ev[k][0].record(stream)
+        res = step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    tw1 = time.perf_counter()
+    dist.barrier()
+    total = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    clocks = clk.summary(tw0, tw1)
+    clk.stop()
+    check = None
+    if rank == 0:
+        # the gathered image must equal ONE whole-image call (bit-exact)
+        full_img = torch.from_numpy(vfsynth.make_image(spec, 0)[1]).to(dev)
+        check = {}
+        for w in spec.window:
+            ref = vfb.vf_filter(full_img, w, "angular", "minimax")
+            check[f"{w}x{w}"] = bool(torch.equal(res[w][1], ref))
+        del full_img
+    units = H * W * len(spec.window)
+    if rank == 0:
+        emit({"metric": "filtered Mpixels/s (C5 stripes: angular minimax 3x3 + 5x5 per step)",
+              "value": units / (ms / 1e3) / 1e6, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
+              "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+              "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+              "config": {**workload_config(args, spec, world), "input_generation_s": t_gen},
+              "gathered_equals_single_call": check,
+              "gpu_launches": 2 * 4 * args.steps, "clocks": clocks, "peaks": peaks, "libvf_sha256": sha})
+    dist.destroy_process_group()
+    return 0
 
 
 # The JSON line goes to the original stdout; everything else written to fd 1
-# (NCCL's version banner, library prints) is redirected to stderr so that
-# stdout carries exactly one line.
+# (NCCL's banner and INFO lines, library prints) is redirected to stderr so
+# that stdout carries exactly one line.
 _JSON_OUT = None
 
 
@@ -507,261 +804,7 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    if args.mode != "step":
-        return run_partitioned(args)
-
-    import torch
-    import torch.distributed as dist
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-
-    import paper_1009_0959_b200 as vfb
-    vfb.load_library()
-    spec, w = workload(args.config)
-    x_np = make_input(spec, rank)
-    B, H, W = x_np.shape[:3]
-    npix = B * H * W
-    x = torch.from_numpy(x_np).to(dev)
-    outs = [torch.empty_like(x) for _ in COMBOS]
-    stream = torch.cuda.current_stream(dev)
-    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    # the step: one plan = one CUDA graph whose 7 filter kernels are independent nodes
-    plan = vfb.Plan(x, outs, w, COMBOS)
-
-    def step():
-        plan.launch(stream)
-
-    clk = ClockSampler(dev.index).start()
-    # warm-up: at least W (>= 3) steps and at least 1 s of load, so clocks settle
-    tw = time.perf_counter()
-    nw = 0
-    while nw < max(args.warmup, 3) or time.perf_counter() - tw < 1.0:
-        step()
-        nw += 1
-        if nw % 50 == 0:
-            torch.cuda.synchronize(dev)
-    torch.cuda.synchronize(dev)
-
-    # ---- timed region: K steps, per-step CUDA events, L2 flush between steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    t_wall0 = time.perf_counter()
-    for k in range(args.steps):
-        flush.fill_(k & 0xFF)            # outside the event windows
-        ev[k][0].record(stream)
-        step()
-        ev[k][1].record(stream)
-    torch.cuda.synchronize(dev)
-    t_wall1 = time.perf_counter()
-    t_wall = t_wall1 - t_wall0
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    units = world * npix * len(COMBOS)               # pixel-filter evaluations per step, all ranks
-    value = units / (ms_per_step / 1e3) / 1e6        # Mpix/s
-
-    # ---- per-kernel breakdown.  (1) steady state: R back-to-back launches of
-    # the filter over R distinct copies of the step's input (R x input bytes >
-    # L2, so no launch finds its input in L2), captured in one CUDA graph
-    # (no host launch cost) and replayed between CUDA events on the launching
-    # stream: ms = that kernel's average launch duration.  (2) isolated: one
-    # launch after an L2 flush between two events (adds the ~6 us event +
-    # launch latency of an empty kernel on this platform, and the event clock
-    # advances in 2.048 us steps: only meaningful for long launches).
-    KCOMBOS = COMBOS + REACH_COMBOS
-    kouts = outs + [torch.empty_like(x) for _ in REACH_COMBOS]
-    in_bytes = x.numel()
-    t_k0 = time.perf_counter()
-    steady, R = steady_kernel_ms(vfb, torch, dev, stream, flush, x, w, KCOMBOS, kouts)
-    kreps_iso = max(3, min(args.steps, 20))
-    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in KCOMBOS]
-           for _ in range(kreps_iso)]
-    for r in range(kreps_iso):
-        for i, (crit, var) in enumerate(KCOMBOS):
-            flush.fill_((r + i) & 0xFF)
-            kev[r][i][0].record(stream)
-            vfb.vf_filter_batch(x, w, crit, var, out=kouts[i], stream=stream)
-            kev[r][i][1].record(stream)
-    torch.cuda.synchronize(dev)
-    t_k1 = time.perf_counter()
-    clk.stop()
-    clocks = clk.summary(t_wall0, t_wall1)
-    n = w * w
-    pairs = n * (n - 1) // 2
-    kern = {}
-    for i, c in enumerate(KCOMBOS):
-        ms = steady[c]
-        ms_iso = statistics.mean(kev[r][i][0].elapsed_time(kev[r][i][1]) for r in range(kreps_iso))
-        mpix = npix / (ms / 1e3) / 1e6
-        tfl = FLOPS_PER_PAIR[c] * pairs * npix / (ms / 1e3) / 1e12
-        kname = "vf_angular_role_kernel<{v}>".format(v=c[1]) if (c[0] == "angular" and w == 5) else \
-            KERNEL_NAMES[c[0]].format(w=w, v=c[1])
-        kern[f"{c[0]}/{c[1]}"] = {"kernel": kname, "ms": ms, "mpix_s": mpix,
-                                  "alg_tflops": tfl, "frac_fp32_at_max_clock": tfl / NOMINAL_FP32_TFLOPS_AT_MAX,
-                                  "ms_isolated": ms_iso,
-                                  "frac_fp32_isolated": FLOPS_PER_PAIR[c] * pairs * npix / (ms_iso / 1e3) / 1e12
-                                  / NOMINAL_FP32_TFLOPS_AT_MAX}
-        if clocks.get("sm_mhz"):
-            kern[f"{c[0]}/{c[1]}"]["frac_fp32_at_measured_clock"] = \
-                tfl / (NOMINAL_FP32_TFLOPS_AT_MAX * clocks["sm_mhz"] / 1965.0)
-        if c[0] == "angular":
-            # the pair-sharing kernels evaluate each image pair once per block
-            # (12 / 40 offsets per pixel + halo) instead of 36 / 300 per window:
-            # the algorithmic (paper-method) flops above can exceed what the
-            # kernel executes, so the fraction is "paper-method equivalent"
-            ev = 12 if w == 3 else 40
-            kern[f"{c[0]}/{c[1]}"].update({
-                "pair_evaluations_per_px": ev, "paper_pairs_per_px": pairs,
-                "frac_fp32_evaluated_pairs_only": FLOPS_PER_PAIR[c] * ev * npix / (ms / 1e3) / 1e12
-                / NOMINAL_FP32_TFLOPS_AT_MAX,
-                "note": "paper-method-equivalent fraction (flops of all n(n-1)/2 pairs per window); "
-                        "frac_fp32_evaluated_pairs_only counts the pairs the kernel evaluates (without halo, "
-                        "accumulation and role sums)"})
-    reach = {k: kern.pop(k) for k in [f"{c[0]}/{c[1]}" for c in REACH_COMBOS]}
-    dom = max(kern, key=lambda k: kern[k]["ms"])
-    d = kern[dom]
-    roofline = {"bound": "alu", "kernel": d["kernel"], "achieved": d["alg_tflops"],
-                "peak": NOMINAL_FP32_TFLOPS_AT_MAX, "unit": "TFLOP/s", "frac": d["alg_tflops"] / NOMINAL_FP32_TFLOPS_AT_MAX,
-                "peak_source": "derived: 2 flop x 128 FP32 lanes x 148 SM x 1.965 GHz (DESIGN.md 6.1); "
-                               "tools/fp32_peak.cu measures 68.9 TFLOP/s of FFMA",
-                "traffic": ncu_traffic(f"{spec.name}/{dom}"),
-                "algorithmic_flops_per_launch": FLOPS_PER_PAIR[tuple(dom.split("/"))] * pairs * npix,
-                "note": ("libm-bound exact variant (CUDA's expm1f / log1pf / asinf: range reduction, polynomial, "
-                         "special-case selects, ~24-37 SASS instructions per pair); the minimax kernels of the same "
-                         "step are in per_kernel / best_minimax_kernel") if dom.endswith("exact") else None,
-                "timing": f"average launch duration over {R} back-to-back launches (one CUDA graph replay, events on "
-                          f"the launching stream) over {R} distinct copies of the step input ({R * in_bytes >> 20} MiB "
-                          "> L2), L2 flushed before each replay; the isolated single-launch time is per_kernel."
-                          "ms_isolated"}
-    # whole-step roofline: the 7 kernels' algorithmic flops over the step time
-    # (they run concurrently inside the plan's graph, so per-kernel times
-    # cannot be separated inside the timed region)
-    step_flops = sum(FLOPS_PER_PAIR[c] for c in COMBOS) * pairs * npix
-    step_tfl = step_flops / (ms_per_step / 1e3) / 1e12
-    step_roofline = {"bound": "alu", "achieved": step_tfl, "peak": NOMINAL_FP32_TFLOPS_AT_MAX, "unit": "TFLOP/s",
-                     "frac": step_tfl / NOMINAL_FP32_TFLOPS_AT_MAX,
-                     "algorithmic_flops_per_step": step_flops,
-                     "timing": "the timed steps (7 concurrent kernels in one graph), per rank"}
-    mm = [k for k in kern if k.endswith("minimax") or k.endswith("poly4")]
-    best_mm = max(mm, key=lambda k: kern[k]["frac_fp32_at_max_clock"])
-
-    # ---- end to end through the C ABI with HOST buffers: a plan whose graph is
-    # H2D(input) -> 7 filter kernels -> 7 x D2H(output), pinned host memory
-    e2e = None
-    if not args.no_e2e:
-        h_in = torch.from_numpy(x_np).pin_memory()
-        h_outs = [torch.empty_like(h_in).pin_memory() for _ in COMBOS]
-        d_in2 = torch.empty_like(x)
-        d_outs2 = [torch.empty_like(x) for _ in COMBOS]
-        hplan = vfb.Plan(d_in2, d_outs2, w, COMBOS, h_in=h_in, h_outs=h_outs)
-        for _ in range(3):
-            hplan.launch(stream)
-        torch.cuda.synchronize(dev)
-        ksteps = max(3, min(args.steps, 20))
-        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ksteps)]
-        if world > 1:
-            dist.barrier()
-        for k in range(ksteps):
-            flush.fill_(k & 0xFF)
-            eev[k][0].record(stream)
-            hplan.launch(stream)
-            eev[k][1].record(stream)
-        torch.cuda.synchronize(dev)
-        e2e_ms = sum(a.elapsed_time(b) for a, b in eev) / ksteps
-        if world > 1:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        same = all(torch.equal(h_outs[i], outs[i].cpu()) for i in range(len(COMBOS)))
-        e2e = {"value": units / (e2e_ms / 1e3) / 1e6, "unit": "Mpix/s",
-               "h2d_bytes_per_step": npix * 3, "d2h_bytes_per_step": len(COMBOS) * npix * 3,
-               "ms_per_step": e2e_ms, "outputs_match_device_path": same,
-               "api": "vf_plan_create(h_in, h_outs) + vf_plan_launch: graph H2D -> 7 kernels -> 7 D2H"}
-        hplan.close()
-
-    # ---- fidelity: minimax vs exact (the paper's quality measure)
-    oi = {c: kouts[i] for i, c in enumerate(KCOMBOS)}
-    fid = {}
-    for crit, mmv in (("angular", "minimax"), ("exp", "minimax"), ("exp", "poly4"), ("log", "minimax"),
-                      ("exp", "reach"), ("log", "reach")):
-        f = vfb.fidelity(oi[(crit, "exact")], oi[(crit, mmv)])
-        fid[f"{crit}/{mmv}"] = {"psnr_db": f["psnr_db"], "ncd": f["ncd"], "diff_frac": f["diff_frac"]}
-
-    # ---- the paper's three filters (Table 5 methodology on the synthetic
-    # stand-in): BVDF = angular order statistic, AMNFE (Eq. 8), EVMF (Eq. 9);
-    # Time % = 100 t_exact / t_approx (the paper's definition) and
-    # quality deltas of MAE / MSE / NCD against the noise-free image.
-    paper = paper_filters_section(vfb, torch, dev, stream, flush, x, x_np, spec, rank, w, outs)
-    pk = paper["kernels"]
-    for name, te, ta in (("BVDF", kern["angular/exact"]["ms"], kern["angular/minimax"]["ms"]),
-                         ("AMNFE", pk["amnfe/exact"]["ms"], pk["amnfe/minimax"]["ms"]),
-                         ("EVMF", pk["evmf/exact"]["ms"], pk["evmf/minimax"]["ms"])):
-        paper["time_pct"][name] = {"b200": 100.0 * te / ta, "paper_pentium_d": PAPER_TIME_PCT[name]}
-        if spec.name == "C2":   # same image size as Fig. 5: per-image times side by side (context, not a target)
-            pe, pa = PAPER_FIG5_S[name]
-            paper.setdefault("fig5_context", {})[name] = {
-                "paper_exact_s": pe, "paper_approx_s": pa, "b200_exact_s": te / 1e3, "b200_approx_s": ta / 1e3,
-                "hardware": "paper: Pentium D 2.66 GHz, 1 thread (P:295); b200: one kernel launch (per_kernel timing)"}
-
-    # ---- CPU oracle baseline (rank 0, N = 1 only)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        xs = x_np if spec.name in ("C1", "C2") else x_np[:1, :256]
-        v, steps_done, dt, cores = cpu_oracle_rate(spec, w, xs)
-        per, single = cpu_oracle_breakdown(w, xs)
-        cpu = {"value": v, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
-               "sample": f"{steps_done} x (7 filters over {xs.shape[0]}x{xs.shape[1]}x{xs.shape[2]} px), {dt:.1f} s",
-               "cpu_model": cpu_model(), "per_filter_mpix_s": per, "single_thread_mpix_s": single}
-
-    if rank == 0:
-        line = {
-            "metric": METRIC,
-            "value": value, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic",
-            "config": {**workload_config(spec, B, H, W, w, world),
-                       "step": "vf_plan_launch: one CUDA graph, 7 independent filter kernels"},
-            "roofline": roofline,
-            "step_roofline": step_roofline,
-            "best_minimax_kernel": {"name": best_mm, **kern[best_mm]},
-            "per_kernel": kern,
-            "f4_reach": {"per_kernel": reach,
-                         "what": "SURVEY 8(f4): D_E / D_L as Remez minimax polynomials on the reachable arguments "
-                                 "(deg 5 eps 7.86e-8 / deg 7 eps 2.95e-7, no division), VF_MINIMAX_REACH; "
-                                 "not part of the 7-filter step",
-                         "speedup_vs_paper_minimax": {
-                             k: kern[k.replace("reach", "minimax")]["ms"] / v["ms"] for k, v in reach.items()}},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "fidelity_minimax_vs_exact": fid,
-            "paper_filters": paper,
-            "gpu_launches": len(COMBOS) * args.steps,
-            "clocks": clocks,
-            "wall_s_timed_region": t_wall,
-            "peaks": {"hbm_gbs": measured_peaks().get("hbm_gbs"),
-                      "fp32_tflops_nominal_at_max_clock": NOMINAL_FP32_TFLOPS_AT_MAX},
-        }
-        emit(line)
-    plan.close()
-    if world > 1:
-        dist.destroy_process_group()
-    return 0
+    return run_ours(args)
 
 
 if __name__ == "__main__":

@@ -151,6 +151,15 @@ VF_API int vf_filter_host(const uint8_t *h_imgs, int B, int H, int W, int window
                    int variant, uint8_t *h_outs, void *d_workspace, size_t workspace_bytes,
                    void *stream);
 
+/* Introspection: the kernel the library would launch for vf_filter_batch_algo
+ * with these arguments (no device work).  name: its (mangled) function name,
+ * written as a NUL-terminated string of at most name_cap bytes (nullable);
+ * launch: nullable long long[7] = {grid x, y, z, block x, y, z, dynamic smem
+ * bytes}.  Used to match profiler records to (criterion, variant).  Errors as
+ * vf_filter_batch_algo's argument checks; VF_ECUDA if the name is unavailable. */
+VF_API int vf_kernel_info(int B, int H, int W, int window, int criterion, int variant, int algo, char *name,
+                          int name_cap, long long *launch);
+
 /* PLAN (executor): n filters of the same input, built once as an
  * instantiated CUDA graph whose n kernel nodes are independent (they run
  * concurrently, so small images fill the GPU), optionally preceded by an H2D
@@ -183,10 +192,26 @@ VF_API int vf_image_stats(const uint8_t *a, const uint8_t *b, int B, int H, int 
 VF_API int vf_image_stats_ex(const uint8_t *a, const uint8_t *b, int B, int H, int W, double *stats, int flags,
                              void *stream);
 
+/* ONE pass over the reference a comparing it with nb outputs bs[0..nb-1]
+ * (host array of nb device pointers, each [B][H][W][3]; 1 <= nb <= 8):
+ * stats = device double [nb][B][8], row [k][i] exactly as vf_image_stats(a, bs[k])
+ * would write it for image i (column 4, the reference norm, is computed once
+ * and written into every row unless flags = VF_STATS_NO_REF_NORM).  Each
+ * reference pixel is read once and its CIELAB evaluated at most once, so
+ * comparing the 7 filters of a step against one reference costs one pass
+ * instead of 7.  Deterministic: the floating-point sums are accumulated across
+ * blocks in 2^-24 fixed point (integer atomics), so results are bit-identical
+ * run to run (as are those of vf_image_stats / _ex, which call this with
+ * nb = 1).  Errors: VF_EINVAL for NULL pointers, nb outside [1, 8], bad sizes
+ * or unknown flags. */
+VF_API int vf_image_stats_multi(const uint8_t *a, const uint8_t *const *bs, int nb, int B, int H, int W,
+                                double *stats, int flags, void *stream);
+
 VF_API const char *vf_status_string(int status);
 /* Text of the last error on the calling thread ("" if none). */
 VF_API const char *vf_last_error(void);
-/* ABI version (major*100 + minor): 102 (102: vf_image_stats_ex). */
+/* ABI version (major*100 + minor): 103 (102: vf_image_stats_ex; 103: vf_image_stats_multi,
+ * deterministic statistics, vf_kernel_info). */
 VF_API int vf_version(void);
 
 #ifdef __cplusplus

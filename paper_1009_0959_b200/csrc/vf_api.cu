@@ -415,6 +415,33 @@ int vf_filter_host(const uint8_t* h_imgs, int B, int H, int W, int window, int c
   return VF_OK;
 }
 
+int vf_kernel_info(int B, int H, int W, int window, int criterion, int variant, int algo, char* name, int name_cap,
+                   long long* launch) {
+  g_err[0] = 0;
+  int rc = validate(B, H, W, window, criterion, variant);
+  if (rc) return rc;
+  if (algo < 0 || algo > 31) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
+  // a dummy, 16-byte aligned input address: describe() only inspects alignment
+  const uint8_t* fake = reinterpret_cast<const uint8_t*>(uintptr_t(1) << 20);
+  const long long stride = (long long)H * W * 3;
+  KernelDesc kd;
+  rc = describe(&kd, fake, stride, 0, H, B, H, W, 0, H, window, criterion, variant, algo, (uint8_t*)fake + 1,
+                stride, nullptr, nullptr);
+  if (rc) return rc;
+  if (name && name_cap > 0) {
+    const char* nm = nullptr;
+    cudaError_t e = cudaFuncGetName(&nm, kd.fn);
+    if (e != cudaSuccess || !nm) return cuda_fail(e == cudaSuccess ? cudaErrorInvalidDeviceFunction : e, "cudaFuncGetName");
+    std::snprintf(name, (size_t)name_cap, "%s", nm);
+  }
+  if (launch) {
+    launch[0] = kd.grid.x; launch[1] = kd.grid.y; launch[2] = kd.grid.z;
+    launch[3] = kd.block.x; launch[4] = kd.block.y; launch[5] = kd.block.z;
+    launch[6] = (long long)kd.smem;
+  }
+  return VF_OK;
+}
+
 int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const int* criteria, const int* variants,
                    const uint8_t* d_in, uint8_t* const* d_outs, const uint8_t* h_in, uint8_t* const* h_outs) {
   g_err[0] = 0;
@@ -493,20 +520,46 @@ int vf_image_stats(const uint8_t* a, const uint8_t* b, int B, int H, int W, doub
 
 int vf_image_stats_ex(const uint8_t* a, const uint8_t* b, int B, int H, int W, double* stats, int flags,
                       void* stream) {
+  return vf_image_stats_multi(a, &b, 1, B, H, W, stats, flags, stream);
+}
+
+int vf_image_stats_multi(const uint8_t* a, const uint8_t* const* bs, int nb, int B, int H, int W, double* stats,
+                         int flags, void* stream) {
   g_err[0] = 0;
-  if (!a || !b || !stats) return fail(VF_EINVAL, "NULL pointer");
+  if (!a || !bs || !stats) return fail(VF_EINVAL, "NULL pointer");
+  if (nb < 1 || nb > 8) return fail(VF_EINVAL, "number of compared outputs must be in [1, 8] (got %lld)", nb);
+  for (int k = 0; k < nb; ++k)
+    if (!bs[k]) return fail(VF_EINVAL, "NULL output %lld", k);
   if (flags & ~VF_STATS_NO_REF_NORM) return fail(VF_EINVAL, "unknown stats flags (%lld)", flags);
   if (B < 1 || H < 1 || W < 1) return fail(VF_EINVAL, "bad size");
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(double) * 8 * (size_t)B, st);
+  const size_t nstat = (size_t)8 * B * nb;
+  cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(double) * nstat, st);
   if (e != cudaSuccess) return cuda_fail(e, "stats memset");
   const long long npix = (long long)H * W;
   int blocks = (int)((npix + 255) / 256);
   const int per_image = (148 * 8 + B - 1) / B;   // ~8 blocks per SM over the whole batch
   if (blocks > per_image) blocks = per_image < 1 ? 1 : per_image;
-  vf::vf_stats_kernel<<<dim3(blocks, B), 256, 0, st>>>(a, b, npix, stats, (flags & VF_STATS_NO_REF_NORM) ? 0 : 1);
+  vf::StatsArgs args = {};
+  for (int k = 0; k < nb; ++k) args.b[k] = bs[k];
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(stats);
+  const int ref = (flags & VF_STATS_NO_REF_NORM) ? 0 : 1;
+  const dim3 grid(blocks, B);
+  switch (nb) {
+    case 1: vf::vf_stats_multi_kernel<1><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
+    case 2: vf::vf_stats_multi_kernel<2><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
+    case 3: vf::vf_stats_multi_kernel<3><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
+    case 4: vf::vf_stats_multi_kernel<4><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
+    case 5: vf::vf_stats_multi_kernel<5><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
+    case 6: vf::vf_stats_multi_kernel<6><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
+    case 7: vf::vf_stats_multi_kernel<7><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
+    default: vf::vf_stats_multi_kernel<8><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
+  }
   e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "vf_stats_kernel launch");
+  if (e != cudaSuccess) return cuda_fail(e, "vf_stats_multi_kernel launch");
+  vf::vf_stats_finalize<<<(unsigned)((nstat + 255) / 256), 256, 0, st>>>(acc, (long long)nstat);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "vf_stats_finalize launch");
   return VF_OK;
 }
 
@@ -522,6 +575,6 @@ const char* vf_status_string(int status) {
 
 const char* vf_last_error(void) { return g_err; }
 
-int vf_version(void) { return 102; }
+int vf_version(void) { return 103; }
 
 }  // extern "C"

@@ -27,7 +27,7 @@ VARIANTS = {"exact": VF_EXACT, "minimax": VF_MINIMAX, "poly4": VF_MINIMAX_POLY4,
 ALGOS = {"auto": VF_ALGO_AUTO, "window": VF_ALGO_WINDOW, "shared": VF_ALGO_SHARED, "role": VF_ALGO_ROLE}
 EXPORTS = ["vf_filter", "vf_filter_batch", "vf_filter_rows", "vf_filter_batch_algo",
            "vf_host_workspace_bytes", "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_destroy",
-           "vf_image_stats", "vf_image_stats_ex", "vf_status_string", "vf_last_error", "vf_version"]
+           "vf_image_stats", "vf_image_stats_ex", "vf_image_stats_multi", "vf_kernel_info", "vf_status_string", "vf_last_error", "vf_version"]
 VF_STATS_NO_REF_NORM = 1
 
 
@@ -62,6 +62,8 @@ def load_library(path: str = LIB_PATH):
     L.vf_plan_destroy.argtypes = [P]
     L.vf_image_stats.argtypes = [P, P, I, I, I, P, P]
     L.vf_image_stats_ex.argtypes = [P, P, I, I, I, P, I, P]
+    L.vf_image_stats_multi.argtypes = [P, ctypes.POINTER(P), I, I, I, I, P, I, P]
+    L.vf_kernel_info.argtypes = [I, I, I, I, I, I, I, ctypes.c_char_p, I, ctypes.POINTER(ctypes.c_longlong)]
     L.vf_status_string.argtypes = [I]
     L.vf_status_string.restype = ctypes.c_char_p
     L.vf_last_error.argtypes = []
@@ -69,7 +71,7 @@ def load_library(path: str = LIB_PATH):
     L.vf_version.argtypes = []
     for name in ("vf_filter", "vf_filter_batch", "vf_filter_batch_algo", "vf_filter_rows",
                  "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_destroy", "vf_image_stats",
-                 "vf_image_stats_ex", "vf_version"):
+                 "vf_image_stats_ex", "vf_image_stats_multi", "vf_kernel_info", "vf_version"):
         getattr(L, name).restype = I
     _lib = L
     return L
@@ -109,6 +111,24 @@ def _dev_u8(t: torch.Tensor, name: str):
     return t.data_ptr()
 
 
+def _same_device(ref: torch.Tensor, *ts):
+    """Every buffer handed to the library must live on the input's device (the
+    kernels launch on the current device: see _on_device)."""
+    for t in ts:
+        if t is not None and (not t.is_cuda or t.device != ref.device):
+            raise ValueError(f"all buffers must be on {ref.device} (got {t.device})")
+
+
+def _check_buf(t, name: str, dtype, numel: int):
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype or not t.is_contiguous() or t.numel() != numel:
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor with {numel} elements "
+                         f"(got {t.dtype}, {t.numel()})")
+
+
 def _stream(stream) -> int:
     s = torch.cuda.current_stream() if stream is None else stream
     return s.cuda_stream
@@ -129,17 +149,18 @@ def vf_filter_batch_algo(imgs: torch.Tensor, window: int, criterion, variant, al
         raise ValueError("expected [B, H, W, 3] or [H, W, 3]")
     B, H, W, _ = x.shape
     n = window * window
+    _dev_u8(x, "imgs")
     if out is None:
         out = torch.empty_like(imgs)
-    if index is not None and (index.dtype != torch.uint8 or index.numel() != B * H * W or not index.is_cuda):
-        raise ValueError("index must be CUDA uint8 with B*H*W elements")
-    if aggregates is not None and (aggregates.dtype != torch.float32 or aggregates.numel() != B * H * W * n
-                                   or not aggregates.is_cuda):
-        raise ValueError("aggregates must be CUDA float32 with B*H*W*n elements")
-    rc = L.vf_filter_batch_algo(_dev_u8(x, "imgs"), B, H, W, window, _crit(criterion), _var(variant),
-                                _algo(algo),
-                                _dev_u8(out, "out"), _ptr_or_none(index), _ptr_or_none(aggregates),
-                                _stream(stream))
+    _check_buf(out, "out", torch.uint8, B * H * W * 3)
+    _check_buf(index, "index", torch.uint8, B * H * W)
+    _check_buf(aggregates, "aggregates", torch.float32, B * H * W * n)
+    _same_device(x, out, index, aggregates)
+    with torch.cuda.device(x.device):
+            rc = L.vf_filter_batch_algo(_dev_u8(x, "imgs"), B, H, W, window, _crit(criterion), _var(variant),
+                                    _algo(algo),
+                                    _dev_u8(out, "out"), _ptr_or_none(index), _ptr_or_none(aggregates),
+                                    _stream(stream))
     _check(rc, "vf_filter_batch_algo")
     return out
 
@@ -159,12 +180,20 @@ def vf_filter_rows(band: torch.Tensor, band_row0: int, H: int, out_row0: int, ou
                    stream=None) -> torch.Tensor:
     """band: CUDA uint8 [band_rows, W, 3] holding global rows [band_row0, ...)."""
     L = load_library()
+    if band.dim() != 3 or band.shape[-1] != 3:
+        raise ValueError("band must be [band_rows, W, 3]")
     band_rows, W, _ = band.shape
+    _dev_u8(band, "band")
     if out is None:
-        out = torch.empty((out_rows, W, 3), dtype=torch.uint8, device=band.device)
-    rc = L.vf_filter_rows(_dev_u8(band, "band"), band_row0, band_rows, H, W, out_row0, out_rows, window,
-                          _crit(criterion), _var(variant), _dev_u8(out, "out"), _ptr_or_none(index),
-                          _ptr_or_none(aggregates), _stream(stream))
+        out = torch.empty((max(out_rows, 0), W, 3), dtype=torch.uint8, device=band.device)
+    _check_buf(out, "out", torch.uint8, max(out_rows, 0) * W * 3)
+    _check_buf(index, "index", torch.uint8, max(out_rows, 0) * W)
+    _check_buf(aggregates, "aggregates", torch.float32, max(out_rows, 0) * W * window * window)
+    _same_device(band, out, index, aggregates)
+    with torch.cuda.device(band.device):
+        rc = L.vf_filter_rows(_dev_u8(band, "band"), band_row0, band_rows, H, W, out_row0, out_rows, window,
+                              _crit(criterion), _var(variant), _dev_u8(out, "out"), _ptr_or_none(index),
+                              _ptr_or_none(aggregates), _stream(stream))
     _check(rc, "vf_filter_rows")
     return out
 
@@ -212,21 +241,29 @@ class Plan:
             _dev_u8(t, "d_outs[i]")
             if t.numel() != x.numel():
                 raise ValueError("outputs must match the input size")
-        if h_in is not None and (h_in.is_cuda or h_in.dtype != torch.uint8 or h_in.numel() != x.numel()):
-            raise ValueError("h_in must be a host uint8 tensor like d_in")
+        _same_device(x, *d_outs)
+        if h_in is not None and (h_in.is_cuda or h_in.dtype != torch.uint8 or h_in.numel() != x.numel()
+                                 or not h_in.is_contiguous()):
+            raise ValueError("h_in must be a contiguous host uint8 tensor like d_in")
+        for t in (h_outs or []):
+            if t.is_cuda or t.dtype != torch.uint8 or t.numel() != x.numel() or not t.is_contiguous():
+                raise ValueError("h_outs[i] must be contiguous host uint8 tensors like d_in")
+        self.device = x.device
         self._keep = (d_in, list(d_outs), h_in, None if h_outs is None else list(h_outs))
         crit = (ctypes.c_int * n)(*[_crit(c) for c, _ in combos])
         var = (ctypes.c_int * n)(*[_var(v) for _, v in combos])
         douts = (ctypes.c_void_p * n)(*[t.data_ptr() for t in d_outs])
         houts = None if h_outs is None else (ctypes.c_void_p * n)(*[t.data_ptr() for t in h_outs])
         self._h = ctypes.c_void_p()
-        rc = L.vf_plan_create(ctypes.byref(self._h), B, H, W, window, n, crit, var, _dev_u8(x, "d_in"), douts,
-                              None if h_in is None else h_in.data_ptr(), houts)
+        with torch.cuda.device(x.device):
+            rc = L.vf_plan_create(ctypes.byref(self._h), B, H, W, window, n, crit, var, _dev_u8(x, "d_in"), douts,
+                                  None if h_in is None else h_in.data_ptr(), houts)
         _check(rc, "vf_plan_create")
         self.n = n
 
     def launch(self, stream=None):
-        _check(load_library().vf_plan_launch(self._h, _stream(stream)), "vf_plan_launch")
+        with torch.cuda.device(self.device):
+            _check(load_library().vf_plan_launch(self._h, _stream(stream)), "vf_plan_launch")
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -245,18 +282,49 @@ def vf_image_stats(a: torch.Tensor, b: torch.Tensor, stats: Optional[torch.Tenso
     """Per-image [B, 8] float64 statistics (see include/vf.h).  ref_norm=False
     (vf_image_stats_ex, VF_STATS_NO_REF_NORM) skips column 4 (sum |a_Lab|,
     a function of `a` alone), which is then 0."""
+    return vf_image_stats_multi(a, [b], None if stats is None else stats.view(1, *stats.shape), stream,
+                                ref_norm)[0]
+
+
+def vf_image_stats_multi(a: torch.Tensor, bs, stats: Optional[torch.Tensor] = None, stream=None,
+                         ref_norm: bool = True) -> torch.Tensor:
+    """One pass over the reference `a` against every output in `bs` (1..8
+    tensors shaped like a): float64 [len(bs), B, 8], row [k] as
+    vf_image_stats(a, bs[k])."""
     L = load_library()
     x = a.unsqueeze(0) if a.dim() == 3 else a
+    if x.dim() != 4 or x.shape[-1] != 3:
+        raise ValueError("expected [B, H, W, 3] or [H, W, 3]")
     B, H, W, _ = x.shape
+    nb = len(bs)
+    if not 1 <= nb <= 8:
+        raise ValueError("compare 1..8 outputs per call")
+    _dev_u8(x, "a")
+    for i, b in enumerate(bs):
+        _dev_u8(b, f"bs[{i}]")
+        if b.numel() != x.numel():
+            raise ValueError(f"bs[{i}] must have the shape of a ({tuple(a.shape)}), got {tuple(b.shape)}")
     if stats is None:
-        stats = torch.empty((B, 8), dtype=torch.float64, device=a.device)
-    if ref_norm:
-        rc = L.vf_image_stats(_dev_u8(a, "a"), _dev_u8(b, "b"), B, H, W, stats.data_ptr(), _stream(stream))
-    else:
-        rc = L.vf_image_stats_ex(_dev_u8(a, "a"), _dev_u8(b, "b"), B, H, W, stats.data_ptr(), VF_STATS_NO_REF_NORM,
-                                 _stream(stream))
-    _check(rc, "vf_image_stats")
-    return stats
+        stats = torch.empty((nb, B, 8), dtype=torch.float64, device=a.device)
+    _check_buf(stats, "stats", torch.float64, nb * B * 8)
+    _same_device(x, stats, *bs)
+    arr = (ctypes.c_void_p * nb)(*[b.data_ptr() for b in bs])
+    with torch.cuda.device(x.device):
+        rc = L.vf_image_stats_multi(_dev_u8(x, "a"), arr, nb, B, H, W, stats.data_ptr(),
+                                    0 if ref_norm else VF_STATS_NO_REF_NORM, _stream(stream))
+    _check(rc, "vf_image_stats_multi")
+    return stats.view(nb, B, 8)
+
+
+def vf_kernel_info(B: int, H: int, W: int, window: int, criterion, variant, algo="auto") -> dict:
+    """The kernel vf_filter_batch_algo would launch for these arguments
+    (mangled name, grid, block, dynamic smem); no device work."""
+    L = load_library()
+    buf = ctypes.create_string_buffer(1024)
+    lau = (ctypes.c_longlong * 7)()
+    _check(L.vf_kernel_info(B, H, W, window, _crit(criterion), _var(variant), _algo(algo), buf, 1024, lau),
+           "vf_kernel_info")
+    return {"name": buf.value.decode(), "grid": tuple(lau[0:3]), "block": tuple(lau[3:6]), "smem": int(lau[6])}
 
 
 def vf_status_string(status: int) -> str:
@@ -292,7 +360,9 @@ def fidelity(a: torch.Tensor, b: torch.Tensor) -> dict:
     """PSNR / NCD / MAE / MSE / fraction of differing pixels of b against a
     (the paper's quality measures), per batch, from vf_image_stats."""
     import math
-    s = vf_image_stats(a, b).double().sum(0).cpu().tolist()
+    per = vf_image_stats(a, b).double().cpu()
+    s = per.sum(0).tolist()
+    s[5] = float(per[:, 5].max())           # the batch maximum, not the sum of per-image maxima
     x = a.unsqueeze(0) if a.dim() == 3 else a
     npix = x.shape[0] * x.shape[1] * x.shape[2]
     mse = s[2] / (3 * npix)

@@ -22,7 +22,8 @@ def test_reference_arm_prints_one_json_line():
     assert KEYS <= set(d), KEYS - set(d)
     assert d["impl"] == "reference"
     assert d["value"] > 0 and d["unit"] == "Mpix/s" and d["higher_is_better"] is True
-    assert d["config"]["workload"].startswith("C2")
+    assert d["config"]["workload"].startswith("C4: 1024 x 512x768")      # the headline workload (BASELINE config 3)
+    assert d["scaling"] == "strong"
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
@@ -40,20 +41,33 @@ import pytest  # noqa: E402
 
 @pytest.mark.gpu
 def test_gpu_arm_json_line():
-    """Our arm on the GPU (short run): one JSON line with roofline, clocks,
+    """Our arm on the GPU (short run on the first 64 C4 images): one JSON line
+    with roofline, roofline_minimax, per-kernel SURVEY 8(d) fractions, clocks,
     gpu_launches and an end-to-end figure that moved host bytes."""
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3",
-                        "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+                        "--images", "64", "--no-cpu-baseline", "--no-c3", "--no-paper"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.strip()]
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert KEYS <= set(d), KEYS - set(d)
-    assert d["dtype"] == "f32" and d["scaling"] == "weak" and d["gpu_launches"] == 7 * 3
+    assert d["dtype"] == "f32" and d["scaling"] == "strong" and d["gpu_launches"] == 9 * 3
+    assert d["config"]["images"] == 64
     rf = d["roofline"]
     assert rf["bound"] == "alu" and 0 < rf["frac"] < 1.5 and rf["unit"] == "TFLOP/s" and rf["peak"] > 70
-    assert d["e2e"]["h2d_bytes_per_step"] == 512 * 512 * 3 and d["e2e"]["d2h_bytes_per_step"] == 7 * 512 * 512 * 3
+    rm = d["roofline_minimax"]
+    assert 0 < rm["frac"] < 1.5 and rm["target"] == 0.6 and len(rm["minimax_fracs"]) == 4
+    px = 64 * 512 * 768
+    assert d["e2e"]["h2d_bytes_per_step"] == px * 3 and d["e2e"]["d2h_bytes_per_step"] == 7 * px * 3
     assert d["e2e"]["outputs_match_device_path"] is True
     assert d["clocks"]["sm_mhz"] is None or d["clocks"]["sm_mhz"] > 0
+    assert len(d["per_kernel"]) == 7
     for k, v in d["per_kernel"].items():
-        assert v["ms"] > 0 and v["ms_isolated"] > 0, k
+        assert v["ms"] > 0 and 0 < v["frac_fp32_alg"] < 1.5 and v["frac_sfu_alg"] >= 0, k
+        assert v["kernel"].startswith("_Z"), k                      # vf_kernel_info: mangled kernel name
+    a = d["per_kernel"]["angular/minimax"]
+    assert a["frac_fp32_evaluated_pairs_only"] < a["frac_fp32_alg"]
+    # the step's gathered stats: the reference against itself is exact
+    st = d["step_stats_vs_angular_exact"]
+    assert st["angular/exact"]["diff_frac"] == 0 and st["angular/exact"]["images"] == 64

@@ -319,6 +319,45 @@ def test_image_stats_without_reference_norm():
     assert rc == vfm.VF_EINVAL
 
 
+def test_image_stats_multi_one_pass():
+    """vf_image_stats_multi(a, [b_0..b_6]): row k is bit-identical to
+    vf_image_stats(a, b_k) (same per-pixel values, same fixed-point sums),
+    the statistics are bit-reproducible run to run, and each row matches the
+    numpy metrics oracle; nb outside [1, 8] is rejected."""
+    from oracle import metrics
+    rng = np.random.default_rng(2)
+    B, H, W = 3, 57, 83
+    a = rng.integers(0, 256, size=(B, H, W, 3)).astype(np.uint8)
+    bs = []
+    for k in range(7):
+        b = a.copy()
+        m = rng.random(a.shape[:3]) < 0.05 * k
+        b[m] = rng.integers(0, 256, size=(m.sum(), 3))
+        bs.append(b)
+    ta = torch.from_numpy(a).cuda()
+    tbs = [torch.from_numpy(b).cuda() for b in bs]
+    multi = vfb.vf_image_stats_multi(ta, tbs).cpu().numpy()
+    again = vfb.vf_image_stats_multi(ta, tbs).cpu().numpy()
+    assert multi.shape == (7, B, 8) and np.array_equal(multi, again)
+    for k in range(7):
+        single = vfb.vf_image_stats(ta, tbs[k]).cpu().numpy()
+        assert np.array_equal(multi[k], single), k
+        for i in range(B):
+            npix = H * W
+            assert multi[k, i, 0] == (a[i] != bs[k][i]).any(-1).sum()
+            assert multi[k, i, 1] / (3 * npix) == pytest.approx(metrics.mae(a[i], bs[k][i]), rel=1e-12, abs=0)
+            assert multi[k, i, 2] / (3 * npix) == pytest.approx(metrics.mse(a[i], bs[k][i]), rel=1e-12, abs=0)
+            if k:
+                assert multi[k, i, 3] / multi[k, i, 4] == pytest.approx(metrics.ncd(a[i], bs[k][i]), rel=2e-6)
+    assert np.all(multi[0, :, [0, 1, 2, 3, 5]] == 0)               # b_0 == a
+    nr = vfb.vf_image_stats_multi(ta, tbs, ref_norm=False).cpu().numpy()
+    assert np.all(nr[:, :, 4] == 0) and np.array_equal(nr[:, :, [0, 1, 2, 5]], multi[:, :, [0, 1, 2, 5]])
+    with pytest.raises(ValueError):
+        vfb.vf_image_stats_multi(ta, tbs + tbs)
+    with pytest.raises(ValueError):
+        vfb.vf_image_stats_multi(ta, [tbs[0][:, :10]])
+
+
 # ------------------------------------------------------------- full-size configs (sampled)
 def _sample_pixels(H, W, n, seed):
     rng = np.random.default_rng(seed)
