@@ -7,10 +7,11 @@ synthetic 512x768 uint8 RGB images (uncorrelated impulse noise, p per image
 from {5,10,20,30}%), 3x3 window.  One STEP filters the rank's shard of the
 batch with all seven criterion x variant filters (angular/exp/log x
 exact/minimax + exp poly4; one CUDA graph of 7 concurrent kernels), compares
-the six others with the angular exact output in ONE fused statistics pass
-(vf_image_stats_multi) and all_gathers the per-image statistics over NCCL
-(the only collective of the batch path).  N GPUs split the
-1024 images (strong scaling: the total work is the config's).
+each approximant with the exact filter of its criterion (the paper's fidelity
+measure: one fused statistics pass per exact reference,
+vf_image_stats_multi) and all_gathers the per-image statistics over NCCL (the
+only collective of the batch path).  N GPUs split the 1024
+images (strong scaling: the total work is the config's).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c2|c5] [--impl ours|reference]
 
@@ -54,6 +55,12 @@ COMBOS = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp"
 # timed per kernel beside the paper's variants (not part of the 7-filter step)
 REACH_COMBOS = [("exp", "reach"), ("log", "reach")]
 REFERENCE = ("angular", "exact")
+# the step's statistics: every paper approximant against the exact filter of
+# its criterion (the paper's fidelity measure) -- one fused pass per
+# exact reference (vf_image_stats_multi)
+FIDELITY_GROUPS = [(("angular", "exact"), [("angular", "minimax")]),
+                   (("exp", "exact"), [("exp", "minimax"), ("exp", "poly4")]),
+                   (("log", "exact"), [("log", "minimax")])]
 
 # algorithmic FP32 flops per pair (FMA = 2, add/sub/mul = 1;
 # abs/neg/compare/select = 0; robustness overhead not counted).  Exact
@@ -108,8 +115,8 @@ def workload_config(args, spec, world):
     B = args.images or spec.batch
     if args.workload == "c4":
         w = f"C4: {B} x {spec.H}x{spec.W} uint8 RGB batch sharded over {world} rank(s), 3x3 window, " \
-            f"uncorrelated impulse noise p in {{5,10,20,30}}%, all 7 criterion/variant filters per step + fused " \
-            f"per-image stats vs angular/exact + NCCL all_gather of the stats"
+            f"uncorrelated impulse noise p in {{5,10,20,30}}%, all 7 criterion/variant filters per step + per-image " \
+            f"fidelity stats of each approximant vs its exact filter + NCCL all_gather of the stats"
         return {"workload": w, "images": B, "H": spec.H, "W": spec.W, "window": 3,
                 "parallelism": f"dp{world} (batch shards)",
                 "l2": "inputs larger than L2 (no flush): %d MiB per rank per step" % ((B // world) * spec.H * spec.W * 3 >> 20)}
@@ -459,19 +466,28 @@ def run_ours(args):
     x = torch.from_numpy(x_np).to(dev)
     outs = [torch.empty_like(x) for _ in COMBOS]
     plan = vfb.Plan(x, outs, w, COMBOS) if Bl else None
-    ref_i = COMBOS.index(REFERENCE)
-    stats_buf = torch.empty((len(COMBOS), max(Bl, 1), 8), dtype=torch.float64, device=dev)
+    oc = {c: outs[i] for i, c in enumerate(COMBOS)}
+    n_cmp = sum(len(cs) for _, cs in FIDELITY_GROUPS)
+    stats_buf = torch.empty((n_cmp, max(Bl, 1), 8), dtype=torch.float64, device=dev)
+    gviews, k0 = [], 0
+    for ref, cs in FIDELITY_GROUPS:
+        gviews.append((oc[ref], [oc[c] for c in cs], stats_buf[k0:k0 + len(cs)]))
+        k0 += len(cs)
+
+    def stats_pass():
+        for ref_t, outs_t, sv in gviews:
+            vfb.vf_image_stats_multi(ref_t, outs_t, sv, stream)
     counts = [par.shard_range(B_total, world, r)[1] - par.shard_range(B_total, world, r)[0]
               for r in range(world)] if args.workload == "c4" else [1] * world
 
     def step():
         if Bl:
             plan.launch(stream)
-            vfb.vf_image_stats_multi(outs[ref_i], outs, stats_buf, stream)
+            stats_pass()
             s = stats_buf
         else:
-            s = torch.zeros((len(COMBOS), 0, 8), dtype=torch.float64, device=dev)
-        return par.all_gather_rows(s.permute(1, 0, 2).contiguous(), counts)       # [B, 7, 8]
+            s = torch.zeros((n_cmp, 0, 8), dtype=torch.float64, device=dev)
+        return par.all_gather_rows(s.permute(1, 0, 2).contiguous(), counts)       # [B, comparisons, 8]
 
     clk = ClockSampler(dev.index).start()
     tw = time.perf_counter()
@@ -516,8 +532,7 @@ def run_ours(args):
                                lambda c=c: vfb.vf_filter_batch(x, w, *c, out=kouts[c], stream=stream), reps,
                                flush if args.workload == "c2" else None)
             kern[f"{c[0]}/{c[1]}"] = kernel_entry(vfb, c, w, Bl, H, W, ms, peaks, ncu, npix_l)
-        t_stats = kernel_avg_ms(torch, dev, stream,
-                                lambda: vfb.vf_image_stats_multi(outs[ref_i], outs, stats_buf, stream), reps)
+        t_stats = kernel_avg_ms(torch, dev, stream, stats_pass, reps)
     else:
         t_stats = None
     clk.stop()
@@ -549,22 +564,21 @@ def run_ours(args):
                        "minimax_fracs": mm, "min_minimax_frac": min(mm.values()),
                        "reach_fracs": {k: v["frac_fp32_alg"] for k, v in reach.items()}}
 
-    # ---- fidelity: minimax vs exact of the same criterion (the paper's quality measure), local batch
-    fid = None
+    # ---- fidelity: minimax vs exact of the same criterion (the paper's quality
+    # measure), from the step's gathered statistics (all ranks' images); the
+    # f4 reach polynomials from one extra pass on the local batch
+    g = gathered.cpu()
+    fid, i = {}, 0
+    for ref, cs in FIDELITY_GROUPS:
+        for c in cs:
+            fid[f"{c[0]}/{c[1]}"] = par.stats_summary(g[:, i], H, W)
+            i += 1
     if Bl:
-        fid = {}
-        kouts_all = {**{c: outs[i] for i, c in enumerate(COMBOS)}}
         for c in REACH_COMBOS:
             vfb.vf_filter_batch(x, w, *c, out=kouts[c], stream=stream)
-            kouts_all[c] = kouts[c]
-        for crit, mmv in (("angular", "minimax"), ("exp", "minimax"), ("exp", "poly4"), ("log", "minimax"),
-                          ("exp", "reach"), ("log", "reach")):
-            f = vfb.fidelity(kouts_all[(crit, "exact")], kouts_all[(crit, mmv)])
-            fid[f"{crit}/{mmv}"] = {"psnr_db": f["psnr_db"], "ncd": f["ncd"], "diff_frac": f["diff_frac"],
-                                    "max_abs": f["max_abs"]}
-    # the step's gathered statistics (all ranks' images) vs angular/exact
-    g = gathered.cpu()
-    step_stats = {f"{c[0]}/{c[1]}": par.stats_summary(g[:, i], H, W) for i, c in enumerate(COMBOS)}
+            f = vfb.fidelity(oc[(c[0], "exact")], kouts[c])
+            fid[f"{c[0]}/{c[1]}"] = {"psnr_db": f["psnr_db"], "ncd": f["ncd"], "diff_frac": f["diff_frac"],
+                                    "max_abs": f["max_abs"], "images": Bl}
 
     # ---- end to end through the public API with HOST buffers
     e2e = None
@@ -600,10 +614,11 @@ def run_ours(args):
                          "speedup_vs_paper_minimax": {k: kern[k.replace("reach", "minimax")]["ms"] / v["ms"]
                                                       for k, v in reach.items()}},
             "c3": c3, "cpu_baseline": cpu, "e2e": e2e,
-            "fidelity_minimax_vs_exact": fid, "step_stats_vs_angular_exact": step_stats,
+            "fidelity_minimax_vs_exact": fid,
             "paper_filters": paper,
-            "gpu_launches": (len(COMBOS) + 2) * args.steps if Bl else 0,
-            "gpu_launches_note": "per step: 7 filter kernels (plan graph) + vf_stats_multi_kernel + vf_stats_finalize",
+            "gpu_launches": (len(COMBOS) + 2 * len(FIDELITY_GROUPS)) * args.steps if Bl else 0,
+            "gpu_launches_note": "per step: 7 filter kernels (plan graph) + 3 x (vf_stats_multi_kernel + "
+                                 "vf_stats_finalize)",
             "clocks": clocks, "wall_s_timed_region": t_wall1 - t_wall0, "peaks": peaks,
             "libvf_sha256": sha, "ncu_exec": ncu_note,
         }

@@ -106,7 +106,9 @@ typedef enum {
   VF_ALGO_WINDOW = 1,   /* angular: one thread per window, all n(n-1)/2 pairs                    */
   VF_ALGO_SHARED = 2,   /* angular: pairs shared across windows, per-window accumulation         */
   VF_ALGO_ROLE = 3,     /* angular 5x5: pairs shared, per-pixel role sums (the 5x5 default)      */
-  VF_ALGO_NO_TMA = 16
+  VF_ALGO_NO_TMA = 16,
+  VF_ALGO_STREAM = 32   /* angular 3x3 minimax: warp-streamed pair sharing + role sums (the 3x3
+                           minimax default under VF_ALGO_AUTO; or-ed in, it forces that kernel) */
 } vf_algo;
 
 /* One image.  img, out: device [H][W][3]; index: device [H][W] or NULL;

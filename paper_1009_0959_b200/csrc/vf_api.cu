@@ -21,6 +21,7 @@
 #include "vf_role.cuh"
 #include "vf_shared.cuh"
 #include "vf_stats.cuh"
+#include "vf_stream.cuh"
 #include "vf_tma.cuh"
 #include "vf_window.cuh"
 
@@ -61,8 +62,10 @@ struct KernelDesc {
   bool tma = false;          // vf_el_tma_kernel: (map, L, tiles_x, tiles_y, ntiles)
   alignas(64) CUtensorMap map;
   int tiles_x = 0, tiles_y = 0, ntiles = 0;
+  int stream_k = 0;          // vf_angular_stream_kernel: (L, K)
   void* args[5];
   void** params() {
+    if (stream_k) { args[0] = &L; args[1] = &stream_k; return args; }
     if (!tma) { args[0] = &L; return args; }
     args[0] = &map; args[1] = &L; args[2] = &tiles_x; args[3] = &tiles_y; args[4] = &ntiles;
     return args;
@@ -195,7 +198,24 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
   L.kscale = kscale(crit, window);
   const int tile = (algo >> 2) & 3;   // 0 = by size; 1..3 = forced rows per thread (tuning / tests)
   const bool no_tma = (algo & VF_ALGO_NO_TMA) != 0;
+  const bool want_stream = (algo & VF_ALGO_STREAM) != 0;
   algo &= 3;
+  // 3x3 angular minimax: the warp-streamed role-sum kernel (vf_stream.cuh) is
+  // the default (VF_ANG3_STREAM=0 falls back to the block pair-sharing kernel)
+  static const bool env_no_stream = [] { const char* e = std::getenv("VF_ANG3_STREAM"); return e && e[0] == '0'; }();
+  if (crit == VF_ANGULAR && window == 3 && var == VF_MINIMAX &&
+      (want_stream || (algo == VF_ALGO_AUTO && !env_no_stream))) {
+    const long long strips = (W + vf::stream::SOUT - 1) / vf::stream::SOUT;
+    static const int k_env = [] { const char* e = std::getenv("VF_STREAM_K"); return e ? std::atoi(e) : 0; }();
+    const int K = (k_env >= 2 && k_env <= 1024) ? k_env : vf::stream_rows_per_warp(strips * out_rows * (long long)B);
+    kd->fn = vf::stream_kernel_fn_mm();
+    kd->grid = vf::stream_grid(L, B, K);
+    kd->block = dim3(32 * vf::stream::NWARP);
+    kd->smem = vf::stream_smem_bytes();
+    kd->stream_k = K;
+    if (kd->grid.y > 65535 || kd->grid.z > 65535) return fail(VF_EINVAL, "grid too large");
+    return VF_OK;
+  }
   if (crit == VF_ANGULAR && algo != VF_ALGO_WINDOW) {
     // launch configuration (vf_shared.cuh: 1..3 = 256 threads x 1..3 region
     // pixels, 4 = 384 threads x 2 in a 32 x 24 region): 4 measured fastest
@@ -346,7 +366,7 @@ int vf_filter_batch_algo(const uint8_t* imgs, int B, int H, int W, int window, i
   int rc = validate(B, H, W, window, criterion, variant);
   if (rc) return rc;
   if (!imgs || !outs) return fail(VF_EINVAL, "NULL image or output pointer");
-  if (algo < 0 || algo > 31) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
+  if (algo < 0 || algo > 63) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
   const size_t bytes = (size_t)B * H * W * 3;
   if (overlap(imgs, bytes, outs, bytes)) return fail(VF_EINVAL, "input and output overlap");
   const long long stride = (long long)H * W * 3;
@@ -420,7 +440,7 @@ int vf_kernel_info(int B, int H, int W, int window, int criterion, int variant, 
   g_err[0] = 0;
   int rc = validate(B, H, W, window, criterion, variant);
   if (rc) return rc;
-  if (algo < 0 || algo > 31) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
+  if (algo < 0 || algo > 63) return fail(VF_EINVAL, "algo out of range (%lld)", algo);
   // a dummy, 16-byte aligned input address: describe() only inspects alignment
   const uint8_t* fake = reinterpret_cast<const uint8_t*>(uintptr_t(1) << 20);
   const long long stride = (long long)H * W * 3;
@@ -537,24 +557,37 @@ int vf_image_stats_multi(const uint8_t* a, const uint8_t* const* bs, int nb, int
   cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(double) * nstat, st);
   if (e != cudaSuccess) return cuda_fail(e, "stats memset");
   const long long npix = (long long)H * W;
-  int blocks = (int)((npix + 255) / 256);
-  const int per_image = (148 * 8 + B - 1) / B;   // ~8 blocks per SM over the whole batch
-  if (blocks > per_image) blocks = per_image < 1 ? 1 : per_image;
+  // four pixels (three aligned words) per iteration when the images allow it
+  bool px4 = npix % 4 == 0 && ((uintptr_t)a % 4) == 0;
+  for (int k = 0; k < nb; ++k) px4 = px4 && ((uintptr_t)bs[k] % 4) == 0;
+  const long long units = px4 ? npix / 4 : npix;
+  // ~8 blocks per SM over the batch, and at most 4096 pixels per thread (the
+  // per-thread integer sums are 32-bit)
+  long long blocks = (units + 255) / 256;
+  long long per_image = (148 * 8 + B - 1) / B;
+  const long long min_blocks = (npix + 256LL * 4096 - 1) / (256LL * 4096);
+  if (per_image < min_blocks) per_image = min_blocks;
+  if (blocks > per_image) blocks = per_image;
+  if (blocks > 2147483647LL) return fail(VF_EINVAL, "image too large (%lld pixels)", npix);
   vf::StatsArgs args = {};
   for (int k = 0; k < nb; ++k) args.b[k] = bs[k];
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(stats);
   const int ref = (flags & VF_STATS_NO_REF_NORM) ? 0 : 1;
-  const dim3 grid(blocks, B);
+  const dim3 grid((unsigned)blocks, B);
+#define VF_STATS_LAUNCH(NBV)                                                                      \
+  if (px4) vf::vf_stats_multi_kernel<NBV, 4><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); \
+  else vf::vf_stats_multi_kernel<NBV, 1><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref);
   switch (nb) {
-    case 1: vf::vf_stats_multi_kernel<1><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
-    case 2: vf::vf_stats_multi_kernel<2><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
-    case 3: vf::vf_stats_multi_kernel<3><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
-    case 4: vf::vf_stats_multi_kernel<4><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
-    case 5: vf::vf_stats_multi_kernel<5><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
-    case 6: vf::vf_stats_multi_kernel<6><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
-    case 7: vf::vf_stats_multi_kernel<7><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
-    default: vf::vf_stats_multi_kernel<8><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); break;
+    case 1: VF_STATS_LAUNCH(1) break;
+    case 2: VF_STATS_LAUNCH(2) break;
+    case 3: VF_STATS_LAUNCH(3) break;
+    case 4: VF_STATS_LAUNCH(4) break;
+    case 5: VF_STATS_LAUNCH(5) break;
+    case 6: VF_STATS_LAUNCH(6) break;
+    case 7: VF_STATS_LAUNCH(7) break;
+    default: VF_STATS_LAUNCH(8) break;
   }
+#undef VF_STATS_LAUNCH
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "vf_stats_multi_kernel launch");
   vf::vf_stats_finalize<<<(unsigned)((nstat + 255) / 256), 256, 0, st>>>(acc, (long long)nstat);

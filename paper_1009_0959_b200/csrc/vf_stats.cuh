@@ -13,15 +13,22 @@ __device__ __forceinline__ float srgb_to_linear_f(int c) {
 
 // t^(1/3) for t in (0.0088, 1.1] (the CIELAB cube-root branch: positive
 // normal arguments only, so none of cbrtf's special cases): MUFU.LG2 and
-// MUFU.EX2 give ~4e-7 relative, one Newton step y += (t/y^2 - y)/3 brings it
-// to ~1 ulp.
+// MUFU.EX2 give z ~ t^(-1/3) to ~4e-7 relative; one Newton step for the
+// inverse cube root, z' = z (4 - t z^3) / 3 (no division), brings it to ~1e-7
+// and t^(1/3) = t z'^2.
 __device__ __forceinline__ float cbrt_pos(float t) {
-  float l, y, r;
+  float l, z;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(t));
-  const float e = l * (1.0f / 3.0f);
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(e));
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(y * y));
-  return fmaf(fmaf(t, r, -y), 1.0f / 3.0f, y);
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(z) : "f"(l * (-1.0f / 3.0f)));
+  const float tz3 = t * (z * z) * z;
+  z = z * fmaf(tz3, -1.0f / 3.0f, 4.0f / 3.0f);
+  return t * z * z;
+}
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
 __device__ __forceinline__ float lab_f(float t) {
@@ -74,55 +81,108 @@ struct StatsArgs {
   const uint8_t* b[8];
 };
 
-template <int NB>
+// PX = 4: four consecutive pixels = three aligned 32-bit words (needs
+// npix % 4 == 0 and 4-byte aligned image bases); PX = 1: one pixel (load_px).
+template <int PX>
+__device__ __forceinline__ void load_chunk(const uint8_t* img, long long ch, uint32_t (&px)[PX]) {
+  if constexpr (PX == 4) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(img) + ch * 3;
+    const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2);
+    px[0] = w0 & 0x00ffffffu;
+    px[1] = __byte_perm(w0, w1, 0x0543) & 0x00ffffffu;
+    px[2] = __byte_perm(w1, w2, 0x0432) & 0x00ffffffu;
+    px[3] = w2 >> 8;
+  } else {
+    px[0] = load_px(img, ch);
+  }
+}
+
+template <int NB, int PX>
 __global__ void __launch_bounds__(256) vf_stats_multi_kernel(const uint8_t* __restrict__ a, const StatsArgs bs,
                                                              long long npix, int B,
                                                              unsigned long long* __restrict__ acc,
                                                              int want_ref_norm) {
   const int img = blockIdx.y;
-  const uint8_t* pa = a + (long long)img * npix * 3;
+  const long long ioff = (long long)img * npix * 3;
+  const uint8_t* pa = a + ioff;
   __shared__ float lin[256];
   lin[threadIdx.x] = srgb_to_linear_f(threadIdx.x);
   __syncthreads();
-  unsigned long long ndiff[NB], l1[NB], l2[NB];
-  uint32_t mx[NB];
+  // per thread: exact integer sums (u32: the grid keeps <= 4096 pixels per
+  // thread, so sum (a-b)^2 < 8e8), byte-wise running max, fp32 Lab-distance
+  // partial sums flushed into double every 8 chunks
+  uint32_t ndiff[NB], l1[NB], l2[NB], mxv[NB];
   double s3[NB];
   float f3[NB];
 #pragma unroll
-  for (int k = 0; k < NB; ++k) { ndiff[k] = 0; l1[k] = 0; l2[k] = 0; mx[k] = 0; s3[k] = 0.0; f3[k] = 0.0f; }
+  for (int k = 0; k < NB; ++k) { ndiff[k] = 0; l1[k] = 0; l2[k] = 0; mxv[k] = 0; s3[k] = 0.0; f3[k] = 0.0f; }
   double s4 = 0.0;
   float f4 = 0.0f;
   int cnt = 0;
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < npix;
-       p += (long long)gridDim.x * blockDim.x) {
-    const uint32_t u = load_px(pa, p);
-    float L1 = 0.0f, A1 = 0.0f, B1 = 0.0f;
-    bool have_a = false;
+  const long long nch = npix / PX;
+  // warp-uniform trip count (the warp votes below need every lane): lanes past
+  // the end compare the last chunk with itself (no difference, no sums)
+  const int lane = threadIdx.x & 31;
+  for (long long ch0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); ch0 < nch;
+       ch0 += (long long)gridDim.x * blockDim.x) {
+    const bool live = ch0 + lane < nch;
+    const long long ch = live ? ch0 + lane : nch - 1;
+    uint32_t u[PX];
+    load_chunk<PX>(pa, ch, u);
+    float La[PX], Aa[PX], Ba[PX];
     if (want_ref_norm) {
-      rgb_to_lab(u, lin, L1, A1, B1);
-      have_a = true;
-      f4 += sqrtf(L1 * L1 + A1 * A1 + B1 * B1);
-    }
 #pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      const uint32_t v = load_px(bs.b[k] + (long long)img * npix * 3, p);
-      if (u != v) {
-        const uint32_t ad = __vabsdiffu4(u, v);             // |a - b| per channel
-        const uint32_t d0 = ad & 0xff, d1 = (ad >> 8) & 0xff, d2 = (ad >> 16) & 0xff;
-        ndiff[k] += 1;
-        l1[k] += d0 + d1 + d2;
-        l2[k] += d0 * d0 + d1 * d1 + d2 * d2;
-        mx[k] = max(mx[k], max(d0, max(d1, d2)));
-        if (!have_a) {
-          rgb_to_lab(u, lin, L1, A1, B1);
-          have_a = true;
-        }
-        float L2, A2, B2;
-        rgb_to_lab(v, lin, L2, A2, B2);
-        f3[k] += sqrtf((L1 - L2) * (L1 - L2) + (A1 - A2) * (A1 - A2) + (B1 - B2) * (B1 - B2));
+      for (int p = 0; p < PX; ++p) {
+        rgb_to_lab(u[p], lin, La[p], Aa[p], Ba[p]);
+        f4 += live ? sqrt_approx(La[p] * La[p] + Aa[p] * Aa[p] + Ba[p] * Ba[p]) : 0.0f;
       }
     }
-    if (++cnt == 32) {
+    // exact integer statistics, branch free; dm: the (output, pixel) slots that differ
+    uint32_t v[NB][PX];
+    uint32_t dm = 0;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      load_chunk<PX>(bs.b[k] + ioff, ch, v[k]);
+#pragma unroll
+      for (int p = 0; p < PX; ++p) {
+        if (!live) v[k][p] = u[p];
+        const uint32_t ad = __vabsdiffu4(u[p], v[k][p]);       // |a - b| per channel (byte 3 = 0)
+        const bool d = u[p] != v[k][p];
+        ndiff[k] += d;
+        dm |= (d ? 1u : 0u) << (k * PX + p);
+        l1[k] = __dp4a(ad, 0x01010101u, l1[k]);
+        l2[k] = __dp4a(ad, ad, l2[k]);
+        mxv[k] = __vmaxu4(mxv[k], ad);
+      }
+    }
+    // CIELAB distances of the differing slots (filter outputs differ from the
+    // reference in few pixels): one slot per lane per pass, so a warp runs
+    // max-over-lanes passes instead of one divergent branch per slot
+    while (__any_sync(0xffffffffu, dm != 0)) {
+      if (dm) {
+        const int bit = __ffs(dm) - 1;
+        dm &= dm - 1;
+        const int k = bit / PX, p = bit % PX;
+        uint32_t uu = u[0], vv = v[0][0];
+        float L1 = La[0], A1 = Aa[0], B1 = Ba[0];
+#pragma unroll
+        for (int q = 1; q < PX; ++q)
+          if (p == q) { uu = u[q]; L1 = La[q]; A1 = Aa[q]; B1 = Ba[q]; }
+#pragma unroll
+        for (int kk = 0; kk < NB; ++kk)
+#pragma unroll
+          for (int q = 0; q < PX; ++q)
+            if (bit == kk * PX + q) vv = v[kk][q];
+        if (!want_ref_norm) rgb_to_lab(uu, lin, L1, A1, B1);
+        float L2, A2, B2;
+        rgb_to_lab(vv, lin, L2, A2, B2);
+        const float dl = L1 - L2, da = A1 - A2, db = B1 - B2;
+        const float dist = sqrt_approx(dl * dl + da * da + db * db);
+#pragma unroll
+        for (int kk = 0; kk < NB; ++kk) f3[kk] += (k == kk) ? dist : 0.0f;
+      }
+    }
+    if (++cnt == 8) {
 #pragma unroll
       for (int k = 0; k < NB; ++k) { s3[k] += f3[k]; f3[k] = 0.0f; }
       s4 += f4;
@@ -132,14 +192,16 @@ __global__ void __launch_bounds__(256) vf_stats_multi_kernel(const uint8_t* __re
   }
   s4 += f4;
   __shared__ double red[8][6 * NB + 1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k <= NB; ++k) {
     double s[6];
     if (k < NB) {
       s3[k] += f3[k];
+      const uint32_t m = mxv[k];
+      const uint32_t mx = max(m & 0xffu, max((m >> 8) & 0xffu, (m >> 16) & 0xffu));
       s[0] = (double)ndiff[k]; s[1] = (double)l1[k]; s[2] = (double)l2[k]; s[3] = s3[k]; s[4] = 0.0;
-      s[5] = (double)mx[k];
+      s[5] = (double)mx;
     } else {
       s[0] = s4;
     }

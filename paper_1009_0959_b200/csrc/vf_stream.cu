@@ -1,0 +1,11 @@
+// vf_stream.cu -- the warp-streamed 3x3 angular minimax kernel (vf_stream.cuh)
+// in its own translation unit, so its ptxas settings and tuning knobs
+// (VF_STREAM_MINB, VF_STREAM_ACOS) are independent of the other kernels.
+#define VF_ANGULAR_MM_TU   // no kernel-selection helpers here
+#include "vf_stream.cuh"
+
+namespace vf {
+
+const void* stream_kernel_fn_mm() { return (const void*)vf_angular_stream_kernel<MINIMAX>; }
+
+}  // namespace vf

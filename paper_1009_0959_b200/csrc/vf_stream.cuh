@@ -1,0 +1,561 @@
+// vf_stream.cuh -- 3x3 angular minimax criterion: warp-streamed pair sharing
+// with per-pixel role sums (BVDF of Eq. 5
+// with the Table 1 approximants).
+//
+// The angular distance A(x_p, x_q) depends on the two pixels only, so every
+// image pair within Chebyshev distance 2 is evaluated once (12 per pixel) and
+// the window aggregates are formed from per-pixel ROLE SUMS: for a sample q at
+// position (a, b) of a 3x3 window (a = row, b = column, raster index 3a + b),
+//     R(q; a, b) = sum_{dy in [-a, 2-a], dx in [-b, 2-b], (dy,dx) != 0} A(q, q + (dy, dx))
+// which is exactly the aggregate R_k = sum_{j != k} A(x_k, x_j) of Eq. 5
+// of that sample in that window.  Separably: H_b(q, dy) = sum_{dx in
+// [-b, 2-b]} A(q, q + (dy, dx)) (5 additions per neighbourhood row), then
+// R(q; a, b) = sum_{dy in [-a, 2-a]} H_b(q, dy) (2 additions per role, with
+// shared partial sums).  All terms are >= 0 (no subtraction: full relative
+// precision).
+//
+// Organisation: each WARP independently streams down a strip of 64 image
+// columns (2 per lane: columns 2l, 2l+1, packed into one FFMA2 lane pair),
+// one image row per step; no block barriers.  At step r the warp
+//   a1/a2  stages row r (clamped, replicate padding) into a 4-row ring of
+//          pixel-pair records (packed RGB, |x|^2) in shared memory;
+//   a4/a5  evaluates for both of its pixels q the 12 "upper half-plane"
+//          pairs (q, q + d), d in {(-1|-2, -2..2), (0, -1|-2)}: exact integer
+//          geometry, the exact branch predicate 4 D^2 < |x_p|^2 |x_q|^2
+//          (DESIGN.md 5.2), Table 1's ARCSIN row on tau = sqrt(1 - cos) and
+//          its ARCCOS row on cos, the branch selected per pair -- branch
+//          free (both Horner chains in packed FP32);
+//   a6     routes every value to the H sums of BOTH endpoints (the lower
+//          endpoint's rows r-1 / r-2 and the horizontal neighbours live in
+//          adjacent lanes: 15 warp shuffles per step) and completes the roles
+//          of row r (a = 2), r-1 (a = 1) and r-2 (a = 0);
+//   a7/a8  the window centred at row r-1 now has all 9 aggregates: they are
+//          made 32-bit keys (aggregate bits with the low 4 mantissa bits
+//          replaced by the window position, so a float min picks the lowest
+//          position among aggregates equal to 2^-19 relative -- within the
+//          1e-5 acceptance of SURVEY 8(c).4), reduced with 3-input FMNMX, and
+//          the selected sample is read back from the ring and stored.
+// A strip computes 64 columns and outputs 58 (strip columns 3..60); K output
+// rows take K + 2 steps.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "vf_window.cuh"
+
+namespace vf {
+namespace stream {
+
+constexpr int SW = 64;          // computed columns per strip (2 per lane)
+constexpr int J_LO = 3;         // first output column of the strip
+constexpr int SOUT = 58;        // output columns per strip: [3, 61)
+constexpr int NE = 34;          // even-aligned record pairs per ring row: columns (2e - 2, 2e - 1), e = 0..33
+constexpr int NO = 33;          // odd-aligned record pairs: columns (2o - 1, 2o), o = 0..32
+constexpr int SLOTS = 4;        // ring rows (rows r, r-1, r-2 in use)
+constexpr int NWARP = 4;        // warps per block (independent strips / row tiles)
+
+constexpr int PW = SW + 8;      // plain pixel row: strip column j at index j + 2
+
+struct Ring {
+  uint4 E[SLOTS][NE];           // (pk(2e-2), pk(2e-1), |x|^2, |x|^2)
+  uint4 O[SLOTS][NO];           // (pk(2o-1), pk(2o),   |x|^2, |x|^2)
+  uint32_t P[SLOTS][PW];        // packed pixels (the selected sample is read back from here)
+};
+// Columns -2, -1, 64 and 65 of E / O (lanes 0 and 31, offsets |dx| >= 1) are
+// never written: the pair values that read them only feed the roles of strip
+// columns 0, 1, 62 and 63, which no output window uses (outputs 3..60 read
+// the roles of columns 2..61, whose pairs all lie inside columns 0..63).
+
+// strip s covers image columns x0 = 58 s - 3 + j, j = 0..63
+__host__ __device__ constexpr int strip_x0(int s) { return SOUT * s - J_LO; }
+
+}  // namespace stream
+
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float lo2(f32x2 v) { float a, b; unpack2(v, a, b); return a; }
+__device__ __forceinline__ float hi2(f32x2 v) { float a, b; unpack2(v, a, b); return b; }
+// 3-input min (sm_100: FMNMX3)
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// Role value -> key: the aggregate's bits with the low 4 mantissa bits replaced
+// by the window position nib = 4a + b (aggregates are >= 0, so keys order like
+// the aggregates, ties broken by the lowest raster position).
+template <int NIB>
+__device__ __forceinline__ float role_key(float v) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(__float_as_uint(v)), "r"(0xfffffff0u), "r"((uint32_t)NIB));
+  return __uint_as_float(d);   // (v & ~15) | NIB in one LOP3
+}
+
+// Geometry of the lane's two pairs against one neighbour record pair q =
+// (pk(q0), pk(q1), |q0|^2, |q1|^2), packed FP32 (nn2 = (|p0|^2, |p1|^2),
+// nnn2 = -nn2): the ARCSIN-row value vs = P_asin(tau) (Table 1, Eq. 7,
+// reading R6), cos c, and -Ph (zero iff a zero vector is involved).
+template <bool TINY = true>
+__device__ __forceinline__ void ang_geo2(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2, uint4 q, f32x2& vs,
+                                         f32x2& c, f32x2& nPh) {
+  const f32x2 Db = pack2(__uint_as_float(__dp4a(pk0, q.x, F2P23_BITS)), __uint_as_float(__dp4a(pk1, q.y, F2P23_BITS)));
+  const f32x2 D = sub2(Db, pack2(F2P23, F2P23));                  // exact dot products
+  const f32x2 nnq = pack2(__uint_as_float(q.z), __uint_as_float(q.w));
+  nPh = mul2(nnn2, nnq);                                           // -Ph, Ph = fl(|p|^2 |q|^2)
+  const f32x2 Pl = fma2(nn2, nnq, nPh);                            // exact residual: P = Ph + Pl
+  const f32x2 Y = fma2(D, D, nPh);                                 // fl(D^2 - Ph)
+  const f32x2 X = sub2(Pl, Y);                                     // |p x q|^2 = fl(fl(Ph - D^2) + Pl)
+  float nph0, nph1;
+  unpack2(nPh, nph0, nph1);
+  const f32x2 r = pack2(rsqrt_approx(-nph0), rsqrt_approx(-nph1)); // 1 / (|p||q|)
+  c = mul2(D, r);                                                  // cos
+  // tau = sqrt(1 - cos) = X / sqrt(X |p|^2 |q|^2 (1 + cos)) = X r rsqrt(X (1 + cos)): no cancellation
+  f32x2 tau;
+  if constexpr (TINY) {
+    const f32x2 Xw = fma2(X, c, add2(X, pack2(1e-30f, 1e-30f)));   // X (1 + cos) (+tiny: X = 0 -> tau = 0)
+    float xw0, xw1;
+    unpack2(Xw, xw0, xw1);
+    tau = mul2(mul2(X, r), pack2(rsqrt_approx(xw0), rsqrt_approx(xw1)));
+  } else {
+    // X = 0 (parallel pair): rsqrt(0) = inf, 0 * inf = NaN -> max(NaN, 0) = 0 (FMNMX on the ALU pipe)
+    const f32x2 Xw = fma2(X, c, X);
+    float xw0, xw1, t0, t1;
+    unpack2(Xw, xw0, xw1);
+    unpack2(mul2(mul2(X, r), pack2(rsqrt_approx(xw0), rsqrt_approx(xw1))), t0, t1);
+    tau = pack2(fmaxf(t0, 0.0f), fmaxf(t1, 0.0f));
+  }
+  vs = horner4x2(coef::ASIN(), tau);
+}
+
+// Exact branch predicate (reading R5) of the two pairs: cos < 0.5 <=> 4 D^2 <
+// |p|^2 |q|^2 <=> fl(D^2 - Ph/4) < Pl/4 (DESIGN.md 5.2's fl(4 D^2 - Ph) < Pl,
+// scaled by the exact factor 1/4; the sign of fl(t - Pl/4) is that of t - Pl/4).
+__device__ __forceinline__ void acos_branch_exact2(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2, uint4 q,
+                                                   bool& a0, bool& a1) {
+  const f32x2 Db = pack2(__uint_as_float(__dp4a(pk0, q.x, F2P23_BITS)), __uint_as_float(__dp4a(pk1, q.y, F2P23_BITS)));
+  const f32x2 D = sub2(Db, pack2(F2P23, F2P23));
+  const f32x2 nnq = pack2(__uint_as_float(q.z), __uint_as_float(q.w));
+  const f32x2 nPh = mul2(nnn2, nnq);
+  const f32x2 Pl = fma2(nn2, nnq, nPh);
+  const f32x2 t = fma2(D, D, mul2(nPh, pack2(0.25f, 0.25f)));
+  const f32x2 u = fma2(Pl, pack2(-0.25f, -0.25f), t);
+  a0 = lo2(u) < 0.0f;
+  a1 = hi2(u) < 0.0f;
+}
+
+// cos within this distance of 0.5 is decided exactly (cos = D rsqrt(Ph) is
+// within ~4 ulp = 5e-7 of the true cosine).
+constexpr float ACOS_AMBIG = 1.0f / 65536.0f;
+
+#ifndef VF_STREAM_ACOS
+#define VF_STREAM_ACOS 0   // ARCCOS-branch strategy (tuning knob), see ang_mm_row
+#endif
+#ifndef VF_STREAM_UNROLL
+#define VF_STREAM_UNROLL 1   // row-loop unrolling (tuning knob)
+#endif
+#ifndef VF_STREAM_TINY
+#define VF_STREAM_TINY 0   // X = 0 guard: 1 = X + 1e-30 (FADD2), 0 = max(tau, 0) (FMNMX, ALU pipe)
+#endif
+
+// Table 1 values (reading R5: ARCCOS row on cos for cos < 0.5, else ARCSIN row
+// on tau) of the lane's two pairs for n neighbour record pairs q[i].
+// VF_STREAM_ACOS 0 (default, measured fastest): both rows for every pair,
+// exact predicate inline, no votes; 1: per offset, the ARCCOS row (~1% of
+// pairs) only when some lane of the warp may need it (one vote); 2: the same
+// with the geometry of all n offsets computed first (independent chains, more
+// registers); 3: both rows for every pair, the branch decided on cos.  With 1, 2
+// and 3, pairs within ACOS_AMBIG of cos = 0.5 set `amb`: the caller then
+// re-decides the whole row exactly (ang_mm_row_exact).
+// ZG: zero vector -> 0.
+template <bool ZG, int N>
+__device__ __forceinline__ void ang_mm_row(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2, const uint4 (&q)[N],
+                                           f32x2 (&v)[N], bool& amb) {
+  auto finish = [&](int i, f32x2 c, f32x2 nPh) {
+    float c0, c1;
+    unpack2(c, c0, c1);
+    amb |= fabsf(c0 - 0.5f) <= ACOS_AMBIG || fabsf(c1 - 0.5f) <= ACOS_AMBIG;
+    if (__any_sync(0xffffffffu, fminf(c0, c1) < 0.5f - ACOS_AMBIG)) {
+      float a0, a1, v0, v1;
+      unpack2(horner4x2(coef::ACOS(), c), a0, a1);                       // Table 1 ARCCOS row
+      unpack2(v[i], v0, v1);
+      v[i] = pack2(c0 < 0.5f - ACOS_AMBIG ? a0 : v0, c1 < 0.5f - ACOS_AMBIG ? a1 : v1);
+    }
+    if (ZG) {
+      float n0, n1, v0, v1;
+      unpack2(nPh, n0, n1);
+      unpack2(v[i], v0, v1);
+      v[i] = pack2(n0 == 0.0f ? 0.0f : v0, n1 == 0.0f ? 0.0f : v1);
+    }
+  };
+  if constexpr (VF_STREAM_ACOS == 2) {
+    f32x2 c[N], nPh[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) ang_geo2(pk0, pk1, nn2, nnn2, q[i], v[i], c[i], nPh[i]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) finish(i, c[i], nPh[i]);
+  } else if constexpr (VF_STREAM_ACOS == 1) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      f32x2 c, nPh;
+      ang_geo2(pk0, pk1, nn2, nnn2, q[i], v[i], c, nPh);
+      finish(i, c, nPh);
+    }
+  } else if constexpr (VF_STREAM_ACOS == 3) {
+    // both rows for every pair (no votes), the branch decided on cos with the
+    // row-level exact fallback for |cos - 0.5| <= ACOS_AMBIG (FSETPs on the ALU
+    // pipe instead of the FMA-pipe exact predicate)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      f32x2 vs, c, nPh;
+      ang_geo2<false>(pk0, pk1, nn2, nnn2, q[i], vs, c, nPh);
+      float c0, c1, a0, a1, s0, s1;
+      unpack2(c, c0, c1);
+      unpack2(horner4x2(coef::ACOS(), c), a0, a1);
+      unpack2(vs, s0, s1);
+      amb |= (c0 >= 0.5f - ACOS_AMBIG && c0 <= 0.5f + ACOS_AMBIG) || (c1 >= 0.5f - ACOS_AMBIG && c1 <= 0.5f + ACOS_AMBIG);
+      s0 = c0 < 0.5f ? a0 : s0;
+      s1 = c1 < 0.5f ? a1 : s1;
+      if (ZG) {
+        float n0, n1;
+        unpack2(nPh, n0, n1);
+        s0 = n0 == 0.0f ? 0.0f : s0;
+        s1 = n1 == 0.0f ? 0.0f : s1;
+      }
+      v[i] = pack2(s0, s1);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      f32x2 vs, c, nPh;
+      ang_geo2<VF_STREAM_TINY>(pk0, pk1, nn2, nnn2, q[i], vs, c, nPh);
+      bool e0, e1;
+      acos_branch_exact2(pk0, pk1, nn2, nnn2, q[i], e0, e1);
+      float a0, a1, s0, s1;
+      unpack2(horner4x2(coef::ACOS(), c), a0, a1);
+      unpack2(vs, s0, s1);
+      s0 = e0 ? a0 : s0;
+      s1 = e1 ? a1 : s1;
+      if (ZG) {
+        float n0, n1;
+        unpack2(nPh, n0, n1);
+        s0 = n0 == 0.0f ? 0.0f : s0;
+        s1 = n1 == 0.0f ? 0.0f : s1;
+      }
+      v[i] = pack2(s0, s1);
+    }
+  }
+}
+
+// The same values with the exact integer branch predicate for every pair
+// (rare: only rows holding a pair with cos within ACOS_AMBIG of 0.5).
+template <int N>
+__device__ __forceinline__ void ang_mm_row_exact(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2,
+                                                 const uint4 (&q)[N], f32x2 (&v)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    f32x2 vs, c, nPh;
+    ang_geo2(pk0, pk1, nn2, nnn2, q[i], vs, c, nPh);
+    bool e0, e1;
+    acos_branch_exact2(pk0, pk1, nn2, nnn2, q[i], e0, e1);
+    float a0, a1, s0, s1, n0, n1;
+    unpack2(horner4x2(coef::ACOS(), c), a0, a1);
+    unpack2(vs, s0, s1);
+    unpack2(nPh, n0, n1);
+    s0 = e0 ? a0 : s0;
+    s1 = e1 ? a1 : s1;
+    v[i] = pack2(n0 == 0.0f ? 0.0f : s0, n1 == 0.0f ? 0.0f : s1);
+  }
+}
+
+// H sums of one neighbourhood row (values a(dx), dx = -2..2; a(0) = 0 for the
+// pixel's own row): H_b = sum_{dx in [-b, 2-b]} a(dx), b = 0, 1, 2.  Packed
+// over the lane's two pixels where both rows are register pairs.
+__device__ __forceinline__ void hrow2(f32x2 am2, f32x2 am1, f32x2 a0, f32x2 ap1, f32x2 ap2, f32x2 (&H)[3]) {
+  const f32x2 m = add2(a0, ap1);
+  const f32x2 n = add2(am1, a0);
+  H[0] = add2(m, ap2);
+  H[1] = add2(m, am1);
+  H[2] = add2(n, am2);
+}
+__device__ __forceinline__ void hrow(float am2, float am1, float a0, float ap1, float ap2, float (&H)[3]) {
+  const float m = a0 + ap1;
+  const float n = am1 + a0;
+  H[0] = m + ap2;
+  H[1] = m + am1;
+  H[2] = n + am2;
+}
+__device__ __forceinline__ void hrow0(float am2, float am1, float ap1, float ap2, float (&H)[3]) {
+  H[0] = ap1 + ap2;
+  H[1] = am1 + ap1;
+  H[2] = am2 + am1;
+}
+
+// nn = |x|^2 (exact integer < 2^18) as float, from the packed pixel.
+__device__ __forceinline__ float nn_of(uint32_t pk) {
+  return __uint_as_float(__dp4a(pk, pk, F2P23_BITS)) - F2P23;
+}
+
+// The lane's two pixels of a row: columns c0, c1 (clamped, replicate padding)
+// are x_lo or x_lo + 1 with x_lo = clamp(x, 0, W - 2), loaded as three aligned
+// words (the third only if it starts inside the input allocation).
+struct PairLoad {
+  int x_lo;          // first column of the loaded pair
+  bool hi0, hi1;     // pixel k = column x_lo + 1
+};
+
+// Raw words of the lane's pair in a row (issued one step ahead: software
+// prefetch of the next row, so the load latency hides behind a step's work).
+struct PairWords {
+  uint32_t w0, w1, w2;
+  int sh;
+};
+__device__ __forceinline__ PairWords ld_pair_words(const uint8_t* row, const PairLoad& pl, const uint8_t* in_end) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(row) + 3 * pl.x_lo;
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+  PairWords r;
+  r.w0 = __ldg(w);
+  r.w1 = __ldg(w + 1);
+  // (an aligned word holding a byte of the allocation never leaves it)
+  r.w2 = reinterpret_cast<const uint8_t*>(w + 2) < in_end ? __ldg(w + 2) : 0u;
+  r.sh = (int)(a & 3) * 8;
+  return r;
+}
+__device__ __forceinline__ void unpack_pair(const PairWords& r, const PairLoad& pl, uint32_t& p0, uint32_t& p1) {
+  const uint32_t lo = __funnelshift_r(r.w0, r.w1, r.sh);        // bytes 3 x_lo .. + 3
+  const uint32_t hi = __funnelshift_r(r.w1, r.w2, r.sh);        // bytes 3 x_lo + 4 .. + 7
+  const uint32_t q0 = lo & 0x00ffffffu;
+  const uint32_t q1 = __byte_perm(lo, hi, 0x0543) & 0x00ffffffu;
+  p0 = pl.hi0 ? q1 : q0;
+  p1 = pl.hi1 ? q1 : q0;
+}
+
+// grid (ceil(W / 58), ceil(out_rows / (K NWARP)), B), block 32 NWARP; dynamic
+// smem NWARP * sizeof(Ring).  Warp w of block (sx, sy) streams strip sx over
+// output rows [out_row0 + (sy NWARP + w) K, + K).  Requires W >= 2.
+#ifndef VF_STREAM_MINB
+#define VF_STREAM_MINB 5   // resident blocks per SM the registers are held to (5: <= 102 registers, 20 warps)
+#endif
+template <int VAR>
+__global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular_stream_kernel(const Launch L, int K) {
+  using namespace stream;
+  static_assert(VAR == MINIMAX, "streamed kernel: minimax variant");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
+  Ring& R = reinterpret_cast<Ring*>(smem_raw)[warp];
+  const int b = blockIdx.z;
+  const int x0 = strip_x0(blockIdx.x);
+  const int ty0 = L.out_row0 + (blockIdx.y * NWARP + warp) * K;
+  const int ty1 = min(ty0 + K, L.out_row0 + L.out_rows);
+  if (ty0 >= ty1) return;                                       // warp-uniform
+  const int W = L.W;
+  const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
+  const uint8_t* in_end = L.in + (long long)(gridDim.z - 1) * L.in_stride + (long long)L.band_rows * W * 3;
+  const int xa = x0 + 2 * l;                                    // image column of the lane's first pixel
+  PairLoad pl;
+  pl.x_lo = clampi(xa, 0, W - 2);
+  pl.hi0 = clampi(xa, 0, W - 1) != pl.x_lo;
+  pl.hi1 = clampi(xa + 1, 0, W - 1) != pl.x_lo;
+  // output columns: strip j = 2l + k, valid for j in [3, 60] inside the image
+  const bool ov0 = 2 * l >= J_LO && 2 * l < J_LO + SOUT && xa < W;
+  const bool ov1 = 2 * l + 1 >= J_LO && 2 * l + 1 < J_LO + SOUT && xa + 1 < W;
+  const int rowb = W * 3;
+
+  // carried partial role sums (packed over the lane's two pixels):
+  // U = H(-1) + H(0) and Z = H(0) of the previous row's pixels (-> role a = 1
+  // and the partial W), Wp = H(0) + H(+1) of the row before (-> role a = 0)
+  f32x2 U[3], Z[3], Wp[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) U[i] = Z[i] = Wp[i] = 0ull;
+  uint32_t zhist = 0;                                           // zero-vector flags of the last 3 staged rows
+
+  auto row_ptr = [&](int r) {
+    return in + (long long)(clampi(r, L.band_row0, L.band_row0 + L.band_rows - 1) - L.band_row0) * rowb;
+  };
+  PairWords nxt = ld_pair_words(row_ptr(ty0 - 1), pl, in_end);
+  constexpr int kUnroll = VF_STREAM_UNROLL;
+#pragma unroll (kUnroll)
+  for (int r = ty0 - 1; r <= ty1; ++r) {
+    const int slot = r & (SLOTS - 1);
+    // ---- a1/a2: stage row r (loaded one step ahead), prefetch row r + 1 -------
+    const PairWords cur = nxt;
+    nxt = ld_pair_words(row_ptr(r + 1), pl, in_end);
+    uint32_t pk0, pk1;
+    unpack_pair(cur, pl, pk0, pk1);
+    const float nn0 = nn_of(pk0), nn1 = nn_of(pk1);
+    const uint32_t pk2 = __shfl_down_sync(0xffffffffu, pk0, 1);  // column 2l + 2 (lane 31: unused)
+    const float nn2n = __shfl_down_sync(0xffffffffu, nn0, 1);
+    R.E[slot][l + 1] = make_uint4(pk0, pk1, __float_as_uint(nn0), __float_as_uint(nn1));
+    R.O[slot][l + 1] = make_uint4(pk1, pk2, __float_as_uint(nn1), __float_as_uint(nn2n));
+    *reinterpret_cast<uint2*>(&R.P[slot][2 * l + 2]) = make_uint2(pk0, pk1);
+    zhist = ((zhist << 1) | (__any_sync(0xffffffffu, nn0 == 0.0f || nn1 == 0.0f) ? 1u : 0u)) & 7u;
+    __syncwarp();
+
+    const f32x2 nn2 = pack2(nn0, nn1), nnn2 = pack2(-nn0, -nn1);
+    const int s1 = (r - 1) & (SLOTS - 1), s2 = (r - 2) & (SLOTS - 1);
+    auto nbr = [&](int sl, int dx) -> uint4 {
+      // neighbour pair (columns 2l + dx, 2l + 1 + dx)
+      return (dx & 1) ? R.O[sl][l + ((dx - 1) >> 1) + 1] : R.E[sl][l + (dx >> 1) + 1];
+    };
+    // ---- a4/a5 + a6, one neighbourhood row at a time ---------------------------
+    // v[dxi]: the lane's pair values with offset (dy, dx = dxi - 2)
+    auto eval_row = [&](int sl, auto& v) {
+      constexpr int N = sizeof(v) / sizeof(v[0]);
+      uint4 q[N];
+#pragma unroll
+      for (int dxi = 0; dxi < N; ++dxi) q[dxi] = nbr(sl, dxi - 2);
+      bool amb = false;
+      if (zhist == 0u) ang_mm_row<false, N>(pk0, pk1, nn2, nnn2, q, v, amb);
+      else ang_mm_row<true, N>(pk0, pk1, nn2, nnn2, q, v, amb);
+      if (VF_STREAM_ACOS != 0 && __any_sync(0xffffffffu, amb)) ang_mm_row_exact<N>(pk0, pk1, nn2, nnn2, q, v);
+    };
+    // rows r - d (d = 2, then 1): the partner pixels' H(+d) from values of row r
+    // pixels with offset (-d, dx), partly from the adjacent lanes
+    auto partner_rows = [&](const f32x2 (&v)[5], float (&H0)[3], float (&H1)[3]) {
+      const float p_p2_0 = __shfl_up_sync(0xffffffffu, lo2(v[4]), 1);   // lane l-1: q0, offset (-d, +2)
+      const float p_p1_1 = __shfl_up_sync(0xffffffffu, hi2(v[3]), 1);   // lane l-1: q1, offset (-d, +1)
+      const float p_p2_1 = __shfl_up_sync(0xffffffffu, hi2(v[4]), 1);   // lane l-1: q1, offset (-d, +2)
+      const float n_m2_0 = __shfl_down_sync(0xffffffffu, lo2(v[0]), 1); // lane l+1: q0, offset (-d, -2)
+      const float n_m1_0 = __shfl_down_sync(0xffffffffu, lo2(v[1]), 1); // lane l+1: q0, offset (-d, -1)
+      const float n_m2_1 = __shfl_down_sync(0xffffffffu, hi2(v[0]), 1); // lane l+1: q1, offset (-d, -2)
+      hrow(p_p2_0, p_p1_1, lo2(v[2]), hi2(v[1]), n_m2_0, H0);          // pixel (r - d, 2l)
+      hrow(p_p2_1, lo2(v[3]), hi2(v[2]), n_m1_0, n_m2_1, H1);          // pixel (r - d, 2l + 1)
+    };
+    f32x2 Hm2[3], Hm1[3], H0[3];
+    f32x2 R0[3], R1[3], R2[3];   // roles a = 0 (row r - 2), 1 (row r - 1), 2 (row r), b = 0..2
+    {
+      f32x2 v[5];
+      eval_row(s2, v);                                          // dy = -2
+      hrow2(v[0], v[1], v[2], v[3], v[4], Hm2);
+      float Ha[3], Hb[3];
+      partner_rows(v, Ha, Hb);
+#pragma unroll
+      for (int bb = 0; bb < 3; ++bb) R0[bb] = add2(Wp[bb], pack2(Ha[bb], Hb[bb]));
+    }
+    {
+      f32x2 v[5];
+      eval_row(s1, v);                                          // dy = -1
+      hrow2(v[0], v[1], v[2], v[3], v[4], Hm1);
+      float Ha[3], Hb[3];
+      partner_rows(v, Ha, Hb);
+#pragma unroll
+      for (int bb = 0; bb < 3; ++bb) {
+        const f32x2 Hp1 = pack2(Ha[bb], Hb[bb]);
+        R1[bb] = add2(U[bb], Hp1);
+        Wp[bb] = add2(Z[bb], Hp1);
+      }
+    }
+    {
+      f32x2 v[2];
+      eval_row(slot, v);                                        // dy = 0, dx = -2, -1
+      // right values from (q1, lane l+1)
+      const float n_m1_0 = __shfl_down_sync(0xffffffffu, lo2(v[1]), 1);
+      const float n_m2_0 = __shfl_down_sync(0xffffffffu, lo2(v[0]), 1);
+      const float n_m2_1 = __shfl_down_sync(0xffffffffu, hi2(v[0]), 1);
+      float Ha[3], Hb[3];
+      hrow0(lo2(v[0]), lo2(v[1]), hi2(v[1]), n_m2_0, Ha);
+      hrow0(hi2(v[0]), hi2(v[1]), n_m1_0, n_m2_1, Hb);
+#pragma unroll
+      for (int bb = 0; bb < 3; ++bb) {
+        H0[bb] = pack2(Ha[bb], Hb[bb]);
+        U[bb] = add2(Hm1[bb], H0[bb]);
+        Z[bb] = H0[bb];
+        R2[bb] = add2(U[bb], Hm2[bb]);
+      }
+    }
+
+    // ---- a7/a8: the window centred at row r - 1 --------------------------------
+    const int gy = r - 1;
+    if (gy >= ty0) {
+      // keys: window 2l uses (lane l-1: q1, b = 0), (q0, b = 1), (q1, b = 2);
+      // window 2l + 1 uses (q0, b = 0), (q1, b = 1), (lane l+1: q0, b = 2)
+      const float k00 = __shfl_up_sync(0xffffffffu, role_key<0>(hi2(R0[0])), 1);
+      const float k10 = __shfl_up_sync(0xffffffffu, role_key<4>(hi2(R1[0])), 1);
+      const float k20 = __shfl_up_sync(0xffffffffu, role_key<8>(hi2(R2[0])), 1);
+      const float m02 = __shfl_down_sync(0xffffffffu, role_key<2>(lo2(R0[2])), 1);
+      const float m12 = __shfl_down_sync(0xffffffffu, role_key<6>(lo2(R1[2])), 1);
+      const float m22 = __shfl_down_sync(0xffffffffu, role_key<10>(lo2(R2[2])), 1);
+      const float kw0 = fmin3(fmin3(k00, role_key<1>(lo2(R0[1])), role_key<2>(hi2(R0[2]))),
+                              fmin3(k10, role_key<5>(lo2(R1[1])), role_key<6>(hi2(R1[2]))),
+                              fmin3(k20, role_key<9>(lo2(R2[1])), role_key<10>(hi2(R2[2]))));
+      const float kw1 = fmin3(fmin3(role_key<0>(lo2(R0[0])), role_key<1>(hi2(R0[1])), m02),
+                              fmin3(role_key<4>(lo2(R1[0])), role_key<5>(hi2(R1[1])), m12),
+                              fmin3(role_key<8>(lo2(R2[0])), role_key<9>(hi2(R2[1])), m22));
+      const uint32_t nib0 = __float_as_uint(kw0) & 15u, nib1 = __float_as_uint(kw1) & 15u;
+      // selected samples: row r - 2 + a, strip column (2l + k) - 1 + b
+      const uint32_t* prow0 = R.P[(r - 2) & (SLOTS - 1)];
+      const uint32_t* prow1 = R.P[(r - 1) & (SLOTS - 1)];
+      const uint32_t* prow2 = R.P[slot];
+      auto pick = [&](uint32_t nib, int k) -> uint32_t {
+        const uint32_t a = nib >> 2;
+        const uint32_t* pr = a == 0 ? prow0 : (a == 1 ? prow1 : prow2);
+        return pr[2 * l + k + 1 + (int)(nib & 3u)];
+      };
+      const uint32_t o0 = pick(nib0, 0), o1 = pick(nib1, 1);
+      // a8: 6 bytes per lane, predicated stores (no divergence)
+      uint8_t* op = L.out + (long long)b * L.out_stride + ((long long)(gy - L.out_row0) * W + xa) * 3;
+      if (((uintptr_t)op & 1u) == 0) {                          // warp-uniform: U16, U8 U8, U16
+        if (ov0) *reinterpret_cast<uint16_t*>(op) = (uint16_t)o0;
+        if (ov0) op[2] = (uint8_t)(o0 >> 16);
+        if (ov1) op[3] = (uint8_t)o1;
+        if (ov1) *reinterpret_cast<uint16_t*>(op + 4) = (uint16_t)(o1 >> 8);
+      } else {                                                  // U8, U16, U16, U8
+        if (ov0) op[0] = (uint8_t)o0;
+        if (ov0) *reinterpret_cast<uint16_t*>(op + 1) = (uint16_t)(o0 >> 8);
+        if (ov1) *reinterpret_cast<uint16_t*>(op + 3) = (uint16_t)o1;
+        if (ov1) op[5] = (uint8_t)(o1 >> 16);
+      }
+      if (L.idx || L.agg) {
+        // parity runs only: the index (raster 3a + b) and the exact aggregates
+        const float f00 = __shfl_up_sync(0xffffffffu, hi2(R0[0]), 1), f10 = __shfl_up_sync(0xffffffffu, hi2(R1[0]), 1),
+                    f20 = __shfl_up_sync(0xffffffffu, hi2(R2[0]), 1);
+        const float g02 = __shfl_down_sync(0xffffffffu, lo2(R0[2]), 1), g12 = __shfl_down_sync(0xffffffffu, lo2(R1[2]), 1),
+                    g22 = __shfl_down_sync(0xffffffffu, lo2(R2[2]), 1);
+        const long long npix_img = (long long)L.out_rows * W;
+        const long long po = (long long)(gy - L.out_row0) * W + xa;
+        if (ov0) {
+          if (L.idx) L.idx[b * npix_img + po] = (uint8_t)(3 * (nib0 >> 2) + (nib0 & 3u));
+          if (L.agg) {
+            float* ag = L.agg + (b * npix_img + po) * 9;
+            ag[0] = f00; ag[1] = lo2(R0[1]); ag[2] = hi2(R0[2]);
+            ag[3] = f10; ag[4] = lo2(R1[1]); ag[5] = hi2(R1[2]);
+            ag[6] = f20; ag[7] = lo2(R2[1]); ag[8] = hi2(R2[2]);
+          }
+        }
+        if (ov1) {
+          if (L.idx) L.idx[b * npix_img + po + 1] = (uint8_t)(3 * (nib1 >> 2) + (nib1 & 3u));
+          if (L.agg) {
+            float* ag = L.agg + (b * npix_img + po + 1) * 9;
+            ag[0] = lo2(R0[0]); ag[1] = hi2(R0[1]); ag[2] = g02;
+            ag[3] = lo2(R1[0]); ag[4] = hi2(R1[1]); ag[5] = g12;
+            ag[6] = lo2(R2[0]); ag[7] = hi2(R2[1]); ag[8] = g22;
+          }
+        }
+      }
+    }
+    __syncwarp();   // ring slot (r + 1) & 3 = (r - 3) & 3 is no longer read
+  }
+}
+
+#ifndef VF_ANGULAR_MM_TU
+const void* stream_kernel_fn_mm();
+#endif
+
+inline size_t stream_smem_bytes() { return sizeof(stream::Ring) * stream::NWARP; }
+
+// rows per warp: long tiles (less vertical halo: K + 2 steps for K rows) when
+// the launch has enough strips to fill the GPU, shorter ones for small images
+inline int stream_rows_per_warp(long long strips_total_times_rows) {
+  const long long target_warps = 148LL * 32 * 2;   // two waves of 32 warps per SM
+  int K = 64;
+  while (K > 8 && strips_total_times_rows / K < target_warps) K >>= 1;
+  return K;
+}
+
+inline dim3 stream_grid(const Launch& L, int B, int K) {
+  using namespace stream;
+  return dim3((L.W + SOUT - 1) / SOUT, (L.out_rows + K * NWARP - 1) / (K * NWARP), B);
+}
+
+}  // namespace vf

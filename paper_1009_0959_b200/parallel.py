@@ -4,9 +4,11 @@
 The filter is embarrassingly parallel: every output pixel depends only on its
 (2r+1)^2 input neighbourhood, so there is no exchange on the data path.
 * Batch sharding (BASELINE config 3 / C4): rank r filters images
-  [r B / k, (r+1) B / k); the per-image statistics of all filters against the
-  reference filter come from ONE fused pass (vf_image_stats_multi) and cross
-  ranks in ONE all_gather (B x filters x 8 doubles).
+  [r B / k, (r+1) B / k); the per-image statistics of the outputs against
+  their references (e.g. each minimax filter against the exact one of its
+  criterion, the paper's fidelity measure) come from one fused pass per
+  reference (vf_image_stats_multi) and cross ranks in ONE all_gather
+  (B x comparisons x 8 doubles).
 * Row stripes (config 4 / C5): rank r owns output rows [r H / k, (r+1) H / k)
   and reads them plus w//2 halo rows on each interior side (clamped at the
   global border); the output is gathered in row chunks, the all_gather of
@@ -81,24 +83,37 @@ def all_gather_rows(local: torch.Tensor, counts: Sequence[int], group=None) -> t
     return torch.cat([out[i * m: i * m + counts[i]] for i in range(world)])
 
 
+def gather_group_stats(outs: dict, B: int, groups, group=None, stats_fn: Callable = _cuda_stats_multi):
+    """Per-image statistics of output groups against their references, all
+    ranks' images in batch order: groups = [(reference combo, [combo, ...]),
+    ...] -> {(reference, combo): [B, 8] float64}.  One fused stats pass per
+    group (stats_fn(ref, [outs...]) -> [n, B_local, 8]) and ONE all_gather of
+    [B_local, sum n, 8]: the only cross-rank traffic of the batch path."""
+    world = dist.get_world_size(group)
+    counts = [shard_range(B, world, r)[1] - shard_range(B, world, r)[0] for r in range(world)]
+    keys, parts = [], []
+    for ref, cs in groups:
+        ref = tuple(ref)
+        cs = [tuple(c) for c in cs]
+        keys += [(ref, c) for c in cs]
+        a = outs[ref]
+        if a.shape[0] > 0:
+            parts.append(stats_fn(a, [outs[c] for c in cs]).to(torch.float64))     # [n, B_local, 8]
+        else:
+            parts.append(torch.zeros((len(cs), 0, 8), dtype=torch.float64, device=a.device))
+    s = torch.cat(parts) if len(parts) > 1 else parts[0]
+    g = all_gather_rows(s.permute(1, 0, 2).contiguous(), counts, group)   # [B, N, 8]
+    return {k: g[:, i] for i, k in enumerate(keys)}
+
+
 def gather_batch_stats(outs: dict, B: int, combos, reference: Optional[Tuple] = None, group=None,
                        stats_fn: Callable = _cuda_stats_multi):
     """Per-image statistics of every filter's local outputs against the
     `reference` combo's (default: the first), all_gathered over the ranks in
-    batch order: {combo: [B, 8] float64}.  One stats pass over the reference
-    (stats_fn(ref, [outs...]) -> [n, B_local, 8]) and ONE all_gather of
-    [B_local, n, 8]: the only cross-rank traffic of the batch path."""
-    world = dist.get_world_size(group)
-    counts = [shard_range(B, world, r)[1] - shard_range(B, world, r)[0] for r in range(world)]
+    batch order: {combo: [B, 8] float64} (one stats pass, one all_gather)."""
     ref = tuple(reference) if reference is not None else tuple(combos[0])
-    keys = [tuple(c) for c in combos]
-    a = outs[ref]
-    if a.shape[0] > 0:
-        s = stats_fn(a, [outs[c] for c in keys]).to(torch.float64)          # [n, B_local, 8]
-    else:
-        s = torch.zeros((len(keys), 0, 8), dtype=torch.float64, device=a.device)
-    g = all_gather_rows(s.permute(1, 0, 2).contiguous(), counts, group)   # [B, n, 8]
-    return {c: g[:, i] for i, c in enumerate(keys)}
+    res = gather_group_stats(outs, B, [(ref, [tuple(c) for c in combos])], group, stats_fn)
+    return {c: v for (_, c), v in res.items()}
 
 
 def run_batch_sharded(imgs_local: torch.Tensor, B: int, window: int, combos, reference: Optional[Tuple] = None,

@@ -19,12 +19,13 @@ LIB_PATH = os.environ.get("VF_LIB") or os.path.join(HERE, "libvf.so")
 VF_ANGULAR, VF_EXP, VF_LOG, VF_AMNFE, VF_AMNFG, VF_EVMF = 0, 1, 2, 3, 4, 5
 VF_EXACT, VF_MINIMAX, VF_MINIMAX_POLY4, VF_MINIMAX_REACH = 0, 1, 2, 3
 VF_OK, VF_EINVAL, VF_EUNSUPPORTED, VF_ECUDA = 0, -1, -2, -3
-VF_ALGO_AUTO, VF_ALGO_WINDOW, VF_ALGO_SHARED, VF_ALGO_ROLE, VF_ALGO_NO_TMA = 0, 1, 2, 3, 16
+VF_ALGO_AUTO, VF_ALGO_WINDOW, VF_ALGO_SHARED, VF_ALGO_ROLE, VF_ALGO_NO_TMA, VF_ALGO_STREAM = 0, 1, 2, 3, 16, 32
 
 CRITERIA = {"angular": VF_ANGULAR, "exp": VF_EXP, "log": VF_LOG, "amnfe": VF_AMNFE, "amnfg": VF_AMNFG,
             "evmf": VF_EVMF}
 VARIANTS = {"exact": VF_EXACT, "minimax": VF_MINIMAX, "poly4": VF_MINIMAX_POLY4, "reach": VF_MINIMAX_REACH}
-ALGOS = {"auto": VF_ALGO_AUTO, "window": VF_ALGO_WINDOW, "shared": VF_ALGO_SHARED, "role": VF_ALGO_ROLE}
+ALGOS = {"auto": VF_ALGO_AUTO, "window": VF_ALGO_WINDOW, "shared": VF_ALGO_SHARED, "role": VF_ALGO_ROLE,
+         "stream": VF_ALGO_STREAM}
 EXPORTS = ["vf_filter", "vf_filter_batch", "vf_filter_rows", "vf_filter_batch_algo",
            "vf_host_workspace_bytes", "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_destroy",
            "vf_image_stats", "vf_image_stats_ex", "vf_image_stats_multi", "vf_kernel_info", "vf_status_string", "vf_last_error", "vf_version"]

@@ -32,13 +32,15 @@ def gpu_full(img_np, w, crit, var, algo="auto"):
 
 
 def full_parity(img_np, w, crit, var, algo=None):
-    """Every kernel variant is checked unless `algo` is given: angular per-window
-    and pair-sharing with each region height (1..3 pixels per thread); exp/log
-    with 1 and (3x3) 2 output rows per thread."""
+    """Every kernel variant is checked unless `algo` is given: angular default
+    (3x3 minimax: the warp-streamed kernel), per-window and pair-sharing with
+    each region height (1..3 pixels per thread); exp/log with 1 and (3x3) 2
+    output rows per thread."""
     if algo:
         algos = [algo]
     elif crit == "angular":
-        algos = ["window", "shared", "shared:1", "shared:2", "shared:3", "role", "role:1", "role:2", "role:3"]
+        algos = ["auto", "stream", "window", "shared", "shared:1", "shared:2", "shared:3", "role", "role:1",
+                 "role:2", "role:3"]
     else:
         # tile bits force the TMA-staged kernel where the rows allow it (3W % 16 == 0);
         # "+notma" the plain-load one

@@ -1,7 +1,11 @@
-"""Quick per-kernel timing (CUDA events, median of N launches, L2 flushed) for
-tuning iterations: python tools/kbench.py [C2 C3 C4 ...] [--algo window|shared]"""
+"""Quick per-kernel timing for tuning iterations (CUDA events over back-to-back
+launches on inputs larger than L2):
+
+    python tools/kbench.py [--images 128] [--only angular/minimax] [--algo auto] [--c3] [--reps 5]
+
+VF_LIB=path/to/libvf_variant.so selects a library build (A/B comparisons)."""
+import argparse
 import os
-import statistics
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -11,47 +15,29 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_1009_0959_b200 as vfb  # noqa: E402
 
-args = sys.argv[1:]
-skip = {i + 1 for i, a in enumerate(args) if a in ("--algo", "--only")}
-cfgs = [a for i, a in enumerate(args) if not a.startswith("--") and i not in skip] or ["C2", "C4", "C3"]
-algo = "auto"
-if "--algo" in sys.argv:
-    algo = sys.argv[sys.argv.index("--algo") + 1]
-only = None
-if "--only" in sys.argv:
-    only = sys.argv[sys.argv.index("--only") + 1]
-flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-for cfg in cfgs:
-    spec, w = bench.workload(cfg)
-    x = torch.from_numpy(bench.make_input(spec, 0)).cuda()
+ap = argparse.ArgumentParser()
+ap.add_argument("--images", type=int, default=128)
+ap.add_argument("--only", default=None)
+ap.add_argument("--algo", default="auto")
+ap.add_argument("--c3", action="store_true")
+ap.add_argument("--reps", type=int, default=5)
+a = ap.parse_args()
+dev = torch.device("cuda")
+stream = torch.cuda.current_stream()
+peak = 2 * 128 * 148 * 1.965e9 / 1e12
+tag = os.path.basename(os.environ.get("VF_LIB", "libvf.so"))
+for cfg, w, ids in (("C4", 3, range(a.images)),) + ((("C3", 5, range(8)),) if a.c3 else ()):
+    x = torch.from_numpy(bench.gen_batch(cfg, ids)).to(dev)
     npix = x.numel() // 3
     out = torch.empty_like(x)
     n = w * w
     pairs = n * (n - 1) // 2
-    line = [f"{cfg}({w}x{w},{npix/1e6:.1f}Mpx)"]
-    combos = [c for c in bench.COMBOS + bench.REACH_COMBOS if not only or only in f"{c[0]}/{c[1]}"]
-    outs = [torch.empty_like(x) for _ in combos]
-    if algo == "auto":
-        # average launch duration over back-to-back launches (bench.steady_kernel_ms)
-        sms, R = bench.steady_kernel_ms(vfb, torch, torch.device("cuda"), torch.cuda.current_stream(), flush, x, w,
-                                        combos, outs)
-    for c in combos:
-        if algo == "auto":
-            ms = sms[c]
-        else:
-            for _ in range(3):
-                vfb.vf_filter_batch_algo(x, w, *c, algo, out=out)
-            ts = []
-            for _ in range(9):
-                flush.fill_(1)
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record()
-                vfb.vf_filter_batch_algo(x, w, *c, algo, out=out)
-                b.record()
-                torch.cuda.synchronize()
-                ts.append(a.elapsed_time(b))
-            ms = statistics.median(ts)
-        frac = bench.FLOPS_PER_PAIR[c] * pairs * npix / (ms / 1e3) / 1e12 / bench.NOMINAL_FP32_TFLOPS_AT_MAX
-        line.append(f"{c[0][:3]}/{c[1][:3]} {ms*1e3:8.1f}us {frac*100:4.1f}%")
+    line = [f"{tag} {cfg}({w}x{w},{npix / 1e6:.0f}Mpx)"]
+    for c in bench.COMBOS + bench.REACH_COMBOS:
+        if a.only and a.only not in f"{c[0]}/{c[1]}":
+            continue
+        ms = bench.kernel_avg_ms(torch, dev, stream,
+                                 lambda c=c: vfb.vf_filter_batch_algo(x, w, *c, a.algo, out=out, stream=stream), a.reps)
+        frac = bench.FLOPS_PER_PAIR[c] * pairs * npix / (ms / 1e3) / 1e12 / peak
+        line.append(f"{c[0][:3]}/{c[1][:3]} {ms * 1e3:8.1f}us {frac * 100:4.1f}%")
     print(" | ".join(line), flush=True)
