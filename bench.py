@@ -262,23 +262,39 @@ def cpu_model() -> str:
 
 
 def lib_sha256(path):
-    h = hashlib.sha256()
+    """sha256 of the library's device code (the ELF .nv_fatbin section: the
+    compiled kernels; bit-reproducible across relinks, unlike the whole .so)."""
+    import struct
     with open(path, "rb") as fh:
-        for blk in iter(lambda: fh.read(1 << 20), b""):
-            h.update(blk)
-    return h.hexdigest()
+        data = fh.read()
+    try:
+        shoff, = struct.unpack_from("<Q", data, 0x28)
+        shentsize, shnum, shstrndx = struct.unpack_from("<HHH", data, 0x3A)
+        def sec(i):
+            name, _, _, _, off, size = struct.unpack_from("<IIQQQQ", data, shoff + i * shentsize)
+            return name, off, size
+        _, stroff, _ = sec(shstrndx)
+        for i in range(shnum):
+            name, off, size = sec(i)
+            nm = data[stroff + name: data.index(b"\0", stroff + name)]
+            if nm == b".nv_fatbin":
+                return hashlib.sha256(data[off: off + size]).hexdigest()
+    except (struct.error, ValueError):
+        pass
+    return hashlib.sha256(data).hexdigest()
 
 
 def load_ncu_exec(sha):
     """profiles/ncu_exec.json (tools/ncu_exec.py): per-kernel ncu pipe
-    utilisations captured from a libvf.so; used only if it is THIS library."""
+    utilisations captured from a libvf.so; used only if its device code is
+    THIS library's (lib_sha256)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_exec.json")) as fh:
             d = json.load(fh)
     except Exception:
         return None, "profiles/ncu_exec.json absent"
     if d.get("libvf_sha256") != sha:
-        return None, "profiles/ncu_exec.json was captured from another libvf.so build (stale): not used"
+        return None, "profiles/ncu_exec.json was captured from other device code (stale): not used"
     return d, "profiles/ncu_exec.json (%s), same libvf.so sha256" % d.get("command", "?")
 
 
