@@ -210,7 +210,7 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
     const int K = (k_env >= 2 && k_env <= 1024) ? k_env : vf::stream_rows_per_warp(strips * out_rows * (long long)B);
     kd->fn = vf::stream_kernel_fn_mm();
     kd->grid = vf::stream_grid(L, B, K);
-    kd->block = dim3(32 * vf::stream::NWARP);
+    kd->block = dim3(vf::stream_block_threads());
     kd->smem = vf::stream_smem_bytes();
     kd->stream_k = K;
     if (kd->grid.y > 65535 || kd->grid.z > 65535) return fail(VF_EINVAL, "grid too large");

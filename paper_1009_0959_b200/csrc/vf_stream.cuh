@@ -51,14 +51,25 @@ constexpr int SOUT = 58;        // output columns per strip: [3, 61)
 constexpr int NE = 34;          // even-aligned record pairs per ring row: columns (2e - 2, 2e - 1), e = 0..33
 constexpr int NO = 33;          // odd-aligned record pairs: columns (2o - 1, 2o), o = 0..32
 constexpr int SLOTS = 4;        // ring rows (rows r, r-1, r-2 in use)
-constexpr int NWARP = 4;        // warps per block (independent strips / row tiles)
+#ifndef VF_STREAM_NWARP
+#define VF_STREAM_NWARP 1   // warps per block: 1 measured fastest (C4: 1591 vs 1662 us for 4 per 256 images)
+#endif
+constexpr int NWARP = VF_STREAM_NWARP;   // warps per block (independent strips / row tiles)
 
 constexpr int PW = SW + 8;      // plain pixel row: strip column j at index j + 2
+
+#ifndef VF_STREAM_RN
+#define VF_STREAM_RN 0   // 1: per-pixel 1/|x| in the ring, r = rn_p rn_q by FMUL2 instead of MUFU.RSQ(Ph)
+#endif
 
 struct Ring {
   uint4 E[SLOTS][NE];           // (pk(2e-2), pk(2e-1), |x|^2, |x|^2)
   uint4 O[SLOTS][NO];           // (pk(2o-1), pk(2o),   |x|^2, |x|^2)
   uint32_t P[SLOTS][PW];        // packed pixels (the selected sample is read back from here)
+#if VF_STREAM_RN
+  uint2 ER[SLOTS][NE];          // (1/|x|, 1/|x|) of the E pairs
+  uint2 OR[SLOTS][NO];          // of the O pairs
+#endif
 };
 // Columns -2, -1, 64 and 65 of E / O (lanes 0 and 31, offsets |dx| >= 1) are
 // never written: the pair values that read them only feed the roles of strip
@@ -99,7 +110,7 @@ __device__ __forceinline__ float role_key(float v) {
 // reading R6), cos c, and -Ph (zero iff a zero vector is involved).
 template <bool TINY = true>
 __device__ __forceinline__ void ang_geo2(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2, uint4 q, f32x2& vs,
-                                         f32x2& c, f32x2& nPh) {
+                                         f32x2& c, f32x2& nPh, const f32x2* rin = nullptr) {
   const f32x2 Db = pack2(__uint_as_float(__dp4a(pk0, q.x, F2P23_BITS)), __uint_as_float(__dp4a(pk1, q.y, F2P23_BITS)));
   const f32x2 D = sub2(Db, pack2(F2P23, F2P23));                  // exact dot products
   const f32x2 nnq = pack2(__uint_as_float(q.z), __uint_as_float(q.w));
@@ -109,7 +120,8 @@ __device__ __forceinline__ void ang_geo2(uint32_t pk0, uint32_t pk1, f32x2 nn2, 
   const f32x2 X = sub2(Pl, Y);                                     // |p x q|^2 = fl(fl(Ph - D^2) + Pl)
   float nph0, nph1;
   unpack2(nPh, nph0, nph1);
-  const f32x2 r = pack2(rsqrt_approx(-nph0), rsqrt_approx(-nph1)); // 1 / (|p||q|)
+  // 1 / (|p||q|): MUFU.RSQ of Ph, or the product of the per-pixel 1/|x| (rin)
+  const f32x2 r = rin ? *rin : pack2(rsqrt_approx(-nph0), rsqrt_approx(-nph1));
   c = mul2(D, r);                                                  // cos
   // tau = sqrt(1 - cos) = X / sqrt(X |p|^2 |q|^2 (1 + cos)) = X r rsqrt(X (1 + cos)): no cancellation
   f32x2 tau;
@@ -171,7 +183,7 @@ constexpr float ACOS_AMBIG = 1.0f / 65536.0f;
 // ZG: zero vector -> 0.
 template <bool ZG, int N>
 __device__ __forceinline__ void ang_mm_row(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2, const uint4 (&q)[N],
-                                           f32x2 (&v)[N], bool& amb) {
+                                           f32x2 (&v)[N], bool& amb, const f32x2* rr = nullptr) {
   auto finish = [&](int i, f32x2 c, f32x2 nPh) {
     float c0, c1;
     unpack2(c, c0, c1);
@@ -229,7 +241,7 @@ __device__ __forceinline__ void ang_mm_row(uint32_t pk0, uint32_t pk1, f32x2 nn2
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       f32x2 vs, c, nPh;
-      ang_geo2<VF_STREAM_TINY>(pk0, pk1, nn2, nnn2, q[i], vs, c, nPh);
+      ang_geo2<VF_STREAM_TINY>(pk0, pk1, nn2, nnn2, q[i], vs, c, nPh, rr ? &rr[i] : nullptr);
       bool e0, e1;
       acos_branch_exact2(pk0, pk1, nn2, nnn2, q[i], e0, e1);
       float a0, a1, s0, s1;
@@ -335,7 +347,7 @@ __device__ __forceinline__ void unpack_pair(const PairWords& r, const PairLoad& 
 // smem NWARP * sizeof(Ring).  Warp w of block (sx, sy) streams strip sx over
 // output rows [out_row0 + (sy NWARP + w) K, + K).  Requires W >= 2.
 #ifndef VF_STREAM_MINB
-#define VF_STREAM_MINB 5   // resident blocks per SM the registers are held to (5: <= 102 registers, 20 warps)
+#define VF_STREAM_MINB (20 / VF_STREAM_NWARP)   // resident blocks per SM: 20 warps per SM, <= 102 registers
 #endif
 template <int VAR>
 __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular_stream_kernel(const Launch L, int K) {
@@ -383,16 +395,27 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
     nxt = ld_pair_words(row_ptr(r + 1), pl, in_end);
     uint32_t pk0, pk1;
     unpack_pair(cur, pl, pk0, pk1);
-    const float nn0 = nn_of(pk0), nn1 = nn_of(pk1);
+    // |x|^2 of the two pixels created as one register pair (the packed pair
+    // operands below then need no moves); exact integers < 2^18
+    const f32x2 nnb = pack2(__uint_as_float(__dp4a(pk0, pk0, F2P23_BITS)), __uint_as_float(__dp4a(pk1, pk1, F2P23_BITS)));
+    const f32x2 nn2 = sub2(nnb, pack2(F2P23, F2P23));
+    const f32x2 nnn2 = sub2(pack2(F2P23, F2P23), nnb);
+    const float nn0 = lo2(nn2), nn1 = hi2(nn2);
     const uint32_t pk2 = __shfl_down_sync(0xffffffffu, pk0, 1);  // column 2l + 2 (lane 31: unused)
     const float nn2n = __shfl_down_sync(0xffffffffu, nn0, 1);
     R.E[slot][l + 1] = make_uint4(pk0, pk1, __float_as_uint(nn0), __float_as_uint(nn1));
     R.O[slot][l + 1] = make_uint4(pk1, pk2, __float_as_uint(nn1), __float_as_uint(nn2n));
+#if VF_STREAM_RN
+    const float rn0 = rsqrt_approx(nn0), rn1 = rsqrt_approx(nn1);
+    const f32x2 rn2 = pack2(rn0, rn1);
+    const float rn2n = __shfl_down_sync(0xffffffffu, rn0, 1);
+    R.ER[slot][l + 1] = make_uint2(__float_as_uint(rn0), __float_as_uint(rn1));
+    R.OR[slot][l + 1] = make_uint2(__float_as_uint(rn1), __float_as_uint(rn2n));
+#endif
     *reinterpret_cast<uint2*>(&R.P[slot][2 * l + 2]) = make_uint2(pk0, pk1);
     zhist = ((zhist << 1) | (__any_sync(0xffffffffu, nn0 == 0.0f || nn1 == 0.0f) ? 1u : 0u)) & 7u;
     __syncwarp();
 
-    const f32x2 nn2 = pack2(nn0, nn1), nnn2 = pack2(-nn0, -nn1);
     const int s1 = (r - 1) & (SLOTS - 1), s2 = (r - 2) & (SLOTS - 1);
     auto nbr = [&](int sl, int dx) -> uint4 {
       // neighbour pair (columns 2l + dx, 2l + 1 + dx)
@@ -406,8 +429,20 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
 #pragma unroll
       for (int dxi = 0; dxi < N; ++dxi) q[dxi] = nbr(sl, dxi - 2);
       bool amb = false;
-      if (zhist == 0u) ang_mm_row<false, N>(pk0, pk1, nn2, nnn2, q, v, amb);
-      else ang_mm_row<true, N>(pk0, pk1, nn2, nnn2, q, v, amb);
+#if VF_STREAM_RN
+      f32x2 rr[N];
+#pragma unroll
+      for (int dxi = 0; dxi < N; ++dxi) {
+        const int dx = dxi - 2;
+        const uint2 t = (dx & 1) ? R.OR[sl][l + ((dx - 1) >> 1) + 1] : R.ER[sl][l + (dx >> 1) + 1];
+        rr[dxi] = mul2(rn2, pack2(__uint_as_float(t.x), __uint_as_float(t.y)));
+      }
+      const f32x2* rrp = rr;
+#else
+      const f32x2* rrp = nullptr;
+#endif
+      if (zhist == 0u) ang_mm_row<false, N>(pk0, pk1, nn2, nnn2, q, v, amb, rrp);
+      else ang_mm_row<true, N>(pk0, pk1, nn2, nnn2, q, v, amb, rrp);
       if (VF_STREAM_ACOS != 0 && __any_sync(0xffffffffu, amb)) ang_mm_row_exact<N>(pk0, pk1, nn2, nnn2, q, v);
     };
     // rows r - d (d = 2, then 1): the partner pixels' H(+d) from values of row r
@@ -539,10 +574,10 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
 }
 
 #ifndef VF_ANGULAR_MM_TU
+// defined in vf_stream.cu, whose compile flags (tuning knobs) fix the ring layout
 const void* stream_kernel_fn_mm();
+size_t stream_smem_bytes();
 #endif
-
-inline size_t stream_smem_bytes() { return sizeof(stream::Ring) * stream::NWARP; }
 
 // rows per warp: long tiles (less vertical halo: K + 2 steps for K rows) when
 // the launch has enough strips to fill the GPU, shorter ones for small images
@@ -553,9 +588,16 @@ inline int stream_rows_per_warp(long long strips_total_times_rows) {
   return K;
 }
 
-inline dim3 stream_grid(const Launch& L, int B, int K) {
+#ifdef VF_ANGULAR_MM_TU
+// launch geometry, defined with the kernel (vf_stream.cu) so the tuning knobs
+// of that translation unit fix it
+inline dim3 stream_grid_impl(const Launch& L, int B, int K) {
   using namespace stream;
   return dim3((L.W + SOUT - 1) / SOUT, (L.out_rows + K * NWARP - 1) / (K * NWARP), B);
 }
+#else
+dim3 stream_grid(const Launch& L, int B, int K);
+int stream_block_threads();
+#endif
 
 }  // namespace vf
