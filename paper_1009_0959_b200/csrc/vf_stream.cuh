@@ -35,8 +35,9 @@
 //          position among aggregates equal to 2^-19 relative -- within the
 //          1e-5 acceptance of SURVEY 8(c).4), reduced with 3-input FMNMX, and
 //          the selected sample is read back from the ring and stored.
-// A strip computes 64 columns and outputs 58 (strip columns 3..60); K output
-// rows take K + 2 steps.
+// A strip computes 64 columns and outputs 62 (strip columns 1..62: a window
+// only needs the pairs among its own 3 columns); K output rows take K + 2
+// steps.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -46,8 +47,8 @@ namespace vf {
 namespace stream {
 
 constexpr int SW = 64;          // computed columns per strip (2 per lane)
-constexpr int J_LO = 3;         // first output column of the strip
-constexpr int SOUT = 58;        // output columns per strip: [3, 61)
+constexpr int J_LO = 1;         // first output column of the strip
+constexpr int SOUT = 62;        // output columns per strip: [1, 63)
 constexpr int NE = 34;          // even-aligned record pairs per ring row: columns (2e - 2, 2e - 1), e = 0..33
 constexpr int NO = 33;          // odd-aligned record pairs: columns (2o - 1, 2o), o = 0..32
 constexpr int SLOTS = 4;        // ring rows (rows r, r-1, r-2 in use)
@@ -71,12 +72,13 @@ struct Ring {
   uint2 OR[SLOTS][NO];          // of the O pairs
 #endif
 };
-// Columns -2, -1, 64 and 65 of E / O (lanes 0 and 31, offsets |dx| >= 1) are
-// never written: the pair values that read them only feed the roles of strip
-// columns 0, 1, 62 and 63, which no output window uses (outputs 3..60 read
-// the roles of columns 2..61, whose pairs all lie inside columns 0..63).
+// Columns -2, -1, 64 and 65 (E[0], E[33], the first half of O[0], the second
+// half of O[32]) are never written: a window centred at strip column c only
+// reads the roles (c-1, b=0), (c, b=1), (c+1, b=2), i.e. the pair values
+// among columns c-1..c+1, so the windows at columns 1..62 never see a pair
+// with a column outside 0..63.
 
-// strip s covers image columns x0 = 58 s - 3 + j, j = 0..63
+// strip s covers image columns x0 + j, x0 = 62 s - 1, j = 0..63
 __host__ __device__ constexpr int strip_x0(int s) { return SOUT * s - J_LO; }
 
 }  // namespace stream
@@ -226,7 +228,11 @@ __device__ __forceinline__ void ang_mm_row(uint32_t pk0, uint32_t pk1, f32x2 nn2
       unpack2(c, c0, c1);
       unpack2(horner4x2(coef::ACOS(), c), a0, a1);
       unpack2(vs, s0, s1);
-      amb |= (c0 >= 0.5f - ACOS_AMBIG && c0 <= 0.5f + ACOS_AMBIG) || (c1 >= 0.5f - ACOS_AMBIG && c1 <= 0.5f + ACOS_AMBIG);
+      // |cos - 0.5| <= ACOS_AMBIG as one unsigned range test on the float bits
+      // (cos >= 0 for these integer vectors, and NaN/garbage only in unused pairs)
+      constexpr uint32_t LO = 0x3EFFFE00u;   // bits of 0.5 - 2^-16 = 0.4999847
+      constexpr uint32_t SPAN = 0x3F000100u - LO;   // up to 0.5 + 2^-16 = 0.5000153
+      amb |= (__float_as_uint(c0) - LO <= SPAN) | (__float_as_uint(c1) - LO <= SPAN);
       s0 = c0 < 0.5f ? a0 : s0;
       s1 = c1 < 0.5f ? a1 : s1;
       if (ZG) {
@@ -343,7 +349,7 @@ __device__ __forceinline__ void unpack_pair(const PairWords& r, const PairLoad& 
   p1 = pl.hi1 ? q1 : q0;
 }
 
-// grid (ceil(W / 58), ceil(out_rows / (K NWARP)), B), block 32 NWARP; dynamic
+// grid (ceil(W / 62), ceil(out_rows / (K NWARP)), B), block 32 NWARP; dynamic
 // smem NWARP * sizeof(Ring).  Warp w of block (sx, sy) streams strip sx over
 // output rows [out_row0 + (sy NWARP + w) K, + K).  Requires W >= 2.
 #ifndef VF_STREAM_MINB
@@ -369,7 +375,7 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
   pl.x_lo = clampi(xa, 0, W - 2);
   pl.hi0 = clampi(xa, 0, W - 1) != pl.x_lo;
   pl.hi1 = clampi(xa + 1, 0, W - 1) != pl.x_lo;
-  // output columns: strip j = 2l + k, valid for j in [3, 60] inside the image
+  // output columns: strip j = 2l + k, valid for j in [1, 62] inside the image
   const bool ov0 = 2 * l >= J_LO && 2 * l < J_LO + SOUT && xa < W;
   const bool ov1 = 2 * l + 1 >= J_LO && 2 * l + 1 < J_LO + SOUT && xa + 1 < W;
   const int rowb = W * 3;
@@ -405,6 +411,7 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
     const float nn2n = __shfl_down_sync(0xffffffffu, nn0, 1);
     R.E[slot][l + 1] = make_uint4(pk0, pk1, __float_as_uint(nn0), __float_as_uint(nn1));
     R.O[slot][l + 1] = make_uint4(pk1, pk2, __float_as_uint(nn1), __float_as_uint(nn2n));
+    if (l == 0) R.O[slot][0] = make_uint4(0u, pk0, 0u, __float_as_uint(nn0));   // column 0 as an O-pair's second pixel
 #if VF_STREAM_RN
     const float rn0 = rsqrt_approx(nn0), rn1 = rsqrt_approx(nn1);
     const f32x2 rn2 = pack2(rn0, rn1);
@@ -443,7 +450,13 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
 #endif
       if (zhist == 0u) ang_mm_row<false, N>(pk0, pk1, nn2, nnn2, q, v, amb, rrp);
       else ang_mm_row<true, N>(pk0, pk1, nn2, nnn2, q, v, amb, rrp);
-      if (VF_STREAM_ACOS != 0 && __any_sync(0xffffffffu, amb)) ang_mm_row_exact<N>(pk0, pk1, nn2, nnn2, q, v);
+      if (VF_STREAM_ACOS != 0 && __any_sync(0xffffffffu, amb)) {
+        // rare: re-load the records (keeping q live across the row would cost registers)
+        uint4 q2[N];
+#pragma unroll
+        for (int dxi = 0; dxi < N; ++dxi) q2[dxi] = nbr(sl, dxi - 2);
+        ang_mm_row_exact<N>(pk0, pk1, nn2, nnn2, q2, v);
+      }
     };
     // rows r - d (d = 2, then 1): the partner pixels' H(+d) from values of row r
     // pixels with offset (-d, dx), partly from the adjacent lanes
