@@ -200,15 +200,18 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
   const bool no_tma = (algo & VF_ALGO_NO_TMA) != 0;
   const bool want_stream = (algo & VF_ALGO_STREAM) != 0;
   algo &= 3;
-  // 3x3 angular minimax: the warp-streamed role-sum kernel (vf_stream.cuh) is
-  // the default (VF_ANG3_STREAM=0 falls back to the block pair-sharing kernel)
+  // 3x3 angular (minimax and exact): the warp-streamed role-sum kernel
+  // (vf_stream.cuh) is the default; VF_ANG3_STREAM=0 (both variants) or
+  // VF_ANG3_STREAM_EXACT=0 (exact only) fall back to the block pair-sharing
+  // kernel (C4 256 images: exact 2471 vs 2674 us, minimax 1467 vs 1849 us)
   static const bool env_no_stream = [] { const char* e = std::getenv("VF_ANG3_STREAM"); return e && e[0] == '0'; }();
-  if (crit == VF_ANGULAR && window == 3 && var == VF_MINIMAX &&
-      (want_stream || (algo == VF_ALGO_AUTO && !env_no_stream))) {
+  static const bool env_no_stream_ex = [] { const char* e = std::getenv("VF_ANG3_STREAM_EXACT"); return e && e[0] == '0'; }();
+  if (crit == VF_ANGULAR && window == 3 && (var == VF_MINIMAX || var == VF_EXACT) &&
+      (want_stream || (algo == VF_ALGO_AUTO && !env_no_stream && !(var == VF_EXACT && env_no_stream_ex)))) {
     const long long strips = (W + vf::stream::SOUT - 1) / vf::stream::SOUT;
     static const int k_env = [] { const char* e = std::getenv("VF_STREAM_K"); return e ? std::atoi(e) : 0; }();
     const int K = (k_env >= 2 && k_env <= 1024) ? k_env : vf::stream_rows_per_warp(strips * out_rows * (long long)B);
-    kd->fn = vf::stream_kernel_fn_mm();
+    kd->fn = var == VF_EXACT ? vf::stream_kernel_fn_ex() : vf::stream_kernel_fn_mm();
     kd->grid = vf::stream_grid(L, B, K);
     kd->block = dim3(vf::stream_block_threads());
     kd->smem = vf::stream_smem_bytes();

@@ -110,7 +110,7 @@ __device__ __forceinline__ float role_key(float v) {
 // (pk(q0), pk(q1), |q0|^2, |q1|^2), packed FP32 (nn2 = (|p0|^2, |p1|^2),
 // nnn2 = -nn2): the ARCSIN-row value vs = P_asin(tau) (Table 1, Eq. 7,
 // reading R6), cos c, and -Ph (zero iff a zero vector is involved).
-template <bool TINY = true>
+template <bool TINY = true, bool EXACT_V = false>
 __device__ __forceinline__ void ang_geo2(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2, uint4 q, f32x2& vs,
                                          f32x2& c, f32x2& nPh, const f32x2* rin = nullptr) {
   const f32x2 Db = pack2(__uint_as_float(__dp4a(pk0, q.x, F2P23_BITS)), __uint_as_float(__dp4a(pk1, q.y, F2P23_BITS)));
@@ -140,7 +140,14 @@ __device__ __forceinline__ void ang_geo2(uint32_t pk0, uint32_t pk1, f32x2 nn2, 
     unpack2(mul2(mul2(X, r), pack2(rsqrt_approx(xw0), rsqrt_approx(xw1))), t0, t1);
     tau = pack2(fmaxf(t0, 0.0f), fmaxf(t1, 0.0f));
   }
-  vs = horner4x2(coef::ASIN(), tau);
+  if constexpr (EXACT_V) {
+    // Eq. 6 with libm: arccos z = 2 arcsin(sqrt((1 - z) / 2)) = 2 asinf(tau / sqrt2) for z >= 0.5
+    float t0, t1;
+    unpack2(tau, t0, t1);
+    vs = pack2(2.0f * asinf(t0 * 0.70710678118654752f), 2.0f * asinf(t1 * 0.70710678118654752f));
+  } else {
+    vs = horner4x2(coef::ASIN(), tau);                             // Table 1 ARCSIN row (Eq. 7, reading R6)
+  }
 }
 
 // Exact branch predicate (reading R5) of the two pairs: cos < 0.5 <=> 4 D^2 <
@@ -183,9 +190,30 @@ constexpr float ACOS_AMBIG = 1.0f / 65536.0f;
 // and 3, pairs within ACOS_AMBIG of cos = 0.5 set `amb`: the caller then
 // re-decides the whole row exactly (ang_mm_row_exact).
 // ZG: zero vector -> 0.
-template <bool ZG, int N>
+template <bool ZG, int N, bool EXACT_V = false>
 __device__ __forceinline__ void ang_mm_row(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2, const uint4 (&q)[N],
                                            f32x2 (&v)[N], bool& amb, const f32x2* rr = nullptr) {
+  if constexpr (EXACT_V) {
+    // exact variant (libm): the exact predicate for every pair; acosf (the ~1%
+    // of pairs with cos < 0.5) only in lanes that need it, the ARCSIN side by
+    // Eq. 6 with asinf.  Zero vectors need no fix-up: tau = 0 and cos < 0.5
+    // is false, so the value is 2 asinf(0) = 0.
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      f32x2 vs, c, nPh;
+      ang_geo2<false, true>(pk0, pk1, nn2, nnn2, q[i], vs, c, nPh);
+      bool e0, e1;
+      acos_branch_exact2(pk0, pk1, nn2, nnn2, q[i], e0, e1);
+      float s0, s1;
+      unpack2(vs, s0, s1);
+      if (__any_sync(0xffffffffu, e0 || e1)) {
+        if (e0) s0 = acosf(lo2(c));
+        if (e1) s1 = acosf(hi2(c));
+      }
+      v[i] = pack2(s0, s1);
+    }
+    return;
+  }
   auto finish = [&](int i, f32x2 c, f32x2 nPh) {
     float c0, c1;
     unpack2(c, c0, c1);
@@ -358,7 +386,7 @@ __device__ __forceinline__ void unpack_pair(const PairWords& r, const PairLoad& 
 template <int VAR>
 __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular_stream_kernel(const Launch L, int K) {
   using namespace stream;
-  static_assert(VAR == MINIMAX, "streamed kernel: minimax variant");
+  static_assert(VAR == MINIMAX || VAR == EXACT, "streamed kernel: angular minimax or exact");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
   Ring& R = reinterpret_cast<Ring*>(smem_raw)[warp];
@@ -448,9 +476,10 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
 #else
       const f32x2* rrp = nullptr;
 #endif
-      if (zhist == 0u) ang_mm_row<false, N>(pk0, pk1, nn2, nnn2, q, v, amb, rrp);
+      if constexpr (VAR == EXACT) ang_mm_row<false, N, true>(pk0, pk1, nn2, nnn2, q, v, amb);
+      else if (zhist == 0u) ang_mm_row<false, N>(pk0, pk1, nn2, nnn2, q, v, amb, rrp);
       else ang_mm_row<true, N>(pk0, pk1, nn2, nnn2, q, v, amb, rrp);
-      if (VF_STREAM_ACOS != 0 && __any_sync(0xffffffffu, amb)) {
+      if (VAR != EXACT && VF_STREAM_ACOS != 0 && __any_sync(0xffffffffu, amb)) {
         // rare: re-load the records (keeping q live across the row would cost registers)
         uint4 q2[N];
 #pragma unroll
@@ -589,6 +618,7 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
 #ifndef VF_ANGULAR_MM_TU
 // defined in vf_stream.cu, whose compile flags (tuning knobs) fix the ring layout
 const void* stream_kernel_fn_mm();
+const void* stream_kernel_fn_ex();
 size_t stream_smem_bytes();
 #endif
 
