@@ -201,14 +201,21 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
   const bool want_stream = (algo & VF_ALGO_STREAM) != 0;
   algo &= 3;
   // 3x3 angular (minimax and exact): the warp-streamed role-sum kernel
-  // (vf_stream.cuh) is the default; VF_ANG3_STREAM=0 (both variants) or
-  // VF_ANG3_STREAM_EXACT=0 (exact only) fall back to the block pair-sharing
-  // kernel (C4 256 images: exact 2471 vs 2674 us, minimax 1467 vs 1849 us)
+  // (vf_stream.cuh) is the default for large launches; VF_ANG3_STREAM=0
+  // (both variants) or VF_ANG3_STREAM_EXACT=0 (exact only) fall back to the
+  // block pair-sharing kernel, VF_ANG3_STREAM=1 forces the streamed one at any
+  // size (tests) (C4 256 images: exact 2471 vs 2674 us, minimax 1467 vs 1849 us)
   static const bool env_no_stream = [] { const char* e = std::getenv("VF_ANG3_STREAM"); return e && e[0] == '0'; }();
   static const bool env_no_stream_ex = [] { const char* e = std::getenv("VF_ANG3_STREAM_EXACT"); return e && e[0] == '0'; }();
+  // Small launches (less than one wave of 64-row warps, e.g. one 512x512
+  // image) keep the block kernel: a warp-streamed strip needs long columns
+  // of work (C2: stream exact 35 us vs 15 us)
+  const long long strips = (W + vf::stream::SOUT - 1) / vf::stream::SOUT;
+  static const bool env_force_stream = [] { const char* e = std::getenv("VF_ANG3_STREAM"); return e && e[0] == '1'; }();
+  const bool stream_big = env_force_stream || strips * out_rows * (long long)B >= 148LL * 20 * 64;
   if (crit == VF_ANGULAR && window == 3 && (var == VF_MINIMAX || var == VF_EXACT) &&
-      (want_stream || (algo == VF_ALGO_AUTO && !env_no_stream && !(var == VF_EXACT && env_no_stream_ex)))) {
-    const long long strips = (W + vf::stream::SOUT - 1) / vf::stream::SOUT;
+      (want_stream || (algo == VF_ALGO_AUTO && stream_big && !env_no_stream &&
+                       !(var == VF_EXACT && env_no_stream_ex)))) {
     static const int k_env = [] { const char* e = std::getenv("VF_STREAM_K"); return e ? std::atoi(e) : 0; }();
     const int K = (k_env >= 2 && k_env <= 1024) ? k_env : vf::stream_rows_per_warp(strips * out_rows * (long long)B);
     kd->fn = var == VF_EXACT ? vf::stream_kernel_fn_ex() : vf::stream_kernel_fn_mm();

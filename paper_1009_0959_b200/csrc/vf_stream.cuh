@@ -417,7 +417,9 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
   uint32_t zhist = 0;                                           // zero-vector flags of the last 3 staged rows
 
   auto row_ptr = [&](int r) {
-    return in + (long long)(clampi(r, L.band_row0, L.band_row0 + L.band_rows - 1) - L.band_row0) * rowb;
+    const int br = clampi(r, L.band_row0, L.band_row0 + L.band_rows - 1) - L.band_row0;
+    VF_CHECK(br >= 0 && br < L.band_rows);
+    return in + (long long)br * rowb;
   };
   PairWords nxt = ld_pair_words(row_ptr(ty0 - 1), pl, in_end);
   constexpr int kUnroll = VF_STREAM_UNROLL;
@@ -567,10 +569,13 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
       auto pick = [&](uint32_t nib, int k) -> uint32_t {
         const uint32_t a = nib >> 2;
         const uint32_t* pr = a == 0 ? prow0 : (a == 1 ? prow1 : prow2);
+        VF_CHECK(a <= 2 && (nib & 3u) <= 2);
         return pr[2 * l + k + 1 + (int)(nib & 3u)];
       };
       const uint32_t o0 = pick(nib0, 0), o1 = pick(nib1, 1);
       // a8: 6 bytes per lane, predicated stores (no divergence)
+      VF_CHECK(!(ov0 || ov1) || (gy >= L.out_row0 && gy < L.out_row0 + L.out_rows && xa + (ov0 ? 0 : 1) >= 0 &&
+                                  xa + (ov1 ? 1 : 0) < W));
       uint8_t* op = L.out + (long long)b * L.out_stride + ((long long)(gy - L.out_row0) * W + xa) * 3;
       if (((uintptr_t)op & 1u) == 0) {                          // warp-uniform: U16, U8 U8, U16
         if (ov0) *reinterpret_cast<uint16_t*>(op) = (uint16_t)o0;

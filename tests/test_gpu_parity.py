@@ -152,6 +152,18 @@ def test_tma_path_row_stripes():
     assert r.returncode == 0 and "tma stripes ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+def test_stream_kernel_paths():
+    """The streamed 3x3 angular kernels (forced at every size in a child
+    process, VF_ANG3_STREAM=1): oracle parity, row stripes, batches, odd
+    strides and a misaligned base are bit-identical to the whole-image call."""
+    import subprocess
+    import sys
+    child = os.path.join(os.path.dirname(os.path.abspath(__file__)), "stream_paths_child.py")
+    r = subprocess.run([sys.executable, child], env=dict(os.environ, VF_ANG3_STREAM="1"), capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "stream paths ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_el_block_shapes_bit_identical():
     """exp/log 3x3 large launches: the default 4-warp x 4-row blocks, the
     8-warp blocks with 4 or 2 rows and 4-warp x 2-row blocks give bit-identical
@@ -418,9 +430,16 @@ def test_c4_full_batch_sampled(crit, var):
         full[b] = torch.from_numpy(xb[j]).cuda()
     out, idx, _ = vfb.filter(full, 3, crit, var, want_index=True)
     torch.cuda.synchronize()
+    # the per-image call must use the batched call's kernel (the angular
+    # default depends on the launch size: streamed for the batch; the exp/log
+    # kernels of different tile shapes are bit-identical by construction)
+    algo = "stream" if crit == "angular" else "auto"
+    if crit == "angular":
+        assert vfb.vf_kernel_info(1024, 512, 768, 3, crit, var)["name"] == \
+            vfb.vf_kernel_info(1, 512, 768, 3, crit, var, algo)["name"]
     for j, b in enumerate(ids):
         sub = full[b:b + 1]
-        o2, i2, a2 = vfb.filter(sub.contiguous(), 3, crit, var, want_index=True, want_agg=True)
+        o2, i2, a2 = vfb.filter(sub.contiguous(), 3, crit, var, algo=algo, want_index=True, want_agg=True)
         assert torch.equal(o2[0], out[b]) and torch.equal(i2[0], idx[b])
         sampled_parity(xb[j], 3, crit, var, o2[0].cpu().numpy(), i2[0].cpu().numpy(), a2[0].cpu().numpy(),
                        nsample=5000, seed=b)

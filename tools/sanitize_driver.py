@@ -19,7 +19,8 @@ for H, W in [(37, 45), (64, 64), (5, 70), (77, 144), (300, 96)]:   # 3W % 16 == 
         if w > min(H, W):
             continue
         for c in combos:
-            algos = (["window", "shared", "shared:1", "shared:2", "shared:3", "role", "role:1", "role:2", "role:3"] if c[0] == "angular" else
+            algos = (["stream", "window", "shared", "shared:1", "shared:2", "shared:3", "role", "role:1", "role:2",
+                      "role:3"] if c[0] == "angular" else
                      ["auto:1", "auto:2", "auto:3", "auto:1+notma", "auto:2+notma", "auto:3+notma"])
             for a in algos:
                 vfb.filter(x, w, *c, algo=a, want_index=True, want_agg=True)
