@@ -212,10 +212,13 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
   // of work (C2: stream exact 35 us vs 15 us)
   const long long strips = (W + vf::stream::SOUT - 1) / vf::stream::SOUT;
   static const bool env_force_stream = [] { const char* e = std::getenv("VF_ANG3_STREAM"); return e && e[0] == '1'; }();
+  // (the minimax streamed kernel is also the faster one for small launches:
+  // C2 11.4 vs 12.5 us; VF_ANG3_SMALL_SHARED=1 restores the block kernel there)
+  static const bool env_small_shared = [] { const char* e = std::getenv("VF_ANG3_SMALL_SHARED"); return e && e[0] == '1'; }();
   const bool stream_big = env_force_stream || strips * out_rows * (long long)B >= 148LL * 20 * 64;
   if (crit == VF_ANGULAR && window == 3 && (var == VF_MINIMAX || var == VF_EXACT) &&
-      (want_stream || (algo == VF_ALGO_AUTO && stream_big && !env_no_stream &&
-                       !(var == VF_EXACT && env_no_stream_ex)))) {
+      (want_stream || (algo == VF_ALGO_AUTO && (stream_big || (var == VF_MINIMAX && !env_small_shared)) &&
+                       !env_no_stream && !(var == VF_EXACT && env_no_stream_ex)))) {
     static const int k_env = [] { const char* e = std::getenv("VF_STREAM_K"); return e ? std::atoi(e) : 0; }();
     const int K = (k_env >= 2 && k_env <= 1024) ? k_env : vf::stream_rows_per_warp(strips * out_rows * (long long)B);
     kd->fn = var == VF_EXACT ? vf::stream_kernel_fn_ex() : vf::stream_kernel_fn_mm();
