@@ -176,6 +176,12 @@ VF_API int vf_plan_create(vf_plan *plan, int B, int H, int W, int window, int n,
                           const int *variants, const uint8_t *d_in, uint8_t *const *d_outs,
                           const uint8_t *h_in, uint8_t *const *h_outs);
 VF_API int vf_plan_launch(vf_plan plan, void *stream);
+/* Number of kernel nodes of a plan (>= 1; VF_EINVAL for an invalid plan).  Plans
+ * of at least 2^21 pixels fuse their exp/log filters into one node (they share
+ * the L1 distances and S1, readings R2/R3; outputs bit-identical to the
+ * single-filter kernels; the environment variable VF_PLAN_FUSE=0 disables it),
+ * so a plan of the 7 paper filters has 3 kernel nodes. */
+VF_API int vf_plan_kernels(vf_plan plan);
 VF_API int vf_plan_destroy(vf_plan plan);
 
 /* Per-image fidelity statistics of two device image batches a, b
@@ -212,8 +218,8 @@ VF_API int vf_image_stats_multi(const uint8_t *a, const uint8_t *const *bs, int 
 VF_API const char *vf_status_string(int status);
 /* Text of the last error on the calling thread ("" if none). */
 VF_API const char *vf_last_error(void);
-/* ABI version (major*100 + minor): 103 (102: vf_image_stats_ex; 103: vf_image_stats_multi,
- * deterministic statistics, vf_kernel_info). */
+/* ABI version (major*100 + minor): 104 (102: vf_image_stats_ex; 103: vf_image_stats_multi,
+ * deterministic statistics, vf_kernel_info; 104: vf_plan_kernels, fused exp/log plan nodes). */
 VF_API int vf_version(void);
 
 #ifdef __cplusplus

@@ -28,6 +28,13 @@
 namespace vf {
 // vf_el_ty4.cu (its own translation unit and ptxas setting)
 const void* el_kernel_ty4(int opt, int crit, int var);
+// vf_fused.cu: the fused exp/log node of a plan
+struct ElFused {
+  Launch L[8];
+  int code[8];
+  int n;
+};
+const void* el_fused_kernel(int window, bool big, int* opt, int* nty);
 }  // namespace vf
 
 namespace {
@@ -503,7 +510,57 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (H2D)"));
   }
   const long long stride = (long long)H * W * 3;
+  // Plan-level fusion: the exp/log filters share d1 and S1 (readings R2/R3),
+  // so two or more of them become ONE kernel node that stages each tile and
+  // forms S1 once (vf_fused.cu; outputs bit-identical to the single-filter
+  // kernels).  VF_PLAN_FUSE=0 keeps one node per filter.
+  static const bool env_no_fuse = [] { const char* e = std::getenv("VF_PLAN_FUSE"); return e && e[0] == '0'; }();
+  bool fused[64] = {};
+  {
+    int idx[8], m = 0;
+    for (int i = 0; i < n && m < 8; ++i)
+      if (criteria[i] == VF_EXP || criteria[i] == VF_LOG) idx[m++] = i;
+    // (small inputs keep one node per filter: the graph's concurrency then
+    // matters more than the shared staging -- C2: 70 vs 60 us)
+    const bool fuse_big = (long long)B * H * W >= (1LL << 21);
+    if (m >= 2 && !env_no_fuse && window <= 5 && fuse_big) {
+      vf::ElFused F = {};
+      F.n = m;
+      for (int k = 0; k < m; ++k) {
+        KernelDesc kd;
+        int rc = describe(&kd, d_in, stride, 0, H, B, H, W, 0, H, window, criteria[idx[k]], variants[idx[k]],
+                          VF_ALGO_AUTO | VF_ALGO_NO_TMA, d_outs[idx[k]], stride, nullptr, nullptr);
+        if (rc) return bail(rc);
+        F.L[k] = kd.L;
+        F.code[k] = 4 * (criteria[idx[k]] == VF_EXP ? vf::EXPC : vf::LOGC) + variants[idx[k]];
+        fused[idx[k]] = true;
+      }
+      int opt = 1, nty = vf::TY;
+      const bool big = window == 3;
+      cudaKernelNodeParams kp = {};
+      kp.func = (void*)vf::el_fused_kernel(window, big, &opt, &nty);
+      kp.gridDim = dim3((W + vf::TX - 1) / vf::TX, (H + nty * opt - 1) / (nty * opt), B);
+      kp.blockDim = dim3(vf::TX, nty);
+      kp.sharedMemBytes = 0;
+      void* args[1] = {&F};
+      kp.kernelParams = args;
+      if (kp.gridDim.y > 65535 || kp.gridDim.z > 65535) return bail(fail(VF_EINVAL, "grid too large"));
+      cudaGraphNode_t kn;
+      e = cudaGraphAddKernelNode(&kn, p->graph, h2d ? &h2d : nullptr, h2d ? 1 : 0, &kp);
+      if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddKernelNode (fused)"));
+      ++p->nkernels;
+      if (h_outs) {
+        for (int k = 0; k < m; ++k) {
+          cudaGraphNode_t d2h;
+          e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, &kn, 1, h_outs[idx[k]], d_outs[idx[k]], bytes,
+                                       cudaMemcpyDeviceToHost);
+          if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (D2H)"));
+        }
+      }
+    }
+  }
   for (int i = 0; i < n; ++i) {
+    if (fused[i]) continue;
     KernelDesc kd;
     int rc = describe(&kd, d_in, stride, 0, H, B, H, W, 0, H, window, criteria[i], variants[i], VF_ALGO_AUTO,
                       d_outs[i], stride, nullptr, nullptr);
@@ -517,6 +574,7 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
     cudaGraphNode_t kn;
     e = cudaGraphAddKernelNode(&kn, p->graph, h2d ? &h2d : nullptr, h2d ? 1 : 0, &kp);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddKernelNode"));
+    ++p->nkernels;
     if (h_outs) {
       cudaGraphNode_t d2h;
       e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, &kn, 1, h_outs[i], d_outs[i], bytes, cudaMemcpyDeviceToHost);
@@ -525,7 +583,6 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
   }
   e = cudaGraphInstantiate(&p->exec, p->graph, 0);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphInstantiate"));
-  p->nkernels = n;
   *plan = p;
   return VF_OK;
 }
@@ -536,6 +593,12 @@ int vf_plan_launch(vf_plan plan, void* stream) {
   cudaError_t e = cudaGraphLaunch(plan->exec, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
   return VF_OK;
+}
+
+int vf_plan_kernels(vf_plan plan) {
+  g_err[0] = 0;
+  if (!plan || !plan->exec) return fail(VF_EINVAL, "invalid plan");
+  return plan->nkernels;
 }
 
 int vf_plan_destroy(vf_plan plan) {
@@ -621,6 +684,6 @@ const char* vf_status_string(int status) {
 
 const char* vf_last_error(void) { return g_err; }
 
-int vf_version(void) { return 103; }
+int vf_version(void) { return 104; }
 
 }  // extern "C"

@@ -27,7 +27,7 @@ VARIANTS = {"exact": VF_EXACT, "minimax": VF_MINIMAX, "poly4": VF_MINIMAX_POLY4,
 ALGOS = {"auto": VF_ALGO_AUTO, "window": VF_ALGO_WINDOW, "shared": VF_ALGO_SHARED, "role": VF_ALGO_ROLE,
          "stream": VF_ALGO_STREAM}
 EXPORTS = ["vf_filter", "vf_filter_batch", "vf_filter_rows", "vf_filter_batch_algo",
-           "vf_host_workspace_bytes", "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_destroy",
+           "vf_host_workspace_bytes", "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_kernels", "vf_plan_destroy",
            "vf_image_stats", "vf_image_stats_ex", "vf_image_stats_multi", "vf_kernel_info", "vf_status_string", "vf_last_error", "vf_version"]
 VF_STATS_NO_REF_NORM = 1
 
@@ -61,6 +61,7 @@ def load_library(path: str = LIB_PATH):
     L.vf_plan_create.argtypes = [ctypes.POINTER(P), I, I, I, I, I, P, P, P, P, P, P]
     L.vf_plan_launch.argtypes = [P, P]
     L.vf_plan_destroy.argtypes = [P]
+    L.vf_plan_kernels.argtypes = [P]
     L.vf_image_stats.argtypes = [P, P, I, I, I, P, P]
     L.vf_image_stats_ex.argtypes = [P, P, I, I, I, P, I, P]
     L.vf_image_stats_multi.argtypes = [P, ctypes.POINTER(P), I, I, I, I, P, I, P]
@@ -71,7 +72,7 @@ def load_library(path: str = LIB_PATH):
     L.vf_last_error.restype = ctypes.c_char_p
     L.vf_version.argtypes = []
     for name in ("vf_filter", "vf_filter_batch", "vf_filter_batch_algo", "vf_filter_rows",
-                 "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_destroy", "vf_image_stats",
+                 "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_kernels", "vf_plan_destroy", "vf_image_stats",
                  "vf_image_stats_ex", "vf_image_stats_multi", "vf_kernel_info", "vf_version"):
         getattr(L, name).restype = I
     _lib = L
@@ -265,6 +266,13 @@ class Plan:
     def launch(self, stream=None):
         with torch.cuda.device(self.device):
             _check(load_library().vf_plan_launch(self._h, _stream(stream)), "vf_plan_launch")
+
+    def kernels(self) -> int:
+        """Kernel nodes of the plan's graph (exp/log filters of large plans fuse into one)."""
+        rc = load_library().vf_plan_kernels(self._h)
+        if rc < 0:
+            _check(rc, "vf_plan_kernels")
+        return rc
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

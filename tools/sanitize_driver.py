@@ -34,5 +34,11 @@ outs = [torch.empty_like(xb) for _ in combos]
 plan = vfb.Plan(xb, outs, 3, combos)
 plan.launch()
 vfb.vf_image_stats(xb, outs[0])
+# a fused plan (>= 2^21 pixels: the exp/log filters in one node), ragged width
+xl = torch.from_numpy(vfsynth.make_batch(vfsynth.ImageSpec("t", 300, 1201, 6, (3,), 4, False, "uncorrelated", 0.2))).cuda()
+louts = [torch.empty_like(xl) for _ in combos[:9]]
+lplan = vfb.Plan(xl, louts, 3, combos[:9])
+assert lplan.kernels() < 9
+lplan.launch()
 torch.cuda.synchronize()
 print("sanitize driver done")
