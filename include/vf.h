@@ -178,9 +178,11 @@ VF_API int vf_plan_create(vf_plan *plan, int B, int H, int W, int window, int n,
 VF_API int vf_plan_launch(vf_plan plan, void *stream);
 /* Number of kernel nodes of a plan (>= 1; VF_EINVAL for an invalid plan).  Plans
  * of at least 2^21 pixels fuse their exp/log filters into one node (they share
- * the L1 distances and S1, readings R2/R3; outputs bit-identical to the
- * single-filter kernels; the environment variable VF_PLAN_FUSE=0 disables it),
- * so a plan of the 7 paper filters has 3 kernel nodes. */
+ * the L1 distances and S1, readings R2/R3) and their 3x3 angular exact and
+ * minimax filters into one node (one pair-geometry evaluation for both
+ * variants); outputs are bit-identical to the single-filter kernels; the
+ * environment variable VF_PLAN_FUSE=0 disables fusion.  A large plan of the 7
+ * paper filters has 2 kernel nodes. */
 VF_API int vf_plan_kernels(vf_plan plan);
 VF_API int vf_plan_destroy(vf_plan plan);
 

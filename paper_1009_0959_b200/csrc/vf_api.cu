@@ -69,10 +69,11 @@ struct KernelDesc {
   bool tma = false;          // vf_el_tma_kernel: (map, L, tiles_x, tiles_y, ntiles)
   alignas(64) CUtensorMap map;
   int tiles_x = 0, tiles_y = 0, ntiles = 0;
-  int stream_k = 0;          // vf_angular_stream_kernel: (L, K)
+  int stream_k = 0;          // vf_angular_stream_kernel: (L, K, L2)
+  Launch L2;                 // the fused kernel's second output (exact); = L otherwise
   void* args[5];
   void** params() {
-    if (stream_k) { args[0] = &L; args[1] = &stream_k; return args; }
+    if (stream_k) { args[0] = &L; args[1] = &stream_k; args[2] = &L2; return args; }
     if (!tma) { args[0] = &L; return args; }
     args[0] = &map; args[1] = &L; args[2] = &tiles_x; args[3] = &tiles_y; args[4] = &ntiles;
     return args;
@@ -233,6 +234,7 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
     kd->block = dim3(vf::stream_block_threads());
     kd->smem = vf::stream_smem_bytes();
     kd->stream_k = K;
+    kd->L2 = L;
     if (kd->grid.y > 65535 || kd->grid.z > 65535) return fail(VF_EINVAL, "grid too large");
     return VF_OK;
   }
@@ -555,6 +557,50 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
           e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, &kn, 1, h_outs[idx[k]], d_outs[idx[k]], bytes,
                                        cudaMemcpyDeviceToHost);
           if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (D2H)"));
+        }
+      }
+    }
+  }
+  // Plan-level fusion of BVDF minimax and exact (3x3, streamed kernels): one
+  // geometry evaluation per pair feeds both variants (vf_stream.cuh, NV = 2).
+  // VF_PLAN_FUSE=0 keeps one node per filter.
+  {
+    int im = -1, ie = -1;
+    for (int i = 0; i < n; ++i) {
+      if (criteria[i] != VF_ANGULAR || fused[i]) continue;
+      if (variants[i] == VF_MINIMAX && im < 0) im = i;
+      if (variants[i] == VF_EXACT && ie < 0) ie = i;
+    }
+    if (im >= 0 && ie >= 0 && window == 3 && !env_no_fuse) {
+      KernelDesc km, ke;
+      int rc = describe(&km, d_in, stride, 0, H, B, H, W, 0, H, window, VF_ANGULAR, VF_MINIMAX, VF_ALGO_AUTO,
+                        d_outs[im], stride, nullptr, nullptr);
+      if (rc) return bail(rc);
+      rc = describe(&ke, d_in, stride, 0, H, B, H, W, 0, H, window, VF_ANGULAR, VF_EXACT, VF_ALGO_AUTO, d_outs[ie],
+                    stride, nullptr, nullptr);
+      if (rc) return bail(rc);
+      if (km.stream_k && ke.stream_k) {               // both streamed (large launches)
+        km.fn = vf::stream_kernel_fn_both();
+        km.L2 = ke.L;
+        cudaKernelNodeParams kp = {};
+        kp.func = (void*)km.fn;
+        kp.gridDim = km.grid;
+        kp.blockDim = km.block;
+        kp.sharedMemBytes = (unsigned)km.smem;
+        kp.kernelParams = km.params();
+        cudaGraphNode_t kn;
+        e = cudaGraphAddKernelNode(&kn, p->graph, h2d ? &h2d : nullptr, h2d ? 1 : 0, &kp);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddKernelNode (fused angular)"));
+        ++p->nkernels;
+        fused[im] = fused[ie] = true;
+        if (h_outs) {
+          const int ids[2] = {im, ie};
+          for (int k = 0; k < 2; ++k) {
+            cudaGraphNode_t d2h;
+            e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, &kn, 1, h_outs[ids[k]], d_outs[ids[k]], bytes,
+                                         cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (D2H)"));
+          }
         }
       }
     }

@@ -8,6 +8,7 @@ namespace vf {
 
 const void* stream_kernel_fn_mm() { return (const void*)vf_angular_stream_kernel<MINIMAX>; }
 const void* stream_kernel_fn_ex() { return (const void*)vf_angular_stream_kernel<EXACT>; }
+const void* stream_kernel_fn_both() { return (const void*)vf_angular_stream_kernel<MINIMAX, 2>; }
 size_t stream_smem_bytes() { return sizeof(stream::Ring) * stream::NWARP; }
 dim3 stream_grid(const Launch& L, int B, int K) { return stream_grid_impl(L, B, K); }
 int stream_block_threads() { return 32 * stream::NWARP; }

@@ -112,7 +112,7 @@ __device__ __forceinline__ float role_key(float v) {
 // reading R6), cos c, and -Ph (zero iff a zero vector is involved).
 template <bool TINY = true, bool EXACT_V = false>
 __device__ __forceinline__ void ang_geo2(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2, uint4 q, f32x2& vs,
-                                         f32x2& c, f32x2& nPh, const f32x2* rin = nullptr) {
+                                         f32x2& c, f32x2& nPh, const f32x2* rin = nullptr, f32x2* tau_out = nullptr) {
   const f32x2 Db = pack2(__uint_as_float(__dp4a(pk0, q.x, F2P23_BITS)), __uint_as_float(__dp4a(pk1, q.y, F2P23_BITS)));
   const f32x2 D = sub2(Db, pack2(F2P23, F2P23));                  // exact dot products
   const f32x2 nnq = pack2(__uint_as_float(q.z), __uint_as_float(q.w));
@@ -140,6 +140,7 @@ __device__ __forceinline__ void ang_geo2(uint32_t pk0, uint32_t pk1, f32x2 nn2, 
     unpack2(mul2(mul2(X, r), pack2(rsqrt_approx(xw0), rsqrt_approx(xw1))), t0, t1);
     tau = pack2(fmaxf(t0, 0.0f), fmaxf(t1, 0.0f));
   }
+  if (tau_out) *tau_out = tau;
   if constexpr (EXACT_V) {
     // Eq. 6 with libm: arccos z = 2 arcsin(sqrt((1 - z) / 2)) = 2 asinf(tau / sqrt2) for z >= 0.5
     float t0, t1;
@@ -315,6 +316,36 @@ __device__ __forceinline__ void ang_mm_row_exact(uint32_t pk0, uint32_t pk1, f32
   }
 }
 
+// Both variants of the lane's two pairs for n neighbour record pairs from ONE
+// geometry evaluation (plan-level fusion of BVDF exact and minimax): vm =
+// Table 1 values (minimax, zero vectors -> 0), ve = libm values (Eq. 6).
+template <int N>
+__device__ __forceinline__ void ang_both_row(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2, const uint4 (&q)[N],
+                                             f32x2 (&vm)[N], f32x2 (&ve)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    f32x2 vs, c, nPh, tau;
+    ang_geo2<false, false>(pk0, pk1, nn2, nnn2, q[i], vs, c, nPh, nullptr, &tau);
+    bool e0, e1;
+    acos_branch_exact2(pk0, pk1, nn2, nnn2, q[i], e0, e1);
+    float a0, a1, s0, s1, n0, n1, c0, c1, t0, t1;
+    unpack2(horner4x2(coef::ACOS(), c), a0, a1);
+    unpack2(vs, s0, s1);
+    unpack2(nPh, n0, n1);
+    unpack2(c, c0, c1);
+    unpack2(tau, t0, t1);
+    s0 = e0 ? a0 : s0;
+    s1 = e1 ? a1 : s1;
+    vm[i] = pack2(n0 == 0.0f ? 0.0f : s0, n1 == 0.0f ? 0.0f : s1);
+    float x0 = 2.0f * asinf(t0 * 0.70710678118654752f), x1 = 2.0f * asinf(t1 * 0.70710678118654752f);
+    if (__any_sync(0xffffffffu, e0 || e1)) {
+      if (e0) x0 = acosf(c0);
+      if (e1) x1 = acosf(c1);
+    }
+    ve[i] = pack2(x0, x1);
+  }
+}
+
 // H sums of one neighbourhood row (values a(dx), dx = -2..2; a(0) = 0 for the
 // pixel's own row): H_b = sum_{dx in [-b, 2-b]} a(dx), b = 0, 1, 2.  Packed
 // over the lane's two pixels where both rows are register pairs.
@@ -383,10 +414,15 @@ __device__ __forceinline__ void unpack_pair(const PairWords& r, const PairLoad& 
 #ifndef VF_STREAM_MINB
 #define VF_STREAM_MINB (20 / VF_STREAM_NWARP)   // resident blocks per SM: 20 warps per SM, <= 102 registers
 #endif
-template <int VAR>
-__global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular_stream_kernel(const Launch L, int K) {
+// NV = 2 (VAR = MINIMAX): both variants from one geometry evaluation per pair
+// (plan-level fusion of BVDF minimax and exact): L writes the minimax output,
+// L2 the exact one; NV = 1: the variant VAR into L (L2 unused).
+template <int VAR, int NV = 1>
+__global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB)
+    vf_angular_stream_kernel(const Launch L, int K, const Launch L2) {
   using namespace stream;
   static_assert(VAR == MINIMAX || VAR == EXACT, "streamed kernel: angular minimax or exact");
+  static_assert(NV == 1 || (NV == 2 && VAR == MINIMAX), "fused: minimax + exact");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
   Ring& R = reinterpret_cast<Ring*>(smem_raw)[warp];
@@ -411,9 +447,11 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
   // carried partial role sums (packed over the lane's two pixels):
   // U = H(-1) + H(0) and Z = H(0) of the previous row's pixels (-> role a = 1
   // and the partial W), Wp = H(0) + H(+1) of the row before (-> role a = 0)
-  f32x2 U[3], Z[3], Wp[3];
+  f32x2 U[NV][3], Z[NV][3], Wp[NV][3];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) U[i] = Z[i] = Wp[i] = 0ull;
+  for (int t = 0; t < NV; ++t)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) U[t][i] = Z[t][i] = Wp[t][i] = 0ull;
   uint32_t zhist = 0;                                           // zero-vector flags of the last 3 staged rows
 
   auto row_ptr = [&](int r) {
@@ -460,33 +498,38 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
     };
     // ---- a4/a5 + a6, one neighbourhood row at a time ---------------------------
     // v[dxi]: the lane's pair values with offset (dy, dx = dxi - 2)
-    auto eval_row = [&](int sl, auto& v) {
-      constexpr int N = sizeof(v) / sizeof(v[0]);
+    auto eval_row = [&](int sl, auto& vv) {
+      constexpr int N = sizeof(vv[0]) / sizeof(vv[0][0]);
       uint4 q[N];
 #pragma unroll
       for (int dxi = 0; dxi < N; ++dxi) q[dxi] = nbr(sl, dxi - 2);
-      bool amb = false;
+      if constexpr (NV == 2) {
+        ang_both_row<N>(pk0, pk1, nn2, nnn2, q, vv[0], vv[1]);
+      } else {
+        auto& v = vv[0];
+        bool amb = false;
 #if VF_STREAM_RN
-      f32x2 rr[N];
+        f32x2 rr[N];
 #pragma unroll
-      for (int dxi = 0; dxi < N; ++dxi) {
-        const int dx = dxi - 2;
-        const uint2 t = (dx & 1) ? R.OR[sl][l + ((dx - 1) >> 1) + 1] : R.ER[sl][l + (dx >> 1) + 1];
-        rr[dxi] = mul2(rn2, pack2(__uint_as_float(t.x), __uint_as_float(t.y)));
-      }
-      const f32x2* rrp = rr;
+        for (int dxi = 0; dxi < N; ++dxi) {
+          const int dx = dxi - 2;
+          const uint2 t = (dx & 1) ? R.OR[sl][l + ((dx - 1) >> 1) + 1] : R.ER[sl][l + (dx >> 1) + 1];
+          rr[dxi] = mul2(rn2, pack2(__uint_as_float(t.x), __uint_as_float(t.y)));
+        }
+        const f32x2* rrp = rr;
 #else
-      const f32x2* rrp = nullptr;
+        const f32x2* rrp = nullptr;
 #endif
-      if constexpr (VAR == EXACT) ang_mm_row<false, N, true>(pk0, pk1, nn2, nnn2, q, v, amb);
-      else if (zhist == 0u) ang_mm_row<false, N>(pk0, pk1, nn2, nnn2, q, v, amb, rrp);
-      else ang_mm_row<true, N>(pk0, pk1, nn2, nnn2, q, v, amb, rrp);
-      if (VAR != EXACT && VF_STREAM_ACOS != 0 && __any_sync(0xffffffffu, amb)) {
-        // rare: re-load the records (keeping q live across the row would cost registers)
-        uint4 q2[N];
+        if constexpr (VAR == EXACT) ang_mm_row<false, N, true>(pk0, pk1, nn2, nnn2, q, v, amb);
+        else if (zhist == 0u) ang_mm_row<false, N>(pk0, pk1, nn2, nnn2, q, v, amb, rrp);
+        else ang_mm_row<true, N>(pk0, pk1, nn2, nnn2, q, v, amb, rrp);
+        if (VAR != EXACT && VF_STREAM_ACOS != 0 && __any_sync(0xffffffffu, amb)) {
+          // rare: re-load the records (keeping q live across the row would cost registers)
+          uint4 q2[N];
 #pragma unroll
-        for (int dxi = 0; dxi < N; ++dxi) q2[dxi] = nbr(sl, dxi - 2);
-        ang_mm_row_exact<N>(pk0, pk1, nn2, nnn2, q2, v);
+          for (int dxi = 0; dxi < N; ++dxi) q2[dxi] = nbr(sl, dxi - 2);
+          ang_mm_row_exact<N>(pk0, pk1, nn2, nnn2, q2, v);
+        }
       }
     };
     // rows r - d (d = 2, then 1): the partner pixels' H(+d) from values of row r
@@ -501,66 +544,78 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
       hrow(p_p2_0, p_p1_1, lo2(v[2]), hi2(v[1]), n_m2_0, H0);          // pixel (r - d, 2l)
       hrow(p_p2_1, lo2(v[3]), hi2(v[2]), n_m1_0, n_m2_1, H1);          // pixel (r - d, 2l + 1)
     };
-    f32x2 Hm2[3], Hm1[3], H0[3];
-    f32x2 R0[3], R1[3], R2[3];   // roles a = 0 (row r - 2), 1 (row r - 1), 2 (row r), b = 0..2
+    f32x2 Hm2[NV][3], Hm1[NV][3], H0[NV][3];
+    f32x2 R0[NV][3], R1[NV][3], R2[NV][3];   // roles a = 0 (row r - 2), 1 (row r - 1), 2 (row r), b = 0..2
     {
-      f32x2 v[5];
+      f32x2 v[NV][5];
       eval_row(s2, v);                                          // dy = -2
-      hrow2(v[0], v[1], v[2], v[3], v[4], Hm2);
-      float Ha[3], Hb[3];
-      partner_rows(v, Ha, Hb);
 #pragma unroll
-      for (int bb = 0; bb < 3; ++bb) R0[bb] = add2(Wp[bb], pack2(Ha[bb], Hb[bb]));
-    }
-    {
-      f32x2 v[5];
-      eval_row(s1, v);                                          // dy = -1
-      hrow2(v[0], v[1], v[2], v[3], v[4], Hm1);
-      float Ha[3], Hb[3];
-      partner_rows(v, Ha, Hb);
+      for (int t = 0; t < NV; ++t) {
+        hrow2(v[t][0], v[t][1], v[t][2], v[t][3], v[t][4], Hm2[t]);
+        float Ha[3], Hb[3];
+        partner_rows(v[t], Ha, Hb);
 #pragma unroll
-      for (int bb = 0; bb < 3; ++bb) {
-        const f32x2 Hp1 = pack2(Ha[bb], Hb[bb]);
-        R1[bb] = add2(U[bb], Hp1);
-        Wp[bb] = add2(Z[bb], Hp1);
+        for (int bb = 0; bb < 3; ++bb) R0[t][bb] = add2(Wp[t][bb], pack2(Ha[bb], Hb[bb]));
       }
     }
     {
-      f32x2 v[2];
-      eval_row(slot, v);                                        // dy = 0, dx = -2, -1
-      // right values from (q1, lane l+1)
-      const float n_m1_0 = __shfl_down_sync(0xffffffffu, lo2(v[1]), 1);
-      const float n_m2_0 = __shfl_down_sync(0xffffffffu, lo2(v[0]), 1);
-      const float n_m2_1 = __shfl_down_sync(0xffffffffu, hi2(v[0]), 1);
-      float Ha[3], Hb[3];
-      hrow0(lo2(v[0]), lo2(v[1]), hi2(v[1]), n_m2_0, Ha);
-      hrow0(hi2(v[0]), hi2(v[1]), n_m1_0, n_m2_1, Hb);
+      f32x2 v[NV][5];
+      eval_row(s1, v);                                          // dy = -1
 #pragma unroll
-      for (int bb = 0; bb < 3; ++bb) {
-        H0[bb] = pack2(Ha[bb], Hb[bb]);
-        U[bb] = add2(Hm1[bb], H0[bb]);
-        Z[bb] = H0[bb];
-        R2[bb] = add2(U[bb], Hm2[bb]);
+      for (int t = 0; t < NV; ++t) {
+        hrow2(v[t][0], v[t][1], v[t][2], v[t][3], v[t][4], Hm1[t]);
+        float Ha[3], Hb[3];
+        partner_rows(v[t], Ha, Hb);
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) {
+          const f32x2 Hp1 = pack2(Ha[bb], Hb[bb]);
+          R1[t][bb] = add2(U[t][bb], Hp1);
+          Wp[t][bb] = add2(Z[t][bb], Hp1);
+        }
+      }
+    }
+    {
+      f32x2 v[NV][2];
+      eval_row(slot, v);                                        // dy = 0, dx = -2, -1
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        // right values from (q1, lane l+1)
+        const float n_m1_0 = __shfl_down_sync(0xffffffffu, lo2(v[t][1]), 1);
+        const float n_m2_0 = __shfl_down_sync(0xffffffffu, lo2(v[t][0]), 1);
+        const float n_m2_1 = __shfl_down_sync(0xffffffffu, hi2(v[t][0]), 1);
+        float Ha[3], Hb[3];
+        hrow0(lo2(v[t][0]), lo2(v[t][1]), hi2(v[t][1]), n_m2_0, Ha);
+        hrow0(hi2(v[t][0]), hi2(v[t][1]), n_m1_0, n_m2_1, Hb);
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) {
+          H0[t][bb] = pack2(Ha[bb], Hb[bb]);
+          U[t][bb] = add2(Hm1[t][bb], H0[t][bb]);
+          Z[t][bb] = H0[t][bb];
+          R2[t][bb] = add2(U[t][bb], Hm2[t][bb]);
+        }
       }
     }
 
     // ---- a7/a8: the window centred at row r - 1 --------------------------------
     const int gy = r - 1;
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+    const Launch& Lt = t == 0 ? L : L2;
     if (gy >= ty0) {
       // keys: window 2l uses (lane l-1: q1, b = 0), (q0, b = 1), (q1, b = 2);
       // window 2l + 1 uses (q0, b = 0), (q1, b = 1), (lane l+1: q0, b = 2)
-      const float k00 = __shfl_up_sync(0xffffffffu, role_key<0>(hi2(R0[0])), 1);
-      const float k10 = __shfl_up_sync(0xffffffffu, role_key<4>(hi2(R1[0])), 1);
-      const float k20 = __shfl_up_sync(0xffffffffu, role_key<8>(hi2(R2[0])), 1);
-      const float m02 = __shfl_down_sync(0xffffffffu, role_key<2>(lo2(R0[2])), 1);
-      const float m12 = __shfl_down_sync(0xffffffffu, role_key<6>(lo2(R1[2])), 1);
-      const float m22 = __shfl_down_sync(0xffffffffu, role_key<10>(lo2(R2[2])), 1);
-      const float kw0 = fmin3(fmin3(k00, role_key<1>(lo2(R0[1])), role_key<2>(hi2(R0[2]))),
-                              fmin3(k10, role_key<5>(lo2(R1[1])), role_key<6>(hi2(R1[2]))),
-                              fmin3(k20, role_key<9>(lo2(R2[1])), role_key<10>(hi2(R2[2]))));
-      const float kw1 = fmin3(fmin3(role_key<0>(lo2(R0[0])), role_key<1>(hi2(R0[1])), m02),
-                              fmin3(role_key<4>(lo2(R1[0])), role_key<5>(hi2(R1[1])), m12),
-                              fmin3(role_key<8>(lo2(R2[0])), role_key<9>(hi2(R2[1])), m22));
+      const float k00 = __shfl_up_sync(0xffffffffu, role_key<0>(hi2(R0[t][0])), 1);
+      const float k10 = __shfl_up_sync(0xffffffffu, role_key<4>(hi2(R1[t][0])), 1);
+      const float k20 = __shfl_up_sync(0xffffffffu, role_key<8>(hi2(R2[t][0])), 1);
+      const float m02 = __shfl_down_sync(0xffffffffu, role_key<2>(lo2(R0[t][2])), 1);
+      const float m12 = __shfl_down_sync(0xffffffffu, role_key<6>(lo2(R1[t][2])), 1);
+      const float m22 = __shfl_down_sync(0xffffffffu, role_key<10>(lo2(R2[t][2])), 1);
+      const float kw0 = fmin3(fmin3(k00, role_key<1>(lo2(R0[t][1])), role_key<2>(hi2(R0[t][2]))),
+                              fmin3(k10, role_key<5>(lo2(R1[t][1])), role_key<6>(hi2(R1[t][2]))),
+                              fmin3(k20, role_key<9>(lo2(R2[t][1])), role_key<10>(hi2(R2[t][2]))));
+      const float kw1 = fmin3(fmin3(role_key<0>(lo2(R0[t][0])), role_key<1>(hi2(R0[t][1])), m02),
+                              fmin3(role_key<4>(lo2(R1[t][0])), role_key<5>(hi2(R1[t][1])), m12),
+                              fmin3(role_key<8>(lo2(R2[t][0])), role_key<9>(hi2(R2[t][1])), m22));
       const uint32_t nib0 = __float_as_uint(kw0) & 15u, nib1 = __float_as_uint(kw1) & 15u;
       // selected samples: row r - 2 + a, strip column (2l + k) - 1 + b
       const uint32_t* prow0 = R.P[(r - 2) & (SLOTS - 1)];
@@ -576,7 +631,7 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
       // a8: 6 bytes per lane, predicated stores (no divergence)
       VF_CHECK(!(ov0 || ov1) || (gy >= L.out_row0 && gy < L.out_row0 + L.out_rows && xa + (ov0 ? 0 : 1) >= 0 &&
                                   xa + (ov1 ? 1 : 0) < W));
-      uint8_t* op = L.out + (long long)b * L.out_stride + ((long long)(gy - L.out_row0) * W + xa) * 3;
+      uint8_t* op = Lt.out + (long long)b * Lt.out_stride + ((long long)(gy - L.out_row0) * W + xa) * 3;
       if (((uintptr_t)op & 1u) == 0) {                          // warp-uniform: U16, U8 U8, U16
         if (ov0) *reinterpret_cast<uint16_t*>(op) = (uint16_t)o0;
         if (ov0) op[2] = (uint8_t)(o0 >> 16);
@@ -588,33 +643,34 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
         if (ov1) *reinterpret_cast<uint16_t*>(op + 3) = (uint16_t)o1;
         if (ov1) op[5] = (uint8_t)(o1 >> 16);
       }
-      if (L.idx || L.agg) {
+      if (Lt.idx || Lt.agg) {
         // parity runs only: the index (raster 3a + b) and the exact aggregates
-        const float f00 = __shfl_up_sync(0xffffffffu, hi2(R0[0]), 1), f10 = __shfl_up_sync(0xffffffffu, hi2(R1[0]), 1),
-                    f20 = __shfl_up_sync(0xffffffffu, hi2(R2[0]), 1);
-        const float g02 = __shfl_down_sync(0xffffffffu, lo2(R0[2]), 1), g12 = __shfl_down_sync(0xffffffffu, lo2(R1[2]), 1),
-                    g22 = __shfl_down_sync(0xffffffffu, lo2(R2[2]), 1);
+        const float f00 = __shfl_up_sync(0xffffffffu, hi2(R0[t][0]), 1), f10 = __shfl_up_sync(0xffffffffu, hi2(R1[t][0]), 1),
+                    f20 = __shfl_up_sync(0xffffffffu, hi2(R2[t][0]), 1);
+        const float g02 = __shfl_down_sync(0xffffffffu, lo2(R0[t][2]), 1), g12 = __shfl_down_sync(0xffffffffu, lo2(R1[t][2]), 1),
+                    g22 = __shfl_down_sync(0xffffffffu, lo2(R2[t][2]), 1);
         const long long npix_img = (long long)L.out_rows * W;
         const long long po = (long long)(gy - L.out_row0) * W + xa;
         if (ov0) {
-          if (L.idx) L.idx[b * npix_img + po] = (uint8_t)(3 * (nib0 >> 2) + (nib0 & 3u));
-          if (L.agg) {
-            float* ag = L.agg + (b * npix_img + po) * 9;
-            ag[0] = f00; ag[1] = lo2(R0[1]); ag[2] = hi2(R0[2]);
-            ag[3] = f10; ag[4] = lo2(R1[1]); ag[5] = hi2(R1[2]);
-            ag[6] = f20; ag[7] = lo2(R2[1]); ag[8] = hi2(R2[2]);
+          if (Lt.idx) Lt.idx[b * npix_img + po] = (uint8_t)(3 * (nib0 >> 2) + (nib0 & 3u));
+          if (Lt.agg) {
+            float* ag = Lt.agg + (b * npix_img + po) * 9;
+            ag[0] = f00; ag[1] = lo2(R0[t][1]); ag[2] = hi2(R0[t][2]);
+            ag[3] = f10; ag[4] = lo2(R1[t][1]); ag[5] = hi2(R1[t][2]);
+            ag[6] = f20; ag[7] = lo2(R2[t][1]); ag[8] = hi2(R2[t][2]);
           }
         }
         if (ov1) {
-          if (L.idx) L.idx[b * npix_img + po + 1] = (uint8_t)(3 * (nib1 >> 2) + (nib1 & 3u));
-          if (L.agg) {
-            float* ag = L.agg + (b * npix_img + po + 1) * 9;
-            ag[0] = lo2(R0[0]); ag[1] = hi2(R0[1]); ag[2] = g02;
-            ag[3] = lo2(R1[0]); ag[4] = hi2(R1[1]); ag[5] = g12;
-            ag[6] = lo2(R2[0]); ag[7] = hi2(R2[1]); ag[8] = g22;
+          if (Lt.idx) Lt.idx[b * npix_img + po + 1] = (uint8_t)(3 * (nib1 >> 2) + (nib1 & 3u));
+          if (Lt.agg) {
+            float* ag = Lt.agg + (b * npix_img + po + 1) * 9;
+            ag[0] = lo2(R0[t][0]); ag[1] = hi2(R0[t][1]); ag[2] = g02;
+            ag[3] = lo2(R1[t][0]); ag[4] = hi2(R1[t][1]); ag[5] = g12;
+            ag[6] = lo2(R2[t][0]); ag[7] = hi2(R2[t][1]); ag[8] = g22;
           }
         }
       }
+    }
     }
     __syncwarp();   // ring slot (r + 1) & 3 = (r - 3) & 3 is no longer read
   }
@@ -624,6 +680,7 @@ __global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB) vf_angular
 // defined in vf_stream.cu, whose compile flags (tuning knobs) fix the ring layout
 const void* stream_kernel_fn_mm();
 const void* stream_kernel_fn_ex();
+const void* stream_kernel_fn_both();
 size_t stream_smem_bytes();
 #endif
 

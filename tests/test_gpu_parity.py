@@ -448,15 +448,16 @@ def test_c4_full_batch_sampled(crit, var):
 # ------------------------------------------------------------- plan (CUDA-graph executor)
 def test_fused_plan_large_batch():
     """A plan of >= 2^21 pixels fuses its exp/log filters into one kernel node
-    (shared staging and S1): 3 kernel nodes for the 7 filters, outputs
+    (shared staging and S1) and its angular exact + minimax into another (one
+    geometry evaluation): 2 kernel nodes for the 7 filters, outputs
     bit-identical to each filter's own kernel, and to VF_PLAN_FUSE=0 plans
     (the single-filter nodes)."""
-    spec = dataclasses.replace(vfsynth.config("C4"), batch=6)
-    xb = torch.from_numpy(vfsynth.make_batch(spec)).cuda()          # 6 x 512 x 768 = 2.36 M pixels
+    spec = dataclasses.replace(vfsynth.config("C4"), batch=32)
+    xb = torch.from_numpy(vfsynth.make_batch(spec)).cuda()          # 32 x 512 x 768: both fusions apply
     combos = CV[:7]
     outs = [torch.empty_like(xb) for _ in combos]
     plan = vfb.Plan(xb, outs, 3, combos)
-    assert plan.kernels() == 3
+    assert plan.kernels() == 2                                   # exp/log node + angular node
     plan.launch()
     torch.cuda.synchronize()
     for (crit, var), o in zip(combos, outs):
@@ -465,6 +466,8 @@ def test_fused_plan_large_batch():
         assert torch.equal(o, ref), (crit, var)
     small = vfb.Plan(xb[:1].contiguous(), [torch.empty_like(xb[:1]) for _ in combos], 3, combos)
     assert small.kernels() == 7
+    mid = vfb.Plan(xb[:6].contiguous(), [torch.empty_like(xb[:6]) for _ in combos], 3, combos)
+    assert mid.kernels() == 3                                    # exp/log fused, angular not streamed
 
 
 
