@@ -517,6 +517,7 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
   // forms S1 once (vf_fused.cu; outputs bit-identical to the single-filter
   // kernels).  VF_PLAN_FUSE=0 keeps one node per filter.
   static const bool env_no_fuse = [] { const char* e = std::getenv("VF_PLAN_FUSE"); return e && e[0] == '0'; }();
+  static const bool env_force_fuse = [] { const char* e = std::getenv("VF_PLAN_FUSE"); return e && e[0] == '2'; }();
   bool fused[64] = {};
   {
     int idx[8], m = 0;
@@ -524,7 +525,7 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
       if (criteria[i] == VF_EXP || criteria[i] == VF_LOG) idx[m++] = i;
     // (small inputs keep one node per filter: the graph's concurrency then
     // matters more than the shared staging -- C2: 70 vs 60 us)
-    const bool fuse_big = (long long)B * H * W >= (1LL << 21);
+    const bool fuse_big = env_force_fuse || (long long)B * H * W >= (1LL << 21);
     if (m >= 2 && !env_no_fuse && window <= 5 && fuse_big) {
       vf::ElFused F = {};
       F.n = m;
@@ -538,7 +539,7 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
         fused[idx[k]] = true;
       }
       int opt = 1, nty = vf::TY;
-      const bool big = window == 3;
+      const bool big = window == 3 && (long long)B * H * W >= (1LL << 21);
       cudaKernelNodeParams kp = {};
       kp.func = (void*)vf::el_fused_kernel(window, big, &opt, &nty);
       kp.gridDim = dim3((W + vf::TX - 1) / vf::TX, (H + nty * opt - 1) / (nty * opt), B);

@@ -79,9 +79,13 @@ const void* el_fused_kernel(int window, bool big, int* opt, int* nty) {
     *nty = VF_FUSED_NTY3;
     return (const void*)vf_el_fused_kernel<3, VF_FUSED_OPT3, VF_FUSED_NTY3>;
   }
+#ifndef VF_FUSED_SMALL_NTY
+#define VF_FUSED_SMALL_NTY 8
+#endif
   *opt = 1;
-  *nty = TY;
-  return window == 3 ? (const void*)vf_el_fused_kernel<3, 1, TY> : (const void*)vf_el_fused_kernel<5, 1, TY>;
+  *nty = VF_FUSED_SMALL_NTY;
+  return window == 3 ? (const void*)vf_el_fused_kernel<3, 1, VF_FUSED_SMALL_NTY>
+                     : (const void*)vf_el_fused_kernel<5, 1, VF_FUSED_SMALL_NTY>;
 }
 
 }  // namespace vf

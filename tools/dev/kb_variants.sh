@@ -1,3 +1,4 @@
+# dev scratch (round-2 tuning): A/B of library variants built with build.py --variant
 # A/B timing of library variants (VARIANTS="main rn1 ..."; main = libvf.so) and,
 # with CHECK=1, a parity check of each variant on a C2-size image first.
 for v in ${VARIANTS:-main}; do

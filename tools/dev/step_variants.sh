@@ -1,3 +1,4 @@
+# dev scratch (round-2 tuning): A/B of library variants built with build.py --variant
 # step-time A/B of library variants: VARIANTS="main f24 ..." (main = libvf.so)
 for v in ${VARIANTS:-main}; do
   if [ "$v" = "main" ]; then lib=paper_1009_0959_b200/libvf.so; else lib=paper_1009_0959_b200/libvf_$v.so; fi
