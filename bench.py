@@ -561,23 +561,50 @@ def run_ours(args):
     clk.stop()
     reach = {k: kern.pop(k) for k in [f"{c[0]}/{c[1]}" for c in REACH_COMBOS] if k in kern}
     roofline = roofline_mm = None
+    nodes = None
     if kern:
-        dom = max(kern, key=lambda k: kern[k]["ms"])
-        d = kern[dom]
-        roofline = {"bound": "alu", "kernel": dom, "kernel_name": d["kernel"], "achieved": d["alg_tflops"],
+        # the step's kernel nodes: the plan fuses filters (exp/log; angular
+        # exact + minimax), so each node is timed as a plan of its member
+        # filters, with the members' algorithmic flops
+        groups = [("exp/log fused node", [c for c in COMBOS if c[0] in ("exp", "log")]),
+                  ("angular fused node", [c for c in COMBOS if c[0] == "angular"])]
+        nodes = {}
+        for gname, gcs in groups:
+            gplan = vfb.Plan(x, [oc[c] for c in gcs], w, gcs)
+            nk = gplan.kernels()
+            gms = kernel_avg_ms(torch, dev, stream, lambda gp=gplan: gp.launch(stream), reps,
+                                flush if args.workload == "c2" else None)
+            gfl = sum(FLOPS_PER_PAIR[c] for c in gcs) * 36 * npix_l
+            gsfu = sum(SFU_PER_PAIR[c] for c in gcs) * 36 * npix_l
+            names = sorted({kernel_entry(vfb, c, w, Bl, H, W, 1.0, peaks, None, npix_l)["kernel"] for c in gcs})
+            marker = "vf_el_fused_kernel" if gname.startswith("exp") else "vf_angular_stream_kernelILi1ELi2E"
+            rec = None
+            if ncu is not None and args.workload == "c4" and world == 1 and Bl == 1024:
+                rec = next((v for k, v in ncu.get("kernels", {}).items() if marker in k), None)
+            nodes[gname] = {"filters": [f"{c[0]}/{c[1]}" for c in gcs], "kernel_nodes": nk, "ms": gms, "ncu": rec,
+                            "alg_tflops": gfl / (gms / 1e3) / 1e12,
+                            "frac_fp32_alg": gfl / (gms / 1e3) / 1e12 / peaks["fp32_tflops"],
+                            "frac_sfu_alg": gsfu / (gms / 1e3) / 1e12 / peaks["sfu_tops"],
+                            "algorithmic_flops_per_launch": gfl,
+                            "sum_single_filter_kernels_ms": sum(kern[f"{c[0]}/{c[1]}"]["ms"] for c in gcs),
+                            "single_filter_kernel_names": names}
+            gplan.close()
+        dom = max(nodes, key=lambda k: nodes[k]["ms"])
+        d = nodes[dom]
+        roofline = {"bound": "alu", "kernel": dom, "filters": d["filters"], "achieved": d["alg_tflops"],
                     "peak": peaks["fp32_tflops"], "unit": "TFLOP/s", "frac": d["frac_fp32_alg"],
                     "avg_launch_ms": d["ms"], "share_of_step": d["ms"] / ms_per_step,
                     "traffic": (d.get("ncu") or {}).get("dram_bytes"),
-                    "algorithmic_bytes": npix_l * 6,
-                    "algorithmic_flops_per_launch": FLOPS_PER_PAIR[tuple(dom.split("/"))] * 36 * npix_l,
+                    "algorithmic_bytes": npix_l * 3 * (1 + len(d["filters"])),
+                    "algorithmic_flops_per_launch": d["algorithmic_flops_per_launch"],
                     "peak_source": peaks["source"],
-                    "timing": "average launch duration of the kernel over the whole local batch (%d launches between "
-                              "CUDA events on the launching stream; input %d MiB%s)" % (
+                    "timing": "average duration of the node (a plan of its member filters) over the whole local batch "
+                              "(%d launches between CUDA events on the launching stream; input %d MiB%s)" % (
                                   reps, x.numel() >> 20, " > L2" if x.numel() > (126 << 20) else
                                   ", L2 flushed before the launches"),
-                    "note": ("the step's dominant kernel is an exact (libm) variant: SURVEY 8(d) D4 counts only the "
-                             "arithmetic around the libm call, so its algorithmic fraction is low by construction; "
-                             "roofline_minimax holds the paper's approximants") if dom.endswith("exact") else None}
+                    "note": "the step's dominant node holds the exact (libm) exp/log filters: SURVEY 8(d) D4 counts "
+                            "only the arithmetic around each libm call, so its algorithmic fraction is low by "
+                            "construction; roofline_minimax holds the paper's approximants (single-filter kernels)"}
         mm = {k: v["frac_fp32_alg"] for k, v in kern.items() if not k.endswith("exact")}
         a = kern["angular/minimax"]
         roofline_mm = {"bound": "alu", "kernel": "angular/minimax (BVDF, Eq. 5 + Table 1)", "kernel_name": a["kernel"],
@@ -632,7 +659,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": cfg,
-            "roofline": roofline, "roofline_minimax": roofline_mm, "per_kernel": kern,
+            "roofline": roofline, "roofline_minimax": roofline_mm, "per_kernel": kern, "per_node": nodes,
             "step_breakdown": {"stats_multi_ms": t_stats, "sum_kernel_ms": sum(v["ms"] for v in kern.values()),
                                "step_ms": ms_per_step,
                                "note": "the plan's 7 kernels run concurrently; sum_kernel_ms is their serial sum"},

@@ -25,6 +25,12 @@ for cfg, w, ids in (("C4", 3, range(images)), ("C3", 5, range(8))):
         outs[c] = torch.empty_like(x)
         vfb.vf_filter_batch(x, w, *c, out=outs[c], stream=stream)
     if cfg == "C4":
+        # the step's fused plan nodes (exp/log; angular exact + minimax)
+        for gcs in ([c for c in bench.COMBOS if c[0] in ("exp", "log")], [c for c in bench.COMBOS if c[0] == "angular"]):
+            gp = vfb.Plan(x, [outs[c] for c in gcs], w, gcs)
+            gp.launch(stream)
+            torch.cuda.synchronize()
+            gp.close()
         n = sum(len(cs) for _, cs in bench.FIDELITY_GROUPS)
         st = torch.empty((n, x.shape[0], 8), dtype=torch.float64, device=dev)
         k = 0
