@@ -35,6 +35,7 @@ struct ElFused {
   int n;
 };
 const void* el_fused_kernel(int window, bool big, int* opt, int* nty);
+const void* el_fused5_kernel(int* opt, int* nty);
 }  // namespace vf
 
 namespace {
@@ -542,6 +543,27 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
       const bool big = window == 3 && (long long)B * H * W >= (1LL << 21);
       cudaKernelNodeParams kp = {};
       kp.func = (void*)vf::el_fused_kernel(window, big, &opt, &nty);
+      // the canonical 5-filter set (exp exact / minimax / poly4, log exact /
+      // minimax): the pair-major kernel, filters reordered to its layout
+      static const bool env_no_pm = [] { const char* e = std::getenv("VF_FUSED5"); return e && e[0] == '0'; }();
+      const int canon[5] = {4 * vf::EXPC + vf::EXACT, 4 * vf::EXPC + vf::MINIMAX, 4 * vf::EXPC + vf::POLY4,
+                            4 * vf::LOGC + vf::EXACT, 4 * vf::LOGC + vf::MINIMAX};
+      if (window == 3 && big && m == 5 && !env_no_pm) {
+        vf::ElFused G = {};
+        bool ok = true;
+        for (int c = 0; c < 5 && ok; ++c) {
+          int hit = -1;
+          for (int k = 0; k < 5; ++k)
+            if (F.code[k] == canon[c]) hit = k;
+          if (hit < 0) ok = false;
+          else { G.L[c] = F.L[hit]; G.code[c] = canon[c]; }
+        }
+        if (ok) {
+          G.n = 5;
+          F = G;
+          kp.func = (void*)vf::el_fused5_kernel(&opt, &nty);
+        }
+      }
       kp.gridDim = dim3((W + vf::TX - 1) / vf::TX, (H + nty * opt - 1) / (nty * opt), B);
       kp.blockDim = dim3(vf::TX, nty);
       kp.sharedMemBytes = 0;
