@@ -122,8 +122,11 @@ __device__ __forceinline__ void el_window5(const ElFused& F, int b, int ox, int 
   }
 }
 
+#ifndef VF_FUSED5_MINB
+#define VF_FUSED5_MINB 3   // <= 85 registers (80, 24 B of spills): step 64.7 vs 65.0 ms (1: 107 registers)
+#endif
 template <int WIN, int OPT, int NTY>
-__global__ void __launch_bounds__(TX * NTY) vf_el_fused5_kernel(const ElFused F) {
+__global__ void __launch_bounds__(TX * NTY, VF_FUSED5_MINB) vf_el_fused5_kernel(const ElFused F) {
   constexpr int R = WIN / 2;
   constexpr int TYE = NTY * OPT;
   constexpr int SW = TX + 2 * R;

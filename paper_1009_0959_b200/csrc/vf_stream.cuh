@@ -417,8 +417,11 @@ __device__ __forceinline__ void unpack_pair(const PairWords& r, const PairLoad& 
 // NV = 2 (VAR = MINIMAX): both variants from one geometry evaluation per pair
 // (plan-level fusion of BVDF minimax and exact): L writes the minimax output,
 // L2 the exact one; NV = 1: the variant VAR into L (L2 unused).
+#ifndef VF_STREAM_MINB2
+#define VF_STREAM_MINB2 VF_STREAM_MINB   // the fused (NV = 2) kernel
+#endif
 template <int VAR, int NV = 1>
-__global__ void __launch_bounds__(32 * stream::NWARP, VF_STREAM_MINB)
+__global__ void __launch_bounds__(32 * stream::NWARP, NV == 2 ? VF_STREAM_MINB2 : VF_STREAM_MINB)
     vf_angular_stream_kernel(const Launch L, int K, const Launch L2) {
   using namespace stream;
   static_assert(VAR == MINIMAX || VAR == EXACT, "streamed kernel: angular minimax or exact");
