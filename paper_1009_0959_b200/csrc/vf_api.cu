@@ -70,11 +70,17 @@ struct KernelDesc {
   bool tma = false;          // vf_el_tma_kernel: (map, L, tiles_x, tiles_y, ntiles)
   alignas(64) CUtensorMap map;
   int tiles_x = 0, tiles_y = 0, ntiles = 0;
-  int stream_k = 0;          // vf_angular_stream_kernel: (L, K, L2)
+  int stream_k = 0;          // vf_angular_stream_kernel: (L, K, L2, nimg)
+  int stream_b = 0;          //   nimg = the batch size
   Launch L2;                 // the fused kernel's second output (exact); = L otherwise
+  // optional second launch with the same parameters (the streamed kernels'
+  // half-warp remainder strips, vf_stream.cuh); independent of the first
+  const void* fn_tail = nullptr;
+  dim3 grid_tail;
+  size_t smem_tail = 0;
   void* args[5];
   void** params() {
-    if (stream_k) { args[0] = &L; args[1] = &stream_k; args[2] = &L2; return args; }
+    if (stream_k) { args[0] = &L; args[1] = &stream_k; args[2] = &L2; args[3] = &stream_b; return args; }
     if (!tma) { args[0] = &L; return args; }
     args[0] = &map; args[1] = &L; args[2] = &tiles_x; args[3] = &tiles_y; args[4] = &ntiles;
     return args;
@@ -230,12 +236,23 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
                        !env_no_stream && !(var == VF_EXACT && env_no_stream_ex)))) {
     static const int k_env = [] { const char* e = std::getenv("VF_STREAM_K"); return e ? std::atoi(e) : 0; }();
     const int K = (k_env >= 2 && k_env <= 1024) ? k_env : vf::stream_rows_per_warp(strips * out_rows * (long long)B);
+    // the last strip of each image on half a warp when it has <= 30 output
+    // columns (vf_stream.cuh; C4 3x3 minimax 1.50 -> 1.45 ms per 256 images);
+    // VF_STREAM_HALF=0 keeps full-warp strips everywhere
+    static const bool env_no_half = [] { const char* e = std::getenv("VF_STREAM_HALF"); return e && e[0] == '0'; }();
+    const bool split = !env_no_half && B >= 2 && vf::stream::half_tail(W);
     kd->fn = var == VF_EXACT ? vf::stream_kernel_fn_ex() : vf::stream_kernel_fn_mm();
-    kd->grid = vf::stream_grid(L, B, K);
+    kd->grid = vf::stream_grid(L, B, K, split, false);
     kd->block = dim3(vf::stream_block_threads());
     kd->smem = vf::stream_smem_bytes();
     kd->stream_k = K;
+    kd->stream_b = B;
     kd->L2 = L;
+    if (split) {
+      kd->fn_tail = var == VF_EXACT ? vf::stream_kernel_fn_ex(true) : vf::stream_kernel_fn_mm(true);
+      kd->grid_tail = vf::stream_grid(L, B, K, true, true);
+      kd->smem_tail = vf::stream_smem_bytes(true);
+    }
     if (kd->grid.y > 65535 || kd->grid.z > 65535) return fail(VF_EINVAL, "grid too large");
     return VF_OK;
   }
@@ -359,7 +376,31 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
 int launch_desc(KernelDesc& kd, cudaStream_t st) {
   cudaError_t e = cudaLaunchKernel(kd.fn, kd.grid, kd.block, kd.params(), kd.smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  if (kd.fn_tail) {
+    e = cudaLaunchKernel(kd.fn_tail, kd.grid_tail, kd.block, kd.params(), kd.smem_tail, st);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch (remainder strips)");
+  }
   return VF_OK;
+}
+
+// The kernel node(s) of a description (the remainder-strip launch as a second,
+// independent node), each depending on dep (nullable); returns the count.
+int add_kernel_nodes(cudaGraph_t g, KernelDesc& kd, cudaGraphNode_t dep, cudaGraphNode_t* nodes, const char* what) {
+  cudaKernelNodeParams kp = {};
+  kp.func = (void*)kd.fn;
+  kp.gridDim = kd.grid;
+  kp.blockDim = kd.block;
+  kp.sharedMemBytes = (unsigned)kd.smem;
+  kp.kernelParams = kd.params();
+  cudaError_t e = cudaGraphAddKernelNode(&nodes[0], g, dep ? &dep : nullptr, dep ? 1 : 0, &kp);
+  if (e != cudaSuccess) return -cuda_fail(e, what);
+  if (!kd.fn_tail) return 1;
+  kp.func = (void*)kd.fn_tail;
+  kp.gridDim = kd.grid_tail;
+  kp.sharedMemBytes = (unsigned)kd.smem_tail;
+  e = cudaGraphAddKernelNode(&nodes[1], g, dep ? &dep : nullptr, dep ? 1 : 0, &kp);
+  if (e != cudaSuccess) return -cuda_fail(e, what);
+  return 2;
 }
 
 int launch(const uint8_t* in, long long in_stride, int band_row0, int band_rows, int B, int H, int W, int out_row0,
@@ -604,23 +645,18 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
       if (rc) return bail(rc);
       if (km.stream_k && ke.stream_k) {               // both streamed (large launches)
         km.fn = vf::stream_kernel_fn_both();
+        if (km.fn_tail) km.fn_tail = vf::stream_kernel_fn_both(true);
         km.L2 = ke.L;
-        cudaKernelNodeParams kp = {};
-        kp.func = (void*)km.fn;
-        kp.gridDim = km.grid;
-        kp.blockDim = km.block;
-        kp.sharedMemBytes = (unsigned)km.smem;
-        kp.kernelParams = km.params();
-        cudaGraphNode_t kn;
-        e = cudaGraphAddKernelNode(&kn, p->graph, h2d ? &h2d : nullptr, h2d ? 1 : 0, &kp);
-        if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddKernelNode (fused angular)"));
-        ++p->nkernels;
+        cudaGraphNode_t kn[2];
+        const int nk = add_kernel_nodes(p->graph, km, h2d, kn, "cudaGraphAddKernelNode (fused angular)");
+        if (nk < 0) return bail(-nk);
+        p->nkernels += nk;
         fused[im] = fused[ie] = true;
         if (h_outs) {
           const int ids[2] = {im, ie};
           for (int k = 0; k < 2; ++k) {
             cudaGraphNode_t d2h;
-            e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, &kn, 1, h_outs[ids[k]], d_outs[ids[k]], bytes,
+            e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, kn, nk, h_outs[ids[k]], d_outs[ids[k]], bytes,
                                          cudaMemcpyDeviceToHost);
             if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (D2H)"));
           }
@@ -634,19 +670,13 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
     int rc = describe(&kd, d_in, stride, 0, H, B, H, W, 0, H, window, criteria[i], variants[i], VF_ALGO_AUTO,
                       d_outs[i], stride, nullptr, nullptr);
     if (rc) return bail(rc);
-    cudaKernelNodeParams kp = {};
-    kp.func = (void*)kd.fn;
-    kp.gridDim = kd.grid;
-    kp.blockDim = kd.block;
-    kp.sharedMemBytes = (unsigned)kd.smem;
-    kp.kernelParams = kd.params();
-    cudaGraphNode_t kn;
-    e = cudaGraphAddKernelNode(&kn, p->graph, h2d ? &h2d : nullptr, h2d ? 1 : 0, &kp);
-    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddKernelNode"));
-    ++p->nkernels;
+    cudaGraphNode_t kn[2];
+    const int nk = add_kernel_nodes(p->graph, kd, h2d, kn, "cudaGraphAddKernelNode");
+    if (nk < 0) return bail(-nk);
+    p->nkernels += nk;
     if (h_outs) {
       cudaGraphNode_t d2h;
-      e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, &kn, 1, h_outs[i], d_outs[i], bytes, cudaMemcpyDeviceToHost);
+      e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, kn, nk, h_outs[i], d_outs[i], bytes, cudaMemcpyDeviceToHost);
       if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (D2H)"));
     }
   }

@@ -63,7 +63,9 @@ constexpr int PW = SW + 8;      // plain pixel row: strip column j at index j + 
 #define VF_STREAM_RN 0   // 1: per-pixel 1/|x| in the ring, r = rn_p rn_q by FMUL2 instead of MUFU.RSQ(Ph)
 #endif
 
-struct Ring {
+template <int SEG>
+struct RingT {                  // one per strip of 2 SEG columns (SEG = 32: one per warp)
+  static constexpr int NE = SEG + 2, NO = SEG + 1, PW = 2 * SEG + 8;
   uint4 E[SLOTS][NE];           // (pk(2e-2), pk(2e-1), |x|^2, |x|^2)
   uint4 O[SLOTS][NO];           // (pk(2o-1), pk(2o),   |x|^2, |x|^2)
   uint32_t P[SLOTS][PW];        // packed pixels (the selected sample is read back from here)
@@ -72,6 +74,8 @@ struct Ring {
   uint2 OR[SLOTS][NO];          // of the O pairs
 #endif
 };
+using Ring = RingT<32>;
+static_assert(Ring::NE == NE && Ring::NO == NO && Ring::PW == PW, "ring layout");
 // Columns -2, -1, 64 and 65 (E[0], E[33], the first half of O[0], the second
 // half of O[32]) are never written: a window centred at strip column c only
 // reads the roles (c-1, b=0), (c, b=1), (c+1, b=2), i.e. the pair values
@@ -80,6 +84,18 @@ struct Ring {
 
 // strip s covers image columns x0 + j, x0 = 62 s - 1, j = 0..63
 __host__ __device__ constexpr int strip_x0(int s) { return SOUT * s - J_LO; }
+
+// Remainder strips: when the last strip of an image has at most 30 output
+// columns (W - 62 (S - 1) <= 30, S = ceil(W / 62); C4's 768 = 12 x 62 + 24,
+// C2's 512 = 8 x 62 + 16), it is computed by HALF a warp -- 16 lanes, 32
+// columns -- and the two half-warps of a warp take the last strips of two
+// images (a separate launch of the SEG = 16 kernel, grid (1, *, ceil(B / 2))).
+// The full strips' work is unchanged; the last strip costs half the warps.
+constexpr int SOUT_HALF = 30;
+__host__ __device__ constexpr int strips_of(int W) { return (W + SOUT - 1) / SOUT; }
+__host__ __device__ constexpr bool half_tail(int W) {
+  return strips_of(W) >= 2 && W - SOUT * (strips_of(W) - 1) <= SOUT_HALF;
+}
 
 }  // namespace stream
 
@@ -408,9 +424,12 @@ __device__ __forceinline__ void unpack_pair(const PairWords& r, const PairLoad& 
   p1 = pl.hi1 ? q1 : q0;
 }
 
-// grid (ceil(W / 62), ceil(out_rows / (K NWARP)), B), block 32 NWARP; dynamic
-// smem NWARP * sizeof(Ring).  Warp w of block (sx, sy) streams strip sx over
-// output rows [out_row0 + (sy NWARP + w) K, + K).  Requires W >= 2.
+// SEG = 32: grid (S or S - 1, ceil(out_rows / (K NWARP)), B), block 32 NWARP;
+// dynamic smem NWARP * sizeof(Ring).  Warp w of block (sx, sy) streams strip
+// sx of image z over output rows [out_row0 + (sy NWARP + w) K, + K).
+// SEG = 16 (half_tail(W)): grid (1, *, ceil(B / 2)); half-warp h of warp w
+// streams the LAST strip of image 2 z + h (a ghost copy of image B - 1 that
+// stores nothing when 2 z + h = B).  nimg = B.  Requires W >= 2.
 #ifndef VF_STREAM_MINB
 #define VF_STREAM_MINB (20 / VF_STREAM_NWARP)   // resident blocks per SM: 20 warps per SM, <= 102 registers
 #endif
@@ -420,31 +439,42 @@ __device__ __forceinline__ void unpack_pair(const PairWords& r, const PairLoad& 
 #ifndef VF_STREAM_MINB2
 #define VF_STREAM_MINB2 VF_STREAM_MINB   // the fused (NV = 2) kernel
 #endif
-template <int VAR, int NV = 1>
+template <int SEG>
+__device__ __forceinline__ float shup(float v, int d) { return __shfl_up_sync(0xffffffffu, v, d, SEG); }
+template <int SEG>
+__device__ __forceinline__ float shdn(float v, int d) { return __shfl_down_sync(0xffffffffu, v, d, SEG); }
+template <int SEG>
+__device__ __forceinline__ uint32_t shdn(uint32_t v, int d) { return __shfl_down_sync(0xffffffffu, v, d, SEG); }
+
+template <int VAR, int NV = 1, int SEG = 32>
 __global__ void __launch_bounds__(32 * stream::NWARP, NV == 2 ? VF_STREAM_MINB2 : VF_STREAM_MINB)
-    vf_angular_stream_kernel(const Launch L, int K, const Launch L2) {
+    vf_angular_stream_kernel(const Launch L, int K, const Launch L2, int nimg) {
   using namespace stream;
   static_assert(VAR == MINIMAX || VAR == EXACT, "streamed kernel: angular minimax or exact");
   static_assert(NV == 1 || (NV == 2 && VAR == MINIMAX), "fused: minimax + exact");
+  static_assert(SEG == 32 || SEG == 16, "full or half-warp strips");
+  constexpr int SOUTS = 2 * SEG - 2;                            // output columns of the strip
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
-  Ring& R = reinterpret_cast<Ring*>(smem_raw)[warp];
-  const int b = blockIdx.z;
-  const int x0 = strip_x0(blockIdx.x);
+  const int warp = threadIdx.x >> 5, l = threadIdx.x & (SEG - 1), seg = (threadIdx.x & 31) / SEG;
+  RingT<SEG>& R = reinterpret_cast<RingT<SEG>*>(smem_raw)[warp * (32 / SEG) + seg];
+  int b = SEG == 32 ? (int)blockIdx.z : 2 * (int)blockIdx.z + seg;
+  const bool ghost = b >= nimg;                                 // half-warp past the last image
+  if (ghost) b = nimg - 1;
+  const int x0 = SEG == 32 ? strip_x0(blockIdx.x) : strip_x0(strips_of(L.W) - 1);
   const int ty0 = L.out_row0 + (blockIdx.y * NWARP + warp) * K;
   const int ty1 = min(ty0 + K, L.out_row0 + L.out_rows);
   if (ty0 >= ty1) return;                                       // warp-uniform
   const int W = L.W;
   const uint8_t* __restrict__ in = L.in + (long long)b * L.in_stride;
-  const uint8_t* in_end = L.in + (long long)(gridDim.z - 1) * L.in_stride + (long long)L.band_rows * W * 3;
+  const uint8_t* in_end = L.in + (long long)(nimg - 1) * L.in_stride + (long long)L.band_rows * W * 3;
   const int xa = x0 + 2 * l;                                    // image column of the lane's first pixel
   PairLoad pl;
   pl.x_lo = clampi(xa, 0, W - 2);
   pl.hi0 = clampi(xa, 0, W - 1) != pl.x_lo;
   pl.hi1 = clampi(xa + 1, 0, W - 1) != pl.x_lo;
-  // output columns: strip j = 2l + k, valid for j in [1, 62] inside the image
-  const bool ov0 = 2 * l >= J_LO && 2 * l < J_LO + SOUT && xa < W;
-  const bool ov1 = 2 * l + 1 >= J_LO && 2 * l + 1 < J_LO + SOUT && xa + 1 < W;
+  // output columns: strip j = 2l + k, valid for j in [1, 2 SEG - 2] inside the image
+  const bool ov0 = !ghost && 2 * l >= J_LO && 2 * l < J_LO + SOUTS && xa < W;
+  const bool ov1 = !ghost && 2 * l + 1 >= J_LO && 2 * l + 1 < J_LO + SOUTS && xa + 1 < W;
   const int rowb = W * 3;
 
   // carried partial role sums (packed over the lane's two pixels):
@@ -478,15 +508,15 @@ __global__ void __launch_bounds__(32 * stream::NWARP, NV == 2 ? VF_STREAM_MINB2 
     const f32x2 nn2 = sub2(nnb, pack2(F2P23, F2P23));
     const f32x2 nnn2 = sub2(pack2(F2P23, F2P23), nnb);
     const float nn0 = lo2(nn2), nn1 = hi2(nn2);
-    const uint32_t pk2 = __shfl_down_sync(0xffffffffu, pk0, 1);  // column 2l + 2 (lane 31: unused)
-    const float nn2n = __shfl_down_sync(0xffffffffu, nn0, 1);
+    const uint32_t pk2 = shdn<SEG>(pk0, 1);  // column 2l + 2 (last lane: unused)
+    const float nn2n = shdn<SEG>(nn0, 1);
     R.E[slot][l + 1] = make_uint4(pk0, pk1, __float_as_uint(nn0), __float_as_uint(nn1));
     R.O[slot][l + 1] = make_uint4(pk1, pk2, __float_as_uint(nn1), __float_as_uint(nn2n));
     if (l == 0) R.O[slot][0] = make_uint4(0u, pk0, 0u, __float_as_uint(nn0));   // column 0 as an O-pair's second pixel
 #if VF_STREAM_RN
     const float rn0 = rsqrt_approx(nn0), rn1 = rsqrt_approx(nn1);
     const f32x2 rn2 = pack2(rn0, rn1);
-    const float rn2n = __shfl_down_sync(0xffffffffu, rn0, 1);
+    const float rn2n = shdn<SEG>(rn0, 1);
     R.ER[slot][l + 1] = make_uint2(__float_as_uint(rn0), __float_as_uint(rn1));
     R.OR[slot][l + 1] = make_uint2(__float_as_uint(rn1), __float_as_uint(rn2n));
 #endif
@@ -538,12 +568,12 @@ __global__ void __launch_bounds__(32 * stream::NWARP, NV == 2 ? VF_STREAM_MINB2 
     // rows r - d (d = 2, then 1): the partner pixels' H(+d) from values of row r
     // pixels with offset (-d, dx), partly from the adjacent lanes
     auto partner_rows = [&](const f32x2 (&v)[5], float (&H0)[3], float (&H1)[3]) {
-      const float p_p2_0 = __shfl_up_sync(0xffffffffu, lo2(v[4]), 1);   // lane l-1: q0, offset (-d, +2)
-      const float p_p1_1 = __shfl_up_sync(0xffffffffu, hi2(v[3]), 1);   // lane l-1: q1, offset (-d, +1)
-      const float p_p2_1 = __shfl_up_sync(0xffffffffu, hi2(v[4]), 1);   // lane l-1: q1, offset (-d, +2)
-      const float n_m2_0 = __shfl_down_sync(0xffffffffu, lo2(v[0]), 1); // lane l+1: q0, offset (-d, -2)
-      const float n_m1_0 = __shfl_down_sync(0xffffffffu, lo2(v[1]), 1); // lane l+1: q0, offset (-d, -1)
-      const float n_m2_1 = __shfl_down_sync(0xffffffffu, hi2(v[0]), 1); // lane l+1: q1, offset (-d, -2)
+      const float p_p2_0 = shup<SEG>(lo2(v[4]), 1);   // lane l-1: q0, offset (-d, +2)
+      const float p_p1_1 = shup<SEG>(hi2(v[3]), 1);   // lane l-1: q1, offset (-d, +1)
+      const float p_p2_1 = shup<SEG>(hi2(v[4]), 1);   // lane l-1: q1, offset (-d, +2)
+      const float n_m2_0 = shdn<SEG>(lo2(v[0]), 1); // lane l+1: q0, offset (-d, -2)
+      const float n_m1_0 = shdn<SEG>(lo2(v[1]), 1); // lane l+1: q0, offset (-d, -1)
+      const float n_m2_1 = shdn<SEG>(hi2(v[0]), 1); // lane l+1: q1, offset (-d, -2)
       hrow(p_p2_0, p_p1_1, lo2(v[2]), hi2(v[1]), n_m2_0, H0);          // pixel (r - d, 2l)
       hrow(p_p2_1, lo2(v[3]), hi2(v[2]), n_m1_0, n_m2_1, H1);          // pixel (r - d, 2l + 1)
     };
@@ -583,9 +613,9 @@ __global__ void __launch_bounds__(32 * stream::NWARP, NV == 2 ? VF_STREAM_MINB2 
 #pragma unroll
       for (int t = 0; t < NV; ++t) {
         // right values from (q1, lane l+1)
-        const float n_m1_0 = __shfl_down_sync(0xffffffffu, lo2(v[t][1]), 1);
-        const float n_m2_0 = __shfl_down_sync(0xffffffffu, lo2(v[t][0]), 1);
-        const float n_m2_1 = __shfl_down_sync(0xffffffffu, hi2(v[t][0]), 1);
+        const float n_m1_0 = shdn<SEG>(lo2(v[t][1]), 1);
+        const float n_m2_0 = shdn<SEG>(lo2(v[t][0]), 1);
+        const float n_m2_1 = shdn<SEG>(hi2(v[t][0]), 1);
         float Ha[3], Hb[3];
         hrow0(lo2(v[t][0]), lo2(v[t][1]), hi2(v[t][1]), n_m2_0, Ha);
         hrow0(hi2(v[t][0]), hi2(v[t][1]), n_m1_0, n_m2_1, Hb);
@@ -607,12 +637,12 @@ __global__ void __launch_bounds__(32 * stream::NWARP, NV == 2 ? VF_STREAM_MINB2 
     if (gy >= ty0) {
       // keys: window 2l uses (lane l-1: q1, b = 0), (q0, b = 1), (q1, b = 2);
       // window 2l + 1 uses (q0, b = 0), (q1, b = 1), (lane l+1: q0, b = 2)
-      const float k00 = __shfl_up_sync(0xffffffffu, role_key<0>(hi2(R0[t][0])), 1);
-      const float k10 = __shfl_up_sync(0xffffffffu, role_key<4>(hi2(R1[t][0])), 1);
-      const float k20 = __shfl_up_sync(0xffffffffu, role_key<8>(hi2(R2[t][0])), 1);
-      const float m02 = __shfl_down_sync(0xffffffffu, role_key<2>(lo2(R0[t][2])), 1);
-      const float m12 = __shfl_down_sync(0xffffffffu, role_key<6>(lo2(R1[t][2])), 1);
-      const float m22 = __shfl_down_sync(0xffffffffu, role_key<10>(lo2(R2[t][2])), 1);
+      const float k00 = shup<SEG>(role_key<0>(hi2(R0[t][0])), 1);
+      const float k10 = shup<SEG>(role_key<4>(hi2(R1[t][0])), 1);
+      const float k20 = shup<SEG>(role_key<8>(hi2(R2[t][0])), 1);
+      const float m02 = shdn<SEG>(role_key<2>(lo2(R0[t][2])), 1);
+      const float m12 = shdn<SEG>(role_key<6>(lo2(R1[t][2])), 1);
+      const float m22 = shdn<SEG>(role_key<10>(lo2(R2[t][2])), 1);
       const float kw0 = fmin3(fmin3(k00, role_key<1>(lo2(R0[t][1])), role_key<2>(hi2(R0[t][2]))),
                               fmin3(k10, role_key<5>(lo2(R1[t][1])), role_key<6>(hi2(R1[t][2]))),
                               fmin3(k20, role_key<9>(lo2(R2[t][1])), role_key<10>(hi2(R2[t][2]))));
@@ -648,10 +678,10 @@ __global__ void __launch_bounds__(32 * stream::NWARP, NV == 2 ? VF_STREAM_MINB2 
       }
       if (Lt.idx || Lt.agg) {
         // parity runs only: the index (raster 3a + b) and the exact aggregates
-        const float f00 = __shfl_up_sync(0xffffffffu, hi2(R0[t][0]), 1), f10 = __shfl_up_sync(0xffffffffu, hi2(R1[t][0]), 1),
-                    f20 = __shfl_up_sync(0xffffffffu, hi2(R2[t][0]), 1);
-        const float g02 = __shfl_down_sync(0xffffffffu, lo2(R0[t][2]), 1), g12 = __shfl_down_sync(0xffffffffu, lo2(R1[t][2]), 1),
-                    g22 = __shfl_down_sync(0xffffffffu, lo2(R2[t][2]), 1);
+        const float f00 = shup<SEG>(hi2(R0[t][0]), 1), f10 = shup<SEG>(hi2(R1[t][0]), 1),
+                    f20 = shup<SEG>(hi2(R2[t][0]), 1);
+        const float g02 = shdn<SEG>(lo2(R0[t][2]), 1), g12 = shdn<SEG>(lo2(R1[t][2]), 1),
+                    g22 = shdn<SEG>(lo2(R2[t][2]), 1);
         const long long npix_img = (long long)L.out_rows * W;
         const long long po = (long long)(gy - L.out_row0) * W + xa;
         if (ov0) {
@@ -681,10 +711,11 @@ __global__ void __launch_bounds__(32 * stream::NWARP, NV == 2 ? VF_STREAM_MINB2 
 
 #ifndef VF_ANGULAR_MM_TU
 // defined in vf_stream.cu, whose compile flags (tuning knobs) fix the ring layout
-const void* stream_kernel_fn_mm();
-const void* stream_kernel_fn_ex();
-const void* stream_kernel_fn_both();
-size_t stream_smem_bytes();
+// half = true: the SEG = 16 remainder-strip kernel
+const void* stream_kernel_fn_mm(bool half = false);
+const void* stream_kernel_fn_ex(bool half = false);
+const void* stream_kernel_fn_both(bool half = false);
+size_t stream_smem_bytes(bool half = false);
 #endif
 
 // rows per warp: long tiles (less vertical halo: K + 2 steps for K rows) when
@@ -699,12 +730,16 @@ inline int stream_rows_per_warp(long long strips_total_times_rows) {
 #ifdef VF_ANGULAR_MM_TU
 // launch geometry, defined with the kernel (vf_stream.cu) so the tuning knobs
 // of that translation unit fix it
-inline dim3 stream_grid_impl(const Launch& L, int B, int K) {
+// tail = false: the full strips (all of them, or all but the last when
+// split_tail); tail = true: the half-warp launch of the last strips
+inline dim3 stream_grid_impl(const Launch& L, int B, int K, bool split_tail, bool tail) {
   using namespace stream;
-  return dim3((L.W + SOUT - 1) / SOUT, (L.out_rows + K * NWARP - 1) / (K * NWARP), B);
+  const unsigned gy = (L.out_rows + K * NWARP - 1) / (K * NWARP);
+  if (tail) return dim3(1, gy, (B + 1) / 2);
+  return dim3(strips_of(L.W) - (split_tail ? 1 : 0), gy, B);
 }
 #else
-dim3 stream_grid(const Launch& L, int B, int K);
+dim3 stream_grid(const Launch& L, int B, int K, bool split_tail = false, bool tail = false);
 int stream_block_threads();
 #endif
 

@@ -51,4 +51,28 @@ for var in ("minimax", "exact"):
                                          want_agg=True)
         torch.cuda.synchronize()
         assert torch.equal(ob[i], e_out) and torch.equal(ib[i], e_idx) and torch.equal(ab[i], e_agg), (var, i)
+    # half-warp remainder strips (batches with W - 62 (S - 1) <= 30): the last
+    # strip of images 2z, 2z + 1 on the two halves of one warp, a ghost half for
+    # odd batches; must equal the one-image calls (full-warp strips) bit for bit
+    for (nb, hh, ww) in ((2, 29, 80), (3, 23, 92), (3, 19, 63), (2, 17, 155), (5, 21, 142)):
+        xb = np.stack([vfsynth.random_image(300 + 7 * i + ww, hh, ww) for i in range(nb)])
+        xbt = torch.from_numpy(xb).cuda()
+        ob, ib, ab = vfb.filter(xbt, 3, "angular", var, want_index=True, want_agg=True)
+        pout = torch.empty_like(xbt)
+        plan = vfb.Plan(xbt, [pout], 3, [("angular", var)])
+        half = ww - 62 * ((ww + 61) // 62 - 1) <= 30
+        assert plan.kernels() == (2 if half else 1), (ww, plan.kernels())
+        plan.launch()
+        torch.cuda.synchronize()
+        assert torch.equal(pout, ob), (var, ww)
+        plan.close()
+        for i in range(nb):
+            e_out, e_idx, e_agg = vfb.filter(torch.from_numpy(xb[i]).cuda(), 3, "angular", var, want_index=True,
+                                             want_agg=True)
+            torch.cuda.synchronize()
+            assert torch.equal(ob[i], e_out) and torch.equal(ib[i], e_idx) and torch.equal(ab[i], e_agg), (var, ww, i)
+        _, o_idx, o_agg = oracle.filter_image(xb[nb - 1], 3, "angular", var, want_agg=True)
+        rep = check_parity(xb[nb - 1], 3, ob[nb - 1].cpu().numpy(), ib[nb - 1].cpu().numpy(),
+                           ab[nb - 1].cpu().numpy(), o_idx, o_agg)
+        assert rep["ok"], (var, ww, rep)
 print("stream paths ok")

@@ -449,7 +449,8 @@ def test_c4_full_batch_sampled(crit, var):
 def test_fused_plan_large_batch():
     """A plan of >= 2^21 pixels fuses its exp/log filters into one kernel node
     (shared staging and S1) and its angular exact + minimax into another (one
-    geometry evaluation): 2 kernel nodes for the 7 filters, outputs
+    geometry evaluation; plus the half-warp remainder-strip node): 3 kernel
+    nodes for the 7 filters, outputs
     bit-identical to each filter's own kernel, and to VF_PLAN_FUSE=0 plans
     (the single-filter nodes)."""
     spec = dataclasses.replace(vfsynth.config("C4"), batch=32)
@@ -457,7 +458,7 @@ def test_fused_plan_large_batch():
     combos = CV[:7]
     outs = [torch.empty_like(xb) for _ in combos]
     plan = vfb.Plan(xb, outs, 3, combos)
-    assert plan.kernels() == 2                                   # exp/log node + angular node
+    assert plan.kernels() == 3                  # exp/log node + angular node + its remainder strips (768 = 12 x 62 + 24)
     plan.launch()
     torch.cuda.synchronize()
     for (crit, var), o in zip(combos, outs):
@@ -467,7 +468,7 @@ def test_fused_plan_large_batch():
     small = vfb.Plan(xb[:1].contiguous(), [torch.empty_like(xb[:1]) for _ in combos], 3, combos)
     assert small.kernels() == 7
     mid = vfb.Plan(xb[:6].contiguous(), [torch.empty_like(xb[:6]) for _ in combos], 3, combos)
-    assert mid.kernels() == 3                                    # exp/log fused, angular not streamed
+    assert mid.kernels() == 4       # exp/log fused; angular exact block kernel, minimax streamed (+ remainder strips)
 
 
 
