@@ -445,6 +445,39 @@ def test_c4_full_batch_sampled(crit, var):
                        nsample=5000, seed=b)
 
 
+def test_c4_bench_plan_sampled():
+    """The bench's timed launch configuration: the 7-filter plan over the full
+    1024 x 512 x 768 batch (3 kernel nodes: pair-major exp/log, fused angular,
+    angular remainder strips).  For 3 images (first, middle, last) every
+    filter's plan output equals the one-image call bit for bit, and that
+    call's sampled pixels pass the oracle parity check."""
+    import bench
+    spec = vfsynth.config("C4")
+    ids = [0, 511, 1023]
+    xb = vfsynth.make_batch(spec, ids=ids)
+    full = torch.empty((1024, 512, 768, 3), dtype=torch.uint8, device="cuda")
+    full.random_(0, 256, generator=torch.Generator(device="cuda").manual_seed(2))
+    for j, b in enumerate(ids):
+        full[b] = torch.from_numpy(xb[j]).cuda()
+    outs = [torch.empty_like(full) for _ in bench.COMBOS]
+    plan = vfb.Plan(full, outs, 3, bench.COMBOS)
+    assert plan.kernels() == 3
+    plan.launch()
+    torch.cuda.synchronize()
+    for (crit, var), o in zip(bench.COMBOS, outs):
+        algo = "stream" if crit == "angular" else "auto"
+        for j, b in enumerate(ids):
+            o2, i2, a2 = vfb.filter(full[b:b + 1].contiguous(), 3, crit, var, algo=algo, want_index=True,
+                                    want_agg=True)
+            torch.cuda.synchronize()
+            assert torch.equal(o2[0], o[b]), (crit, var, b)
+            sampled_parity(xb[j], 3, crit, var, o2[0].cpu().numpy(), i2[0].cpu().numpy(), a2[0].cpu().numpy(),
+                           nsample=1500, seed=100 + b)
+    plan.close()
+    del outs, full
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------------------------- plan (CUDA-graph executor)
 def test_fused_plan_large_batch():
     """A plan of >= 2^21 pixels fuses its exp/log filters into one kernel node
