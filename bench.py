@@ -58,11 +58,15 @@ COMBOS = [("angular", "exact"), ("angular", "minimax"), ("exp", "exact"), ("exp"
 REACH_COMBOS = [("exp", "reach"), ("log", "reach")]
 REFERENCE = ("angular", "exact")
 # the step's statistics: every paper approximant against the exact filter of
-# its criterion (the paper's fidelity measure) -- one fused pass per
-# exact reference (vf_image_stats_multi)
+# its criterion (the paper's fidelity measure), computed by the plan
+# (vf_plan_create_ex: one statistics node per exact reference in its graph)
 FIDELITY_GROUPS = [(("angular", "exact"), [("angular", "minimax")]),
                    (("exp", "exact"), [("exp", "minimax"), ("exp", "poly4")]),
                    (("log", "exact"), [("log", "minimax")])]
+# refs[i]: the index in COMBOS of filter i's reference (-1: none); the plan
+# numbers its comparisons in increasing i, which is FIDELITY_GROUPS' order
+FIDELITY_REFS = [next((COMBOS.index(r) for r, cs in FIDELITY_GROUPS if c in cs), -1) for c in COMBOS]
+assert [COMBOS[i] for i, r in enumerate(FIDELITY_REFS) if r >= 0] == [c for _, cs in FIDELITY_GROUPS for c in cs]
 
 # algorithmic FP32 flops per pair (FMA = 2, add/sub/mul = 1;
 # abs/neg/compare/select = 0; robustness overhead not counted).  Exact
@@ -482,31 +486,32 @@ def run_ours(args):
     w = 3
     x = torch.from_numpy(x_np).to(dev)
     outs = [torch.empty_like(x) for _ in COMBOS]
-    plan = vfb.Plan(x, outs, w, COMBOS) if Bl else None
-    plan_nodes = plan.kernels() if plan is not None else 0
-    oc = {c: outs[i] for i, c in enumerate(COMBOS)}
+    with_stats = args.workload == "c4"     # C2: the 7 filters of one image per rank, no collective (round 1's step)
     n_cmp = sum(len(cs) for _, cs in FIDELITY_GROUPS)
     stats_buf = torch.empty((n_cmp, max(Bl, 1), 8), dtype=torch.float64, device=dev)
+    # the step's plan: the 7 filters and (C4) the fidelity statistics of each
+    # approximant against its exact filter, as one graph
+    plan = (vfb.Plan(x, outs, w, COMBOS, refs=FIDELITY_REFS, stats=stats_buf) if with_stats
+            else vfb.Plan(x, outs, w, COMBOS)) if Bl else None
+    plan_nodes = plan.kernels() if plan is not None else 0
+    oc = {c: outs[i] for i, c in enumerate(COMBOS)}
     gviews, k0 = [], 0
     for ref, cs in FIDELITY_GROUPS:
         gviews.append((oc[ref], [oc[c] for c in cs], stats_buf[k0:k0 + len(cs)]))
         k0 += len(cs)
 
-    def stats_pass():
+    def stats_pass():          # the separate statistics passes the plan replaces (reported, not in the step)
         for ref_t, outs_t, sv in gviews:
             vfb.vf_image_stats_multi(ref_t, outs_t, sv, stream)
     counts = [par.shard_range(B_total, world, r)[1] - par.shard_range(B_total, world, r)[0]
               for r in range(world)] if args.workload == "c4" else [1] * world
-
-    with_stats = args.workload == "c4"     # C2: the 7 filters of one image per rank, no collective (round 1's step)
 
     def step():
         if not with_stats:
             plan.launch(stream)
             return None
         if Bl:
-            plan.launch(stream)
-            stats_pass()
+            plan.launch(stream)              # filters + statistics (one graph)
             s = stats_buf
         else:
             s = torch.zeros((n_cmp, 0, 8), dtype=torch.float64, device=dev)
@@ -555,9 +560,17 @@ def run_ours(args):
                                lambda c=c: vfb.vf_filter_batch(x, w, *c, out=kouts[c], stream=stream), reps,
                                flush if args.workload == "c2" else None)
             kern[f"{c[0]}/{c[1]}"] = kernel_entry(vfb, c, w, Bl, H, W, ms, peaks, ncu, npix_l)
-        t_stats = kernel_avg_ms(torch, dev, stream, stats_pass, reps)
+        t_stats = kernel_avg_ms(torch, dev, stream, stats_pass, reps) if with_stats else None
+        # the statistics' cost inside the plan: the same plan without them
+        if with_stats:
+            plain = vfb.Plan(x, outs, w, COMBOS)
+            t_plain = kernel_avg_ms(torch, dev, stream, lambda: plain.launch(stream), reps)
+            t_planst = kernel_avg_ms(torch, dev, stream, lambda: plan.launch(stream), reps)
+            plain.close()
+        else:
+            t_plain = t_planst = None
     else:
-        t_stats = None
+        t_stats = t_plain = t_planst = None
     clk.stop()
     reach = {k: kern.pop(k) for k in [f"{c[0]}/{c[1]}" for c in REACH_COMBOS] if k in kern}
     roofline = roofline_mm = None
@@ -668,19 +681,25 @@ def run_ours(args):
             "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": cfg,
             "roofline": roofline, "roofline_minimax": roofline_mm, "per_kernel": kern, "per_node": nodes,
-            "step_breakdown": {"stats_multi_ms": t_stats, "sum_kernel_ms": sum(v["ms"] for v in kern.values()),
-                               "step_ms": ms_per_step,
-                               "note": "the plan's 7 kernels run concurrently; sum_kernel_ms is their serial sum"},
+            "step_breakdown": {"plan_with_stats_ms": t_planst, "plan_without_stats_ms": t_plain,
+                               "separate_stats_passes_ms": t_stats,
+                               "sum_kernel_ms": sum(v["ms"] for v in kern.values()), "step_ms": ms_per_step,
+                               "note": "the plan's kernel nodes run concurrently (sum_kernel_ms: the 7 single-filter "
+                                       "kernels' serial sum); its fidelity statistics nodes (plan_with_stats_ms - "
+                                       "plan_without_stats_ms) overlap the other filters' nodes; "
+                                       "separate_stats_passes_ms: the same 3 statistics passes launched after the "
+                                       "plan (the earlier round-2 step)"},
             "f4_reach": {"per_kernel": reach,
                          "speedup_vs_paper_minimax": {k: kern[k.replace("reach", "minimax")]["ms"] / v["ms"]
                                                       for k, v in reach.items()}},
             "c3": c3, "cpu_baseline": cpu, "e2e": e2e,
             "fidelity_minimax_vs_exact": fid,
             "paper_filters": paper,
-            "gpu_launches": (plan_nodes + (2 * len(FIDELITY_GROUPS) if with_stats else 0)) * args.steps if Bl else 0,
+            "gpu_launches": plan_nodes * args.steps if Bl else 0,
             "gpu_launches_note": (f"per step: the plan graph's {plan_nodes} kernel nodes (exp/log filters fused into one "
                                   "node for large plans; angular exact + minimax into one, plus its half-warp "
-                                  "remainder-strip node) + 3 x (vf_stats_multi_kernel + vf_stats_finalize)")
+                                  "remainder-strip node; one vf_stats_multi_kernel node per exact reference; "
+                                  "vf_stats_finalize)")
                                  if with_stats else f"per step: the plan graph's {plan_nodes} kernel nodes",
             "clocks": clocks, "wall_s_timed_region": t_wall1 - t_wall0, "peaks": peaks,
             "libvf_sha256": sha, "ncu_exec": ncu_note,
@@ -717,20 +736,22 @@ def run_e2e(args, torch, dist, vfb, dev, stream, x_np, x, outs, w, B_total, H, W
         d_in = torch.empty_like(h_in, device=dev)
         d_outs = [torch.empty_like(d_in) for _ in COMBOS]
         st = torch.cuda.Stream(dev)
-        slots.append((vfb.Plan(d_in, d_outs, w, COMBOS, h_in=h_in, h_outs=h_outs), h_outs, st, d_in, d_outs))
-    for pl, _, st, _, _ in slots:
+        sbuf = torch.empty((len([r for r in FIDELITY_REFS if r >= 0]), nb, 8), dtype=torch.float64, device=dev)
+        slots.append((vfb.Plan(d_in, d_outs, w, COMBOS, h_in=h_in, h_outs=h_outs, refs=FIDELITY_REFS, stats=sbuf),
+                       h_outs, st, d_in, d_outs, sbuf))
+    for pl, _, st, *_ in slots:
         pl.launch(st)
     torch.cuda.synchronize(dev)
     steps = max(ns, args.e2e_steps)
     a, b = ev_pair(torch)
     dist.barrier()
     a.record(stream)
-    for _, _, st, _, _ in slots:
+    for _, _, st, *_ in slots:
         st.wait_event(a)
     for k in range(steps):
-        pl, _, st, _, _ = slots[k % ns]
+        pl, _, st, *_ = slots[k % ns]
         pl.launch(st)
-    for _, _, st, _, _ in slots:
+    for _, _, st, *_ in slots:
         e = torch.cuda.Event()
         e.record(st)
         stream.wait_event(e)
@@ -749,8 +770,9 @@ def run_e2e(args, torch, dist, vfb, dev, stream, x_np, x, outs, w, B_total, H, W
     return {"value": units / (ms / 1e3) / 1e6, "unit": "Mpix/s", "h2d_bytes_per_step": nb * H * W * 3,
             "d2h_bytes_per_step": len(COMBOS) * nb * H * W * 3, "ms_per_step": ms, "images_per_rank": nb,
             "outputs_match_device_path": same, "steps": steps, "pipeline_slots": ns,
-            "api": f"vf_plan_create(h_in, h_outs) + vf_plan_launch: graph H2D -> {nodes} kernel nodes (7 filters) -> "
-                   "7 D2H (pinned host); steps round-robin over the slots' streams",
+            "api": f"vf_plan_create_ex(h_in, h_outs, refs, stats) + vf_plan_launch: graph H2D -> {nodes} kernel nodes "
+                   "(7 filters + fidelity statistics) -> 7 D2H (pinned host); steps round-robin over the slots' "
+                   "streams",
             "note": None if nb == Bl else f"host memory bounds the pinned buffers to {nb} of {Bl} images per rank"}
 
 

@@ -175,6 +175,26 @@ typedef struct vf_plan_s *vf_plan;
 VF_API int vf_plan_create(vf_plan *plan, int B, int H, int W, int window, int n, const int *criteria,
                           const int *variants, const uint8_t *d_in, uint8_t *const *d_outs,
                           const uint8_t *h_in, uint8_t *const *h_outs);
+/* As vf_plan_create, plus the paper's fidelity measures of approximate vs exact
+ * filters (the bench's per-step statistics) computed by the plan:
+ * refs (host int[n], nullable): refs[i] = j compares filter i's output with
+ * filter j's (its reference, j != i), -1 = no comparison.  The comparisons
+ * are numbered k = 0, 1, ... in increasing i; d_stats (device double
+ * [ncmp][B][8], non-NULL when any refs[i] >= 0, not overlapping the images)
+ * receives, at every launch, row [k][b] exactly as vf_image_stats_multi(
+ * d_outs[refs[i]], {d_outs[i]}) would write it for image b -- bit-identical:
+ * both sum the same per-pixel fixed-point values.  The graph zeroes d_stats,
+ * runs one statistics node per reference (its comparisons, <= 8 per node: the
+ * reference is read and its CIELAB evaluated once) after the kernel nodes
+ * writing its inputs -- so it overlaps the other filters' nodes -- and a
+ * finalize node.  (Measured: computing the comparisons inside the fused
+ * filter kernels' epilogues is slower -- the exp/log node is issue-bound --
+ * DESIGN.md 5.3.5.)
+ * Errors: VF_EINVAL as vf_plan_create, for refs[i] outside [-1, n) or == i,
+ * or a NULL / overlapping d_stats.  (ABI 105.) */
+VF_API int vf_plan_create_ex(vf_plan *plan, int B, int H, int W, int window, int n, const int *criteria,
+                             const int *variants, const uint8_t *d_in, uint8_t *const *d_outs,
+                             const uint8_t *h_in, uint8_t *const *h_outs, const int *refs, double *d_stats);
 VF_API int vf_plan_launch(vf_plan plan, void *stream);
 /* Number of kernel nodes of a plan (>= 1; VF_EINVAL for an invalid plan).  Plans
  * of at least 2^21 pixels fuse their exp/log filters into one node (they share
@@ -182,7 +202,9 @@ VF_API int vf_plan_launch(vf_plan plan, void *stream);
  * minimax filters into one node (one pair-geometry evaluation for both
  * variants); outputs are bit-identical to the single-filter kernels; the
  * environment variable VF_PLAN_FUSE=0 disables fusion.  A large plan of the 7
- * paper filters has 2 kernel nodes. */
+ * paper filters has 3 kernel nodes (the angular node's remainder strips are a
+ * second node); with statistics (vf_plan_create_ex) the count includes the
+ * statistics nodes and the finalize node (the paper grouping: 3 + 3 + 1). */
 VF_API int vf_plan_kernels(vf_plan plan);
 VF_API int vf_plan_destroy(vf_plan plan);
 
@@ -191,7 +213,7 @@ VF_API int vf_plan_destroy(vf_plan plan);
  *   {pixels with a != b, sum |a-b| (all channels), sum (a-b)^2,
  *    sum |a_Lab - b_Lab|_2, sum |a_Lab|_2, max |a-b|, 0, 0}
  * (MAE/MSE/NCD of P:286-293; CIELAB via sRGB/D65, evaluated in fp32 per
- * pixel and summed in double).  Overwrites stats. */
+ * pixel and summed exactly in 2^-23 fixed point).  Overwrites stats. */
 VF_API int vf_image_stats(const uint8_t *a, const uint8_t *b, int B, int H, int W, double *stats,
                    void *stream);
 /* As vf_image_stats; flags = VF_STATS_NO_REF_NORM (1) skips the reference
@@ -209,10 +231,10 @@ VF_API int vf_image_stats_ex(const uint8_t *a, const uint8_t *b, int B, int H, i
  * and written into every row unless flags = VF_STATS_NO_REF_NORM).  Each
  * reference pixel is read once and its CIELAB evaluated at most once, so
  * comparing the 7 filters of a step against one reference costs one pass
- * instead of 7.  Deterministic: the floating-point sums are accumulated across
- * blocks in 2^-24 fixed point (integer atomics), so results are bit-identical
- * run to run (as are those of vf_image_stats / _ex, which call this with
- * nb = 1).  Errors: VF_EINVAL for NULL pointers, nb outside [1, 8], bad sizes
+ * instead of 7.  Deterministic: every pixel's fp32 CIELAB norm / distance is
+ * rounded to 2^-23 fixed point and the sums are integers (64-bit atomics), so
+ * results are bit-identical run to run and across kernels (vf_image_stats /
+ * _ex call this with nb = 1; plans with statistics produce the same bits).  Errors: VF_EINVAL for NULL pointers, nb outside [1, 8], bad sizes
  * or unknown flags. */
 VF_API int vf_image_stats_multi(const uint8_t *a, const uint8_t *const *bs, int nb, int B, int H, int W,
                                 double *stats, int flags, void *stream);
@@ -220,8 +242,9 @@ VF_API int vf_image_stats_multi(const uint8_t *a, const uint8_t *const *bs, int 
 VF_API const char *vf_status_string(int status);
 /* Text of the last error on the calling thread ("" if none). */
 VF_API const char *vf_last_error(void);
-/* ABI version (major*100 + minor): 104 (102: vf_image_stats_ex; 103: vf_image_stats_multi,
- * deterministic statistics, vf_kernel_info; 104: vf_plan_kernels, fused exp/log plan nodes). */
+/* ABI version (major*100 + minor): 105 (102: vf_image_stats_ex; 103: vf_image_stats_multi,
+ * deterministic statistics, vf_kernel_info; 104: vf_plan_kernels, fused exp/log plan nodes;
+ * 105: vf_plan_create_ex (plan statistics), per-pixel fixed-point statistics sums). */
 VF_API int vf_version(void);
 
 #ifdef __cplusplus

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <mutex>
 #include <cstdio>
@@ -384,23 +385,115 @@ int launch_desc(KernelDesc& kd, cudaStream_t st) {
 }
 
 // The kernel node(s) of a description (the remainder-strip launch as a second,
-// independent node), each depending on dep (nullable); returns the count.
-int add_kernel_nodes(cudaGraph_t g, KernelDesc& kd, cudaGraphNode_t dep, cudaGraphNode_t* nodes, const char* what) {
+// independent node), each depending on deps[0..ndeps); returns the count.
+int add_kernel_nodes(cudaGraph_t g, KernelDesc& kd, const cudaGraphNode_t* deps, int ndeps, cudaGraphNode_t* nodes,
+                     const char* what) {
   cudaKernelNodeParams kp = {};
   kp.func = (void*)kd.fn;
   kp.gridDim = kd.grid;
   kp.blockDim = kd.block;
   kp.sharedMemBytes = (unsigned)kd.smem;
   kp.kernelParams = kd.params();
-  cudaError_t e = cudaGraphAddKernelNode(&nodes[0], g, dep ? &dep : nullptr, dep ? 1 : 0, &kp);
+  cudaError_t e = cudaGraphAddKernelNode(&nodes[0], g, deps, ndeps, &kp);
   if (e != cudaSuccess) return -cuda_fail(e, what);
   if (!kd.fn_tail) return 1;
   kp.func = (void*)kd.fn_tail;
   kp.gridDim = kd.grid_tail;
   kp.sharedMemBytes = (unsigned)kd.smem_tail;
-  e = cudaGraphAddKernelNode(&nodes[1], g, dep ? &dep : nullptr, dep ? 1 : 0, &kp);
+  e = cudaGraphAddKernelNode(&nodes[1], g, deps, ndeps, &kp);
   if (e != cudaSuccess) return -cuda_fail(e, what);
   return 2;
+}
+
+// The sRGB decoding table (IEC 61966-2-1: c/255 linearised), computed in
+// double on the host and rounded to float once, in device memory of every
+// device that runs statistics (allocated on first use, kept for the
+// process).  Every statistics pass (standalone or a plan's node) reads the same
+// table, so their per-pixel CIELAB values are the same bits.
+const float* srgb_table(int* rc) {
+  static std::mutex mu;
+  static float* tabs[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev < 0 || dev >= 64) { *rc = cuda_fail(e == cudaSuccess ? cudaErrorInvalidDevice : e, "cudaGetDevice"); return nullptr; }
+  std::lock_guard<std::mutex> lk(mu);
+  if (!tabs[dev]) {
+    float h[256];
+    for (int c = 0; c < 256; ++c) {
+      const double v = c / 255.0;
+      h[c] = (float)(v <= 0.04045 ? v / 12.92 : std::pow((v + 0.055) / 1.055, 2.4));
+    }
+    float* d = nullptr;
+    e = cudaMalloc(&d, sizeof(h));
+    if (e == cudaSuccess) e = cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { if (d) cudaFree(d); *rc = cuda_fail(e, "sRGB table"); return nullptr; }
+    tabs[dev] = d;
+  }
+  *rc = VF_OK;
+  return tabs[dev];
+}
+
+// The statistics pass (vf_stats_multi_kernel) for a reference a and nb <= 8
+// outputs: kernel, grid and the PX = 4 decision, shared by
+// vf_image_stats_multi and the plans' statistics nodes.
+template <int PX>
+const void* stats_fn(int nb) {
+  switch (nb) {
+    case 1: return (const void*)vf::vf_stats_multi_kernel<1, PX>;
+    case 2: return (const void*)vf::vf_stats_multi_kernel<2, PX>;
+    case 3: return (const void*)vf::vf_stats_multi_kernel<3, PX>;
+    case 4: return (const void*)vf::vf_stats_multi_kernel<4, PX>;
+    case 5: return (const void*)vf::vf_stats_multi_kernel<5, PX>;
+    case 6: return (const void*)vf::vf_stats_multi_kernel<6, PX>;
+    case 7: return (const void*)vf::vf_stats_multi_kernel<7, PX>;
+    default: return (const void*)vf::vf_stats_multi_kernel<8, PX>;
+  }
+}
+struct StatsLaunch {
+  const void* fn;
+  dim3 grid;
+  // kernel arguments (a, args, npix, B, acc, want_ref_norm)
+  const uint8_t* a;
+  vf::StatsArgs args;
+  long long npix;
+  int B;
+  unsigned long long* acc;
+  int ref;
+  void* params[6];
+  void** kparams() {
+    params[0] = &a; params[1] = &args; params[2] = &npix; params[3] = &B; params[4] = &acc; params[5] = &ref;
+    return params;
+  }
+};
+int stats_launch(StatsLaunch* sl, const uint8_t* a, const uint8_t* const* bs, const int* rows, int nb, int B,
+                 long long npix, unsigned long long* acc, int want_ref_norm) {
+  // four pixels (three aligned words) per iteration when the images allow it
+  bool px4 = npix % 4 == 0 && ((uintptr_t)a % 4) == 0;
+  for (int k = 0; k < nb; ++k) px4 = px4 && ((uintptr_t)bs[k] % 4) == 0;
+  const long long units = px4 ? npix / 4 : npix;
+  // ~8 blocks per SM over the batch, and at most 4096 pixels per thread (the
+  // per-thread integer sums are 32-bit)
+  long long blocks = (units + 255) / 256;
+  long long per_image = (148 * 8 + B - 1) / B;
+  const long long min_blocks = (npix + 256LL * 4096 - 1) / (256LL * 4096);
+  if (per_image < min_blocks) per_image = min_blocks;
+  if (blocks > per_image) blocks = per_image;
+  if (blocks > 2147483647LL) return fail(VF_EINVAL, "image too large (%lld pixels)", npix);
+  if (B > 65535) return fail(VF_EINVAL, "too many images for the statistics grid (%lld)", B);
+  int trc = VF_OK;
+  const float* tab = srgb_table(&trc);
+  if (!tab) return trc;
+  sl->fn = px4 ? stats_fn<4>(nb) : stats_fn<1>(nb);
+  sl->grid = dim3((unsigned)blocks, B);
+  sl->a = a;
+  sl->args = vf::StatsArgs{};
+  for (int k = 0; k < nb; ++k) { sl->args.b[k] = bs[k]; sl->args.row[k] = rows[k]; }
+  sl->args.lin = tab;
+  sl->npix = npix;
+  sl->B = B;
+  sl->acc = acc;
+  sl->ref = want_ref_norm;
+  return VF_OK;
 }
 
 int launch(const uint8_t* in, long long in_stride, int band_row0, int band_rows, int B, int H, int W, int out_row0,
@@ -528,6 +621,13 @@ int vf_kernel_info(int B, int H, int W, int window, int criterion, int variant, 
 
 int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const int* criteria, const int* variants,
                    const uint8_t* d_in, uint8_t* const* d_outs, const uint8_t* h_in, uint8_t* const* h_outs) {
+  return vf_plan_create_ex(plan, B, H, W, window, n, criteria, variants, d_in, d_outs, h_in, h_outs, nullptr,
+                           nullptr);
+}
+
+int vf_plan_create_ex(vf_plan* plan, int B, int H, int W, int window, int n, const int* criteria, const int* variants,
+                      const uint8_t* d_in, uint8_t* const* d_outs, const uint8_t* h_in, uint8_t* const* h_outs,
+                      const int* refs, double* d_stats) {
   g_err[0] = 0;
   if (!plan) return fail(VF_EINVAL, "NULL plan pointer");
   *plan = nullptr;
@@ -543,16 +643,60 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
       if (overlap(d_outs[j], bytes, d_outs[i], bytes)) return fail(VF_EINVAL, "outputs %lld overlap", i);
     if (h_outs && !h_outs[i]) return fail(VF_EINVAL, "NULL host output %lld", i);
   }
+  // fidelity comparisons: filter i against filter refs[i] (row cmp_of[i] of d_stats)
+  int cmp_of[64], ncmp = 0;
+  for (int i = 0; i < n; ++i) {
+    cmp_of[i] = -1;
+    if (!refs || refs[i] == -1) continue;
+    if (refs[i] < 0 || refs[i] >= n || refs[i] == i)
+      return fail(VF_EINVAL, "refs[%lld] must be -1 or another filter's index", i);
+    cmp_of[i] = ncmp++;
+  }
+  if (ncmp > 0 && !d_stats) return fail(VF_EINVAL, "NULL statistics buffer");
+  if (ncmp > 0 && B > 65535) return fail(VF_EINVAL, "too many images for the statistics grid (%lld)", B);
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(d_stats);
+  const size_t nstat = (size_t)8 * B * ncmp;
+  if (ncmp > 0 && overlap((const uint8_t*)d_stats, nstat * 8, d_in, bytes))
+    return fail(VF_EINVAL, "statistics buffer overlaps the input");
+  for (int i = 0; i < n && ncmp > 0; ++i)
+    if (overlap((const uint8_t*)d_stats, nstat * 8, d_outs[i], bytes))
+      return fail(VF_EINVAL, "statistics buffer overlaps output %lld", i);
+
   vf_plan_s* p = new (std::nothrow) vf_plan_s();
   if (!p) return fail(VF_ECUDA, "out of host memory");
   cudaError_t e = cudaGraphCreate(&p->graph, 0);
   if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaGraphCreate"); }
   auto bail = [&](int rc) { cudaGraphDestroy(p->graph); delete p; return rc; };
-  cudaGraphNode_t h2d = nullptr;
+  // roots: the H2D copy of the input and the zeroing of the statistics accumulators
+  cudaGraphNode_t roots[2];
+  int nroots = 0;
   if (h_in) {
-    e = cudaGraphAddMemcpyNode1D(&h2d, p->graph, nullptr, 0, (void*)d_in, h_in, bytes, cudaMemcpyHostToDevice);
+    e = cudaGraphAddMemcpyNode1D(&roots[nroots], p->graph, nullptr, 0, (void*)d_in, h_in, bytes,
+                                 cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (H2D)"));
+    ++nroots;
   }
+  if (ncmp > 0) {
+    cudaMemsetParams mp = {};
+    mp.dst = d_stats;
+    mp.value = 0;
+    mp.elementSize = 4;
+    mp.width = nstat * 2;
+    mp.height = 1;
+    mp.pitch = nstat * 8;
+    e = cudaGraphAddMemsetNode(&roots[nroots], p->graph, nullptr, 0, &mp);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemsetNode (statistics)"));
+    ++nroots;
+  }
+  std::vector<cudaGraphNode_t> prod[64];   // the kernel node(s) writing filter i
+  std::vector<cudaGraphNode_t> stat_nodes; // nodes adding to the statistics accumulators
+  auto add_d2h = [&](const cudaGraphNode_t* kn, int nk, int i) -> int {
+    if (!h_outs) return VF_OK;
+    cudaGraphNode_t d2h;
+    cudaError_t e2 = cudaGraphAddMemcpyNode1D(&d2h, p->graph, kn, nk, h_outs[i], d_outs[i], bytes,
+                                              cudaMemcpyDeviceToHost);
+    return e2 == cudaSuccess ? VF_OK : cuda_fail(e2, "cudaGraphAddMemcpyNode1D (D2H)");
+  };
   const long long stride = (long long)H * W * 3;
   // Plan-level fusion: the exp/log filters share d1 and S1 (readings R2/R3),
   // so two or more of them become ONE kernel node that stages each tile and
@@ -612,16 +756,13 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
       kp.kernelParams = args;
       if (kp.gridDim.y > 65535 || kp.gridDim.z > 65535) return bail(fail(VF_EINVAL, "grid too large"));
       cudaGraphNode_t kn;
-      e = cudaGraphAddKernelNode(&kn, p->graph, h2d ? &h2d : nullptr, h2d ? 1 : 0, &kp);
+      e = cudaGraphAddKernelNode(&kn, p->graph, roots, nroots, &kp);
       if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddKernelNode (fused)"));
       ++p->nkernels;
-      if (h_outs) {
-        for (int k = 0; k < m; ++k) {
-          cudaGraphNode_t d2h;
-          e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, &kn, 1, h_outs[idx[k]], d_outs[idx[k]], bytes,
-                                       cudaMemcpyDeviceToHost);
-          if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (D2H)"));
-        }
+      for (int k = 0; k < m; ++k) {
+        prod[idx[k]].push_back(kn);
+        int rc = add_d2h(&kn, 1, idx[k]);
+        if (rc) return bail(rc);
       }
     }
   }
@@ -647,19 +788,16 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
         km.fn = vf::stream_kernel_fn_both();
         if (km.fn_tail) km.fn_tail = vf::stream_kernel_fn_both(true);
         km.L2 = ke.L;
+        const int slot[2] = {im, ie};
         cudaGraphNode_t kn[2];
-        const int nk = add_kernel_nodes(p->graph, km, h2d, kn, "cudaGraphAddKernelNode (fused angular)");
+        const int nk = add_kernel_nodes(p->graph, km, roots, nroots, kn, "cudaGraphAddKernelNode (fused angular)");
         if (nk < 0) return bail(-nk);
         p->nkernels += nk;
         fused[im] = fused[ie] = true;
-        if (h_outs) {
-          const int ids[2] = {im, ie};
-          for (int k = 0; k < 2; ++k) {
-            cudaGraphNode_t d2h;
-            e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, kn, nk, h_outs[ids[k]], d_outs[ids[k]], bytes,
-                                         cudaMemcpyDeviceToHost);
-            if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (D2H)"));
-          }
+        for (int k = 0; k < 2; ++k) {
+          prod[slot[k]].assign(kn, kn + nk);
+          rc = add_d2h(kn, nk, slot[k]);
+          if (rc) return bail(rc);
         }
       }
     }
@@ -671,14 +809,63 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
                       d_outs[i], stride, nullptr, nullptr);
     if (rc) return bail(rc);
     cudaGraphNode_t kn[2];
-    const int nk = add_kernel_nodes(p->graph, kd, h2d, kn, "cudaGraphAddKernelNode");
+    const int nk = add_kernel_nodes(p->graph, kd, roots, nroots, kn, "cudaGraphAddKernelNode");
     if (nk < 0) return bail(-nk);
     p->nkernels += nk;
-    if (h_outs) {
-      cudaGraphNode_t d2h;
-      e = cudaGraphAddMemcpyNode1D(&d2h, p->graph, kn, nk, h_outs[i], d_outs[i], bytes, cudaMemcpyDeviceToHost);
-      if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddMemcpyNode1D (D2H)"));
+    prod[i].assign(kn, kn + nk);
+    rc = add_d2h(kn, nk, i);
+    if (rc) return bail(rc);
+  }
+  // the fidelity comparisons: one statistics pass per reference (<= 8 outputs
+  // each: the reference is read and its CIELAB evaluated once), a graph node
+  // after the nodes writing its inputs (so it can overlap other filters'
+  // nodes)
+  for (int r = 0; r < n && ncmp > 0; ++r) {
+    int outs_i[64], no = 0;
+    for (int i = 0; i < n; ++i)
+      if (cmp_of[i] >= 0 && refs[i] == r) outs_i[no++] = i;
+    for (int c0 = 0; c0 < no; c0 += 8) {
+      const int nb = no - c0 < 8 ? no - c0 : 8;
+      const uint8_t* bs[8];
+      int rows[8];
+      std::vector<cudaGraphNode_t> deps(prod[r]);
+      for (int k = 0; k < nb; ++k) {
+        bs[k] = d_outs[outs_i[c0 + k]];
+        rows[k] = cmp_of[outs_i[c0 + k]];
+        deps.insert(deps.end(), prod[outs_i[c0 + k]].begin(), prod[outs_i[c0 + k]].end());
+      }
+      deps.insert(deps.end(), roots, roots + nroots);
+      std::sort(deps.begin(), deps.end());
+      deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+      StatsLaunch sl;
+      int rc = stats_launch(&sl, d_outs[r], bs, rows, nb, B, (long long)H * W, acc, 1);
+      if (rc) return bail(rc);
+      cudaKernelNodeParams kp = {};
+      kp.func = (void*)sl.fn;
+      kp.gridDim = sl.grid;
+      kp.blockDim = dim3(256);
+      kp.sharedMemBytes = 0;
+      kp.kernelParams = sl.kparams();
+      cudaGraphNode_t sn;
+      e = cudaGraphAddKernelNode(&sn, p->graph, deps.data(), deps.size(), &kp);
+      if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddKernelNode (statistics)"));
+      stat_nodes.push_back(sn);
+      ++p->nkernels;
     }
+  }
+  if (ncmp > 0) {                                   // fixed point -> double, in place
+    unsigned long long* accp = acc;
+    long long nst = (long long)nstat;
+    void* fargs[2] = {&accp, &nst};
+    cudaKernelNodeParams kp = {};
+    kp.func = (void*)vf::vf_stats_finalize;
+    kp.gridDim = dim3((unsigned)((nstat + 255) / 256));
+    kp.blockDim = dim3(256);
+    kp.kernelParams = fargs;
+    cudaGraphNode_t fn;
+    e = cudaGraphAddKernelNode(&fn, p->graph, stat_nodes.data(), stat_nodes.size(), &kp);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphAddKernelNode (statistics finalize)"));
+    ++p->nkernels;
   }
   e = cudaGraphInstantiate(&p->exec, p->graph, 0);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphInstantiate"));
@@ -732,38 +919,12 @@ int vf_image_stats_multi(const uint8_t* a, const uint8_t* const* bs, int nb, int
   cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(double) * nstat, st);
   if (e != cudaSuccess) return cuda_fail(e, "stats memset");
   const long long npix = (long long)H * W;
-  // four pixels (three aligned words) per iteration when the images allow it
-  bool px4 = npix % 4 == 0 && ((uintptr_t)a % 4) == 0;
-  for (int k = 0; k < nb; ++k) px4 = px4 && ((uintptr_t)bs[k] % 4) == 0;
-  const long long units = px4 ? npix / 4 : npix;
-  // ~8 blocks per SM over the batch, and at most 4096 pixels per thread (the
-  // per-thread integer sums are 32-bit)
-  long long blocks = (units + 255) / 256;
-  long long per_image = (148 * 8 + B - 1) / B;
-  const long long min_blocks = (npix + 256LL * 4096 - 1) / (256LL * 4096);
-  if (per_image < min_blocks) per_image = min_blocks;
-  if (blocks > per_image) blocks = per_image;
-  if (blocks > 2147483647LL) return fail(VF_EINVAL, "image too large (%lld pixels)", npix);
-  vf::StatsArgs args = {};
-  for (int k = 0; k < nb; ++k) args.b[k] = bs[k];
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(stats);
-  const int ref = (flags & VF_STATS_NO_REF_NORM) ? 0 : 1;
-  const dim3 grid((unsigned)blocks, B);
-#define VF_STATS_LAUNCH(NBV)                                                                      \
-  if (px4) vf::vf_stats_multi_kernel<NBV, 4><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref); \
-  else vf::vf_stats_multi_kernel<NBV, 1><<<grid, 256, 0, st>>>(a, args, npix, B, acc, ref);
-  switch (nb) {
-    case 1: VF_STATS_LAUNCH(1) break;
-    case 2: VF_STATS_LAUNCH(2) break;
-    case 3: VF_STATS_LAUNCH(3) break;
-    case 4: VF_STATS_LAUNCH(4) break;
-    case 5: VF_STATS_LAUNCH(5) break;
-    case 6: VF_STATS_LAUNCH(6) break;
-    case 7: VF_STATS_LAUNCH(7) break;
-    default: VF_STATS_LAUNCH(8) break;
-  }
-#undef VF_STATS_LAUNCH
-  e = cudaGetLastError();
+  const int rows[8] = {0, 1, 2, 3, 4, 5, 6, 7};
+  StatsLaunch sl;
+  int rc = stats_launch(&sl, a, bs, rows, nb, B, npix, acc, (flags & VF_STATS_NO_REF_NORM) ? 0 : 1);
+  if (rc) return rc;
+  e = cudaLaunchKernel(sl.fn, sl.grid, dim3(256), sl.kparams(), 0, st);
   if (e != cudaSuccess) return cuda_fail(e, "vf_stats_multi_kernel launch");
   vf::vf_stats_finalize<<<(unsigned)((nstat + 255) / 256), 256, 0, st>>>(acc, (long long)nstat);
   e = cudaGetLastError();
@@ -783,6 +944,6 @@ const char* vf_status_string(int status) {
 
 const char* vf_last_error(void) { return g_err; }
 
-int vf_version(void) { return 104; }
+int vf_version(void) { return 105; }
 
 }  // extern "C"

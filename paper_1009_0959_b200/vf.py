@@ -27,8 +27,8 @@ VARIANTS = {"exact": VF_EXACT, "minimax": VF_MINIMAX, "poly4": VF_MINIMAX_POLY4,
 ALGOS = {"auto": VF_ALGO_AUTO, "window": VF_ALGO_WINDOW, "shared": VF_ALGO_SHARED, "role": VF_ALGO_ROLE,
          "stream": VF_ALGO_STREAM}
 EXPORTS = ["vf_filter", "vf_filter_batch", "vf_filter_rows", "vf_filter_batch_algo",
-           "vf_host_workspace_bytes", "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_kernels", "vf_plan_destroy",
-           "vf_image_stats", "vf_image_stats_ex", "vf_image_stats_multi", "vf_kernel_info", "vf_status_string", "vf_last_error", "vf_version"]
+           "vf_host_workspace_bytes", "vf_filter_host", "vf_plan_create", "vf_plan_create_ex", "vf_plan_launch", "vf_plan_kernels",
+           "vf_plan_destroy", "vf_image_stats", "vf_image_stats_ex", "vf_image_stats_multi", "vf_kernel_info", "vf_status_string", "vf_last_error", "vf_version"]
 VF_STATS_NO_REF_NORM = 1
 
 
@@ -59,6 +59,7 @@ def load_library(path: str = LIB_PATH):
     L.vf_host_workspace_bytes.restype = S
     L.vf_filter_host.argtypes = [P, I, I, I, I, I, I, P, P, S, P]
     L.vf_plan_create.argtypes = [ctypes.POINTER(P), I, I, I, I, I, P, P, P, P, P, P]
+    L.vf_plan_create_ex.argtypes = [ctypes.POINTER(P), I, I, I, I, I, P, P, P, P, P, P, P, P]
     L.vf_plan_launch.argtypes = [P, P]
     L.vf_plan_destroy.argtypes = [P]
     L.vf_plan_kernels.argtypes = [P]
@@ -72,7 +73,7 @@ def load_library(path: str = LIB_PATH):
     L.vf_last_error.restype = ctypes.c_char_p
     L.vf_version.argtypes = []
     for name in ("vf_filter", "vf_filter_batch", "vf_filter_batch_algo", "vf_filter_rows",
-                 "vf_filter_host", "vf_plan_create", "vf_plan_launch", "vf_plan_kernels", "vf_plan_destroy", "vf_image_stats",
+                 "vf_filter_host", "vf_plan_create", "vf_plan_create_ex", "vf_plan_launch", "vf_plan_kernels", "vf_plan_destroy", "vf_image_stats",
                  "vf_image_stats_ex", "vf_image_stats_multi", "vf_kernel_info", "vf_version"):
         getattr(L, name).restype = I
     _lib = L
@@ -229,10 +230,14 @@ class Plan:
 
     d_in: CUDA uint8 [B, H, W, 3]; d_outs: list of CUDA tensors like d_in;
     combos: list of (criterion, variant); h_in / h_outs: pinned host tensors
-    (optional).  Buffers are bound at creation; call launch() per step."""
+    (optional).  refs (optional, vf_plan_create_ex): refs[i] = index of the
+    filter whose output filter i is compared with (-1: none); stats: CUDA
+    float64 [ncmp, B, 8] (ncmp = number of refs >= 0) written at every launch
+    with vf_image_stats_multi's rows, bit-identical.  Buffers are bound at
+    creation; call launch() per step."""
 
     def __init__(self, d_in: torch.Tensor, d_outs, window: int, combos, h_in: Optional[torch.Tensor] = None,
-                 h_outs=None):
+                 h_outs=None, refs=None, stats: Optional[torch.Tensor] = None):
         L = load_library()
         x = d_in.unsqueeze(0) if d_in.dim() == 3 else d_in
         B, H, W, _ = x.shape
@@ -250,18 +255,36 @@ class Plan:
         for t in (h_outs or []):
             if t.is_cuda or t.dtype != torch.uint8 or t.numel() != x.numel() or not t.is_contiguous():
                 raise ValueError("h_outs[i] must be contiguous host uint8 tensors like d_in")
+        ncmp = 0
+        if refs is not None:
+            refs = [int(r) for r in refs]
+            if len(refs) != n:
+                raise ValueError("one reference index (or -1) per filter")
+            ncmp = sum(1 for r in refs if r >= 0)
+        if ncmp:
+            if (stats is None or not stats.is_cuda or stats.dtype != torch.float64 or not stats.is_contiguous()
+                    or stats.numel() != ncmp * B * 8):
+                raise ValueError(f"stats must be a contiguous CUDA float64 tensor of {ncmp} x {B} x 8")
+            _same_device(x, stats)
         self.device = x.device
-        self._keep = (d_in, list(d_outs), h_in, None if h_outs is None else list(h_outs))
+        self._keep = (d_in, list(d_outs), h_in, None if h_outs is None else list(h_outs), stats)
         crit = (ctypes.c_int * n)(*[_crit(c) for c, _ in combos])
         var = (ctypes.c_int * n)(*[_var(v) for _, v in combos])
         douts = (ctypes.c_void_p * n)(*[t.data_ptr() for t in d_outs])
         houts = None if h_outs is None else (ctypes.c_void_p * n)(*[t.data_ptr() for t in h_outs])
         self._h = ctypes.c_void_p()
         with torch.cuda.device(x.device):
-            rc = L.vf_plan_create(ctypes.byref(self._h), B, H, W, window, n, crit, var, _dev_u8(x, "d_in"), douts,
-                                  None if h_in is None else h_in.data_ptr(), houts)
-        _check(rc, "vf_plan_create")
+            if refs is None:
+                rc = L.vf_plan_create(ctypes.byref(self._h), B, H, W, window, n, crit, var, _dev_u8(x, "d_in"),
+                                      douts, None if h_in is None else h_in.data_ptr(), houts)
+            else:
+                rarr = (ctypes.c_int * n)(*refs)
+                rc = L.vf_plan_create_ex(ctypes.byref(self._h), B, H, W, window, n, crit, var, _dev_u8(x, "d_in"),
+                                         douts, None if h_in is None else h_in.data_ptr(), houts, rarr,
+                                         None if not ncmp else stats.data_ptr())
+        _check(rc, "vf_plan_create_ex" if refs is not None else "vf_plan_create")
         self.n = n
+        self.ncmp = ncmp
 
     def launch(self, stream=None):
         with torch.cuda.device(self.device):

@@ -52,7 +52,8 @@ def test_gpu_arm_json_line():
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert KEYS <= set(d), KEYS - set(d)
-    assert d["dtype"] == "f32" and d["scaling"] == "strong" and d["gpu_launches"] == (3 + 6) * 3   # fused plan: 3 nodes
+    # fused plan with statistics: exp/log node, angular node + remainder strips, 3 statistics nodes, finalize
+    assert d["dtype"] == "f32" and d["scaling"] == "strong" and d["gpu_launches"] == 7 * 3
     assert d["config"]["images"] == 64
     rf = d["roofline"]
     assert rf["bound"] == "alu" and 0 < rf["frac"] < 1.5 and rf["unit"] == "TFLOP/s" and rf["peak"] > 70

@@ -69,7 +69,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_status_strings_and_version(lib):
     from paper_1009_0959_b200 import vf
-    assert vf.vf_version() == 104
+    assert vf.vf_version() == 105
     assert vf.vf_status_string(0) == "VF_OK"
     assert "invalid" in vf.vf_status_string(-1)
     assert "compiled" in vf.vf_status_string(-2)
