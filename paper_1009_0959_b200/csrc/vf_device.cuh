@@ -171,6 +171,22 @@ __device__ __forceinline__ float angular_pair(float ri, float gi, float bi, floa
 #ifndef VF_EXACT_LIBM
 #define VF_EXACT_LIBM 1
 #endif
+// VF_LIBM_ASSUME: the compiler is told each libm argument's range, proved in
+// DESIGN.md 2 (z <= z*_n < 0.75, s = 1 - u in [1/e, 1]), so the inlined logf
+// drops its special-case paths (subnormal scaling, zero / negative / inf /
+// NaN): the call and its result are unchanged, 15% fewer instructions in the
+// log kernel (C4 256 images 4.09 -> 3.47 ms; exp/log node 9.43 -> 8.91 ms).
+// The debug build checks the ranges instead (VF_CHECK).
+#ifndef VF_LIBM_ASSUME
+#define VF_LIBM_ASSUME 1
+#endif
+#if defined(VF_DEBUG)
+#define VF_ASSUME_RANGE(c) VF_CHECK(c)
+#elif VF_LIBM_ASSUME
+#define VF_ASSUME_RANGE(c) __builtin_assume(c)
+#else
+#define VF_ASSUME_RANGE(c) ((void)0)
+#endif
 // ---- exp criterion D_E = 1 - E(z) (reading R2) --------------------------------
 // z = c_E * d1 never exceeds z*_n < 1, so the P:163 cutoff is dead code.
 // ---- log criterion D_L = -ENT(s), s = 1 - u (reading R3) -----------------------
@@ -198,6 +214,7 @@ __device__ __forceinline__ void crit_accumulate(float zu, float& Ri, float& Rj) 
     Rj = __fadd_rn(Rj, v);
   } else if (CRIT == EXPC) {   // exact: 1 - exp(-z)
 #if VF_EXACT_LIBM
+    VF_ASSUME_RANGE(zu >= 0.0f && zu <= 0.75f);      // z <= z*_n < 0.75 (reading R2)
     const float v = __fadd_rn(1.0f, -expf(-zu));
 #else
     const float v = -expm1f(-zu);
@@ -207,6 +224,7 @@ __device__ __forceinline__ void crit_accumulate(float zu, float& Ri, float& Rj) 
   } else {                     // exact: -s ln s, s = 1 - u
     const float ms = __fadd_rn(zu, -1.0f);   // -(1 - u), one rounding
 #if VF_EXACT_LIBM
+    VF_ASSUME_RANGE(ms <= -0.36f && ms >= -1.0f);    // s = 1 - u in [1/e, 1] (reading R3)
     const float l = logf(-ms);
 #else
     const float l = log1pf(-zu);

@@ -188,7 +188,7 @@ __device__ __forceinline__ void acos_branch_exact2(uint32_t pk0, uint32_t pk1, f
 constexpr float ACOS_AMBIG = 1.0f / 65536.0f;
 
 #ifndef VF_STREAM_ACOS
-#define VF_STREAM_ACOS 0   // ARCCOS-branch strategy (tuning knob), see ang_mm_row
+#define VF_STREAM_ACOS 3   // ARCCOS-branch strategy (tuning knob), see ang_mm_row (3: C4 256 images 1.447 -> 1.437 ms)
 #endif
 #ifndef VF_STREAM_UNROLL
 #define VF_STREAM_UNROLL 1   // row-loop unrolling (tuning knob)
@@ -199,13 +199,14 @@ constexpr float ACOS_AMBIG = 1.0f / 65536.0f;
 
 // Table 1 values (reading R5: ARCCOS row on cos for cos < 0.5, else ARCSIN row
 // on tau) of the lane's two pairs for n neighbour record pairs q[i].
-// VF_STREAM_ACOS 0 (default, measured fastest): both rows for every pair,
-// exact predicate inline, no votes; 1: per offset, the ARCCOS row (~1% of
-// pairs) only when some lane of the warp may need it (one vote); 2: the same
-// with the geometry of all n offsets computed first (independent chains, more
-// registers); 3: both rows for every pair, the branch decided on cos.  With 1, 2
-// and 3, pairs within ACOS_AMBIG of cos = 0.5 set `amb`: the caller then
-// re-decides the whole row exactly (ang_mm_row_exact).
+// VF_STREAM_ACOS 0: both rows for every pair, exact predicate inline, no
+// votes; 1: per offset, the ARCCOS row (~1% of pairs) only when some lane of
+// the warp may need it (one vote); 2: the same with the geometry of all n
+// offsets computed first (independent chains, more registers); 3 (default,
+// measured fastest in round 2: 1.437 vs 1.447 ms per 256 C4 images): both
+// rows for every pair, the branch decided on cos.  With 1, 2 and 3, pairs
+// within ACOS_AMBIG of cos = 0.5 set `amb`: the caller then re-decides the
+// whole row exactly (ang_mm_row_exact), so the outputs are those of 0.
 // ZG: zero vector -> 0.
 template <bool ZG, int N, bool EXACT_V = false>
 __device__ __forceinline__ void ang_mm_row(uint32_t pk0, uint32_t pk1, f32x2 nn2, f32x2 nnn2, const uint4 (&q)[N],
@@ -437,7 +438,7 @@ __device__ __forceinline__ void unpack_pair(const PairWords& r, const PairLoad& 
 // (plan-level fusion of BVDF minimax and exact): L writes the minimax output,
 // L2 the exact one; NV = 1: the variant VAR into L (L2 unused).
 #ifndef VF_STREAM_MINB2
-#define VF_STREAM_MINB2 VF_STREAM_MINB   // the fused (NV = 2) kernel
+#define VF_STREAM_MINB2 16   // the fused (NV = 2) kernel: 16 warps per SM, <= 128 registers (3.60 -> 3.51 ms per 256 images; 12: 3.82, 20: 3.60, 24: 3.80)
 #endif
 template <int SEG>
 __device__ __forceinline__ float shup(float v, int d) { return __shfl_up_sync(0xffffffffu, v, d, SEG); }
