@@ -1,6 +1,5 @@
-# C2: fused exp/log node for small plans (VF_PLAN_FUSE=2) vs one node per filter
-B="python bench.py --workload c2 --steps 200 --warmup 20 --no-cpu-baseline --no-paper --no-e2e"
-$B > gpurun_out/c2_default.json 2>/dev/null
-VF_PLAN_FUSE=2 $B > gpurun_out/c2_fuse4.json 2>/dev/null
-VF_LIB=paper_1009_0959_b200/libvf_n8.so VF_PLAN_FUSE=2 $B > gpurun_out/c2_fuse8.json 2>/dev/null
-$B > gpurun_out/c2_default2.json 2>/dev/null
+# final bench (ncu_exec.json of this library committed: traffic + per-kernel ncu records attach) + ncu --set full of the angular streamed kernels
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench exit $?" >> gpurun_out/bench.err
+PROF_IMAGES=256 timeout 1200 ncu --set full --clock-control none -k regex:vf_angular_stream_kernel -c 6 \
+  -o gpurun_out/r02_full_ang python tools/prof_kernels.py > gpurun_out/ncu_full_ang.log 2>&1
+echo "ncu exit $?" >> gpurun_out/ncu_full_ang.log
