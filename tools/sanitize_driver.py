@@ -40,5 +40,17 @@ louts = [torch.empty_like(xl) for _ in combos[:9]]
 lplan = vfb.Plan(xl, louts, 3, combos[:9])
 assert lplan.kernels() < 9
 lplan.launch()
+# the bench's 7-filter plan (pair-major exp/log node, fused angular node) with
+# its statistics nodes, on noisy images and on a constant batch (flat windows:
+# S1 = 0, z = u = 0 -- the edges of the ranges the libm calls are told,
+# checked here by VF_ASSUME_RANGE -> VF_CHECK)
+for xs in (xl, torch.full_like(xl, 77)):
+    pouts = [torch.empty_like(xs) for _ in combos[:7]]
+    st = torch.empty((4, xs.shape[0], 8), dtype=torch.float64, device="cuda")
+    pplan = vfb.Plan(xs, pouts, 3, combos[:7], refs=[-1, 0, -1, 2, 2, -1, 5], stats=st)
+    pplan.launch()
+    for w in (3, 5):
+        for c in (("exp", "exact"), ("log", "exact")):
+            vfb.filter(xs[:1].contiguous(), w, *c)
 torch.cuda.synchronize()
 print("sanitize driver done")
