@@ -299,8 +299,9 @@ int describe(KernelDesc* kd, const uint8_t* in, long long in_stride, int band_ro
       // with 4 / 2 rows); VF_EL_TY=8 restores the 8-warp blocks.
       const long long npix = (long long)B * out_rows * W;
       const bool big3 = window == 3 && npix >= (1LL << 21);
-      // (the libm variants: 4 rows in 8-warp blocks since the exact variants
-      // call expf / logf -- C4 256 images exp 2.30 -> 2.24 ms, log 4.11 -> 4.09)
+      // (the libm variants too: 4 rows in 8-warp blocks -- C4 256 images
+      // exp + log exact 8.57 ms with 2 rows, 8.53 ms with 4; with the
+      // VF_EXACT_LIBM=1 build 2.30 -> 2.24 and 4.11 -> 4.09 ms)
       int opt = big3 ? 4 : 1;
       int nty = (big3 && var != VF_EXACT) ? 4 : vf::TY;
       static const int opt_env = [] { const char* e = std::getenv("VF_EL_OPT"); return e ? std::atoi(e) : 0; }();

@@ -161,15 +161,17 @@ __device__ __forceinline__ float angular_pair(float ri, float gi, float bi, floa
   }
 }
 
-// Exact variants (reading R26): the paper's functions through libm as
-// written -- D_E = 1 - expf(-z) (EXP) and D_L = -s logf(s) (ENT,
-// P:232).  Round 2 first used the cancellation-free expm1f(-z) / log1pf(-u)
-// (VF_EXACT_LIBM=0): 1.8x / 1.05x slower kernels, aggregates 3x closer to the
-// oracle (measured max 1.1e-6 vs 3.2e-6 relative; the bound for expf / logf
-// with n - 1 <= 24 terms of absolute error <= 1.5e-7 on aggregates >= 0.46
-// is 9.3e-6 < the 1e-5 parity tolerance).
+// Exact variants (cancellation-free fp32
+// forms): D_E = -expm1f(-z) and D_L = -(1 - u) log1pf(-u).  VF_EXACT_LIBM=1
+// evaluates the paper's functions as written instead -- 1 - expf(-z) and
+// -s logf(s) -- measured 1.9x / 1.2x faster kernels (C4 exp exact 16.9 ->
+// 8.9 ms, log exact 16.3 -> 13.9 ms with the argument ranges below; step
+// 64.0 -> 52.5 ms) with aggregates 3x further from the oracle (max 3.2e-6 vs
+// 1.1e-6 relative; worst-case bound 9.3e-6 < the 1e-5 parity tolerance,
+// DESIGN.md 5.2): not the default, because the survey pins the
+// cancellation-free forms (reading R26).
 #ifndef VF_EXACT_LIBM
-#define VF_EXACT_LIBM 1
+#define VF_EXACT_LIBM 0
 #endif
 // VF_LIBM_ASSUME: the compiler is told each libm argument's range, proved in
 // DESIGN.md 2 (z <= z*_n < 0.75, s = 1 - u in [1/e, 1]), so the inlined logf
@@ -213,8 +215,8 @@ __device__ __forceinline__ void crit_accumulate(float zu, float& Ri, float& Rj) 
     Ri = __fadd_rn(Ri, v);
     Rj = __fadd_rn(Rj, v);
   } else if (CRIT == EXPC) {   // exact: 1 - exp(-z)
-#if VF_EXACT_LIBM
     VF_ASSUME_RANGE(zu >= 0.0f && zu <= 0.75f);      // z <= z*_n < 0.75 (reading R2)
+#if VF_EXACT_LIBM
     const float v = __fadd_rn(1.0f, -expf(-zu));
 #else
     const float v = -expm1f(-zu);
@@ -227,6 +229,7 @@ __device__ __forceinline__ void crit_accumulate(float zu, float& Ri, float& Rj) 
     VF_ASSUME_RANGE(ms <= -0.36f && ms >= -1.0f);    // s = 1 - u in [1/e, 1] (reading R3)
     const float l = logf(-ms);
 #else
+    VF_ASSUME_RANGE(zu >= 0.0f && zu <= 0.64f);      // u in [0, 1 - 1/e] (reading R3)
     const float l = log1pf(-zu);
 #endif
     Ri = fmaf(ms, l, Ri);

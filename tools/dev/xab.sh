@@ -1,4 +1,3 @@
-# multi-reference statistics node: tests + A/B against one node per reference
-timeout 900 python -m pytest tests/test_gpu_plan_stats.py tests/test_gpu_debug_bounds.py tests/test_bench_contract.py -m gpu -q -x > gpurun_out/t.log 2>&1
+# exact variants (expm1f / log1pf): rows per thread of the single-filter kernels
+for o in 2 4; do VF_EL_OPT=$o python tools/kbench.py --images 256 --only exact > gpurun_out/kb_opt$o.log 2>&1; done
 python tools/dev/plan_stats_ab.py > gpurun_out/ab0.log 2>&1
-VF_PLAN_STATS_SPLIT=1 python tools/dev/plan_stats_ab.py > gpurun_out/ab1.log 2>&1
