@@ -94,11 +94,19 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False, varia
     return target
 
 
+# The paper's exp / log functions as the exact variants (DESIGN.md reading
+# R26; the default library follows the survey's expm1f / log1pf): a variant
+# build measured beside the default and parity-tested
+# (tests/test_gpu_exact_libm.py); selected at run time with VF_LIB.
+PAPER_LIBM = ("paperlibm", ["-DVF_EXACT_LIBM=1"], ["vf_api.cu", "vf_fused.cu"])
+
+
 def build_all(verbose: bool = False) -> None:
-    """libvf.so and libvf_debug.so, compiled concurrently (one nvcc each)."""
+    """libvf.so, libvf_debug.so and libvf_paperlibm.so, compiled concurrently."""
     import concurrent.futures as cf
-    with cf.ThreadPoolExecutor(2) as ex:
-        futs = [ex.submit(build, True, verbose, False), ex.submit(build, True, False, True)]
+    with cf.ThreadPoolExecutor(3) as ex:
+        futs = [ex.submit(build, True, verbose, False), ex.submit(build, True, False, True),
+                ex.submit(build, True, False, False, PAPER_LIBM[0], PAPER_LIBM[1], PAPER_LIBM[2])]
         for f in futs:
             f.result()
 

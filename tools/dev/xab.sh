@@ -1,3 +1,4 @@
-# exact variants (expm1f / log1pf): rows per thread of the single-filter kernels
-for o in 2 4; do VF_EL_OPT=$o python tools/kbench.py --images 256 --only exact > gpurun_out/kb_opt$o.log 2>&1; done
-python tools/dev/plan_stats_ab.py > gpurun_out/ab0.log 2>&1
+# the VF_EXACT_LIBM=1 build: parity test + the whole default bench under it
+timeout 900 python -m pytest tests/test_gpu_exact_libm.py -m gpu -q -x > gpurun_out/t.log 2>&1
+VF_LIB=paper_1009_0959_b200/libvf_paperlibm.so timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_paperlibm.json 2> gpurun_out/bench_paperlibm.err
+VF_LIB=paper_1009_0959_b200/libvf_paperlibm.so timeout 600 python bench.py --workload c2 --steps 50 --warmup 10 --no-cpu-baseline > gpurun_out/bench_c2_paperlibm.json 2>/dev/null
