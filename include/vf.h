@@ -31,6 +31,10 @@
  *                 reach (z <= z*_25, u = 1 - s <= 1 - 1/e):
  *                 degree 5 for D_E (eps 7.86e-8), 7 for D_L (eps 2.95e-7),
  *                 coefficients tests/golden/remez_reach.txt.
+ *   VF_EXACT evaluates the functions with fp32 libm: acosf / asinf (Eq. 6),
+ *   and the cancellation-free -expm1f(-z) and -(1-u) log1pf(-u) (SURVEY
+ *   8(a) a5); the libvf_paperlibm.so build (VF_EXACT_LIBM=1) uses the
+ *   paper's 1 - expf(-z) and -s logf(s) instead (reading R26).
  *   Arithmetic: fp32 on the device, with exact integer geometry (dot
  *   products, squared norms, L1 distances and the cos < 0.5 branch decision
  *   are exact); aggregates agree with the double-precision oracle within
