@@ -238,8 +238,12 @@ VF_API int vf_image_stats_ex(const uint8_t *a, const uint8_t *b, int B, int H, i
  * instead of 7.  Deterministic: every pixel's fp32 CIELAB norm / distance is
  * rounded to 2^-23 fixed point and the sums are integers (64-bit atomics), so
  * results are bit-identical run to run and across kernels (vf_image_stats /
- * _ex call this with nb = 1; plans with statistics produce the same bits).  Errors: VF_EINVAL for NULL pointers, nb outside [1, 8], bad sizes
- * or unknown flags. */
+ * _ex call this with nb = 1; plans with statistics produce the same bits).
+ * The first statistics call (or plan with statistics) on a device allocates
+ * and fills a 1 KB sRGB decoding table there (cudaMalloc + cudaMemcpy, kept
+ * for the process), so that first call must not be inside a stream capture.
+ * Errors: VF_EINVAL for NULL pointers, nb outside [1, 8], bad sizes or
+ * unknown flags; VF_ECUDA if the table cannot be created. */
 VF_API int vf_image_stats_multi(const uint8_t *a, const uint8_t *const *bs, int nb, int B, int H, int W,
                                 double *stats, int flags, void *stream);
 
