@@ -19,3 +19,6 @@ PROF_IMAGES=256 timeout 1200 ncu --set full --clock-control none -k 'regex:fused
   -o gpurun_out/r02_full python tools/prof_kernels.py > gpurun_out/ncu_full.log 2>&1
 echo "ncu full exit $?" >> gpurun_out/ncu_full.log
 tail -2 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log; tail -1 gpurun_out/bench.err
+# after the call, here: python tools/ncu_launches.py gpurun_out/launches.csv --step el_fused5_kernel:1 \
+#   stream_kernelILi1ELi2ELi32:1 stream_kernelILi1ELi2ELi16:1 stats_multi_kernelILi1ELi4:2 \
+#   stats_multi_kernelILi2ELi4:1 stats_finalize:1 > profiles/r02_launches_summary.md
