@@ -174,11 +174,12 @@ __device__ __forceinline__ float angular_pair(float ri, float gi, float bi, floa
 #define VF_EXACT_LIBM 0
 #endif
 // VF_LIBM_ASSUME: the compiler is told each libm argument's range, proved in
-// DESIGN.md 2 (z <= z*_n < 0.75, s = 1 - u in [1/e, 1]), so the inlined logf
-// drops its special-case paths (subnormal scaling, zero / negative / inf /
-// NaN): the call and its result are unchanged, 15% fewer instructions in the
-// log kernel (C4 256 images 4.09 -> 3.47 ms; exp/log node 9.43 -> 8.91 ms).
-// The debug build checks the ranges instead (VF_CHECK).
+// DESIGN.md 2 (z <= z*_n < 0.75, u in [0, 1 - 1/e], s = 1 - u in [1/e, 1]):
+// the calls and their results are unchanged.  It pays for logf (the
+// VF_EXACT_LIBM=1 build: its special-case paths -- subnormal scaling, zero /
+// negative / inf / NaN -- drop out, 15% fewer instructions in the log kernel,
+// C4 256 images 4.09 -> 3.47 ms); expm1f, log1pf and expf compile to the same
+// code.  The debug build checks the ranges instead (VF_CHECK).
 #ifndef VF_LIBM_ASSUME
 #define VF_LIBM_ASSUME 1
 #endif
