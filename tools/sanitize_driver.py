@@ -52,5 +52,17 @@ for xs in (xl, torch.full_like(xl, 77)):
     for w in (3, 5):
         for c in (("exp", "exact"), ("log", "exact")):
             vfb.filter(xs[:1].contiguous(), w, *c)
+# lone impulses in flat images: the windows holding one reach the largest
+# arguments the criteria can take (z = z*_n: 0.716 / 0.742, u = 1 - 1/e; the
+# bounds the libm calls are told), checked by VF_ASSUME_RANGE -> VF_CHECK
+flat = torch.full((2, 96, 160, 3), 90, dtype=torch.uint8, device="cuda")
+flat[0, 40, 70] = torch.tensor([255, 0, 0], dtype=torch.uint8)
+flat[1, 0, 0] = torch.tensor([0, 255, 255], dtype=torch.uint8)
+flat[1, 95, 159] = torch.tensor([255, 255, 255], dtype=torch.uint8)
+for w in (3, 5):
+    for c in (("exp", "exact"), ("log", "exact"), ("exp", "minimax"), ("log", "minimax")):
+        vfb.filter(flat, w, *c, want_index=True, want_agg=True)
+fouts = [torch.empty_like(flat) for _ in combos[:7]]
+vfb.Plan(flat, fouts, 3, combos[:7]).launch()
 torch.cuda.synchronize()
 print("sanitize driver done")
