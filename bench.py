@@ -106,7 +106,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 (5x5) per-kernel section")
     ap.add_argument("--no-paper", action="store_true", help="skip the AMNF/EVMF section (C2 image)")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=16,
+                    help="e2e: timed steps (measured: 6 steps include the pipeline ramp, 163 ms/step; 12: 157; 18: 155)")
     ap.add_argument("--e2e-slots", type=int, default=3, help="e2e: plans pipelined on their own streams")
     ap.add_argument("--images", type=int, default=0, help="(testing) use only the first N images of the batch")
     return ap.parse_args()
