@@ -626,7 +626,12 @@ def run_ours(args):
                                   ", L2 flushed before the launches"),
                     "note": "the step's dominant node holds the exact (libm) exp/log filters: SURVEY 8(d) D4 counts "
                             "only the arithmetic around each libm call, so its algorithmic fraction is low by "
-                            "construction; roofline_minimax holds the paper's approximants (single-filter kernels)"}
+                            "construction; roofline_minimax holds the paper's approximants (single-filter kernels); "
+                            "`executed`: the node's measured pipe utilisations (ncu, profiles/ncu_exec.json)"}
+        rec = d.get("ncu") or {}
+        if rec:
+            roofline["executed"] = {k: rec.get(k) for k in ("fma_pipe_pct", "alu_pipe_pct", "xu_pipe_pct",
+                                                            "issue_active_pct", "warps_active_pct", "registers")}
         mm = {k: v["frac_fp32_alg"] for k, v in kern.items() if not k.endswith("exact")}
         a = kern["angular/minimax"]
         roofline_mm = {"bound": "alu", "kernel": "angular/minimax (BVDF, Eq. 5 + Table 1)", "kernel_name": a["kernel"],
