@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -518,10 +519,21 @@ struct vf_plan_s {
   int nkernels = 0;
 };
 
+// NVTX range over one C-ABI call (header-only NVTX v3: a no-op unless a
+// profiler injects itself, e.g. ncu --nvtx / nsys), so host-side timelines
+// show which entry point issued which kernels.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 extern "C" {
 
 int vf_filter_batch_algo(const uint8_t* imgs, int B, int H, int W, int window, int criterion, int variant, int algo,
                          uint8_t* outs, uint8_t* index, float* aggregates, void* stream) {
+  NvtxRange nvtx_("vf_filter_batch_algo");
   g_err[0] = 0;
   int rc = validate(B, H, W, window, criterion, variant);
   if (rc) return rc;
@@ -549,6 +561,7 @@ int vf_filter(const uint8_t* img, int H, int W, int window, int criterion, int v
 int vf_filter_rows(const uint8_t* band, int band_row0, int band_rows, int H, int W, int out_row0, int out_rows,
                    int window, int criterion, int variant, uint8_t* out, uint8_t* index, float* aggregates,
                    void* stream) {
+  NvtxRange nvtx_("vf_filter_rows");
   g_err[0] = 0;
   int rc = validate(1, H, W, window, criterion, variant);
   if (rc) return rc;
@@ -574,6 +587,7 @@ size_t vf_host_workspace_bytes(int B, int H, int W) {
 
 int vf_filter_host(const uint8_t* h_imgs, int B, int H, int W, int window, int criterion, int variant, uint8_t* h_outs,
                    void* d_workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("vf_filter_host");
   g_err[0] = 0;
   int rc = validate(B, H, W, window, criterion, variant);
   if (rc) return rc;
@@ -631,6 +645,7 @@ int vf_plan_create(vf_plan* plan, int B, int H, int W, int window, int n, const 
 int vf_plan_create_ex(vf_plan* plan, int B, int H, int W, int window, int n, const int* criteria, const int* variants,
                       const uint8_t* d_in, uint8_t* const* d_outs, const uint8_t* h_in, uint8_t* const* h_outs,
                       const int* refs, double* d_stats) {
+  NvtxRange nvtx_("vf_plan_create_ex");
   g_err[0] = 0;
   if (!plan) return fail(VF_EINVAL, "NULL plan pointer");
   *plan = nullptr;
@@ -877,6 +892,7 @@ int vf_plan_create_ex(vf_plan* plan, int B, int H, int W, int window, int n, con
 }
 
 int vf_plan_launch(vf_plan plan, void* stream) {
+  NvtxRange nvtx_("vf_plan_launch");
   g_err[0] = 0;
   if (!plan || !plan->exec) return fail(VF_EINVAL, "invalid plan");
   cudaError_t e = cudaGraphLaunch(plan->exec, (cudaStream_t)stream);
@@ -905,11 +921,13 @@ int vf_image_stats(const uint8_t* a, const uint8_t* b, int B, int H, int W, doub
 
 int vf_image_stats_ex(const uint8_t* a, const uint8_t* b, int B, int H, int W, double* stats, int flags,
                       void* stream) {
+  NvtxRange nvtx_("vf_image_stats_ex");
   return vf_image_stats_multi(a, &b, 1, B, H, W, stats, flags, stream);
 }
 
 int vf_image_stats_multi(const uint8_t* a, const uint8_t* const* bs, int nb, int B, int H, int W, double* stats,
                          int flags, void* stream) {
+  NvtxRange nvtx_("vf_image_stats_multi");
   g_err[0] = 0;
   if (!a || !bs || !stats) return fail(VF_EINVAL, "NULL pointer");
   if (nb < 1 || nb > 8) return fail(VF_EINVAL, "number of compared outputs must be in [1, 8] (got %lld)", nb);
