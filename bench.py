@@ -446,6 +446,24 @@ def kernel_entry(vfb, c, w, B, H, W, ms, peaks, ncu, npix):
 
 
 # ------------------------------------------------------------------ our arm
+def joint_warmup(step, sync, torch, dist, device, min_steps: int, min_s: float) -> int:
+    """Untimed warm-up: at least `min_steps` steps and `min_s` seconds on every
+    rank.  A step may hold a collective (C4's statistics all_gather), so all
+    ranks must run the SAME number of steps: the continue decision is an
+    all_reduce(MAX) of each rank's own wish (a per-rank time test deadlocks
+    the ranks that stop first).  Returns the number of steps run."""
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        step()
+        n += 1
+        sync()
+        more = torch.tensor([float(n < min_steps or time.perf_counter() - t0 < min_s)], device=device)
+        dist.all_reduce(more, op=dist.ReduceOp.MAX)
+        if more.item() == 0.0:
+            return n
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -455,11 +473,20 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # VF_BENCH_BACKEND=gloo (functional check of the N > 1 code path on a box
+    # with fewer GPUs than ranks: ranks share devices round-robin; its timings
+    # are not measurements).  The driver's runs use NCCL, one rank per GPU.
+    backend = os.environ.get("VF_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29533")
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    else:
+        dist.init_process_group(backend, rank=rank, world_size=world)
     vfb.load_library()
     sha = lib_sha256(vfb.vf.LIB_PATH)
     ncu, ncu_note = load_ncu_exec(sha)
@@ -519,12 +546,7 @@ def run_ours(args):
         return par.all_gather_rows(s.permute(1, 0, 2).contiguous(), counts)       # [B, comparisons, 8]
 
     clk = ClockSampler(dev.index).start()
-    tw = time.perf_counter()
-    nw = 0
-    while nw < max(args.warmup, 3) or time.perf_counter() - tw < 1.0:
-        step()
-        nw += 1
-        torch.cuda.synchronize(dev)
+    nw = joint_warmup(step, lambda: torch.cuda.synchronize(dev), torch, dist, dev, max(args.warmup, 3), 1.0)
     # ---- timed region: K steps, per-step CUDA events on the launching stream
     ev = [ev_pair(torch) for _ in range(args.steps)]
     dist.barrier()

@@ -241,3 +241,49 @@ def test_multiprocess_c5_stripes_and_empty_shards(world):
         mm = stats[("angular", "minimax")]
         assert mm.shape == (2, 8) and np.all(mm[:, 0] == 9) and np.all(mm[:, 1] == 27)
         assert np.all(stats[("angular", "exact")][:, 0] == 0)
+
+
+# ---------------------------------------------------------------- bench warm-up with a collective per step
+def _worker_warmup(rank, world, port, q):
+    import sys
+    import time
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    calls = []
+
+    def step():                          # unequal step times + one collective per step (as C4's stats all_gather)
+        time.sleep(0.004 * (rank + 1))
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        calls.append(float(t.item()))
+    if rank == 0:
+        time.sleep(0.3)                  # ranks start their warm-up at different times
+    n = bench.joint_warmup(step, lambda: None, torch, dist, "cpu", 3, 0.5)
+    t = torch.tensor([float(n)])
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)   # would hang / mismatch if the counts differed
+    q.put((rank, n, len(calls), float(t.item()), set(calls)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_joint_warmup_same_step_count(world):
+    """bench.py's warm-up: every rank runs the same number of steps although
+    their step times and start times differ (a per-rank time test deadlocked
+    the N > 1 C4 bench in round 2: the first rank to stop entered the barrier
+    while the others were still in the step's all_gather)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_warmup, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    counts = {n for _, n, _, _, _ in res}
+    assert len(counts) == 1 and min(counts) >= 3, res
+    for _, n, ncalls, tmax, sums in res:
+        assert ncalls == n and tmax == n and sums == {float(world)}
