@@ -292,6 +292,18 @@ def lib_sha256(path):
     return hashlib.sha256(data).hexdigest()
 
 
+def src_sha256():
+    """sha256 of the kernels' sources (csrc/*.cu, csrc/*.cuh, include/vf.h and
+    the build flags): the same on every box, where lib_sha256 can differ
+    between toolchain installs that compile the same sources."""
+    from paper_1009_0959_b200 import build as vfbuild
+    h = hashlib.sha256(" ".join(vfbuild.NVCC_FLAGS).encode() + repr(sorted(vfbuild.SOURCE_FLAGS.items())).encode())
+    for d in vfbuild.deps():
+        with open(d, "rb") as fh:
+            h.update(os.path.basename(d).encode() + b"\0" + fh.read())
+    return h.hexdigest()
+
+
 def load_ncu_exec(sha):
     """profiles/ncu_exec.json (tools/ncu_exec.py): per-kernel ncu pipe
     utilisations captured from a libvf.so; used only if its device code is
@@ -301,9 +313,15 @@ def load_ncu_exec(sha):
             d = json.load(fh)
     except Exception:
         return None, "profiles/ncu_exec.json absent"
-    if d.get("libvf_sha256") != sha:
-        return None, "profiles/ncu_exec.json was captured from other device code (stale): not used"
-    return d, "profiles/ncu_exec.json (%s), same libvf.so sha256" % d.get("command", "?")
+    if d.get("libvf_sha256") == sha:
+        return d, "profiles/ncu_exec.json (%s), same libvf.so sha256" % d.get("command", "?")
+    try:
+        if d.get("src_sha256") and d["src_sha256"] == src_sha256():
+            return d, ("profiles/ncu_exec.json (%s), captured from a libvf.so built from these same kernel sources "
+                       "and flags (src_sha256 match; this build's device-code sha differs)" % d.get("command", "?"))
+    except Exception:
+        pass
+    return None, "profiles/ncu_exec.json was captured from other device code (stale): not used"
 
 
 # ------------------------------------------------------------------ the oracle (both CPU legs, one method)

@@ -199,7 +199,28 @@ __device__ __forceinline__ float angular_pair(float ri, float gi, float bi, floa
 // Every rounding is spelled out (fmaf / __fadd_rn, which the compiler never
 // contracts), so all kernel instantiations (tile shapes, stripes, batches)
 // produce bit-identical aggregates for the same window.
-template <int CRIT, int VAR>
+// VF_EXACT_CALL_MINWIN: windows of at least this width reach the exact
+// variants' libm routine through one out-of-line copy per kernel (CALL) instead
+// of inlining it per pair.  The 5x5 exact kernels unroll 300 pairs: inlined,
+// that is ~10 K instructions (160 KB) of straight-line code and ncu shows
+// 37-42% of the stall samples on no_instructions (instruction-cache misses,
+// profiles/r02_ncu_full_c3.md).  Same routine, same argument, same rounding:
+// the results are bit-identical.
+#ifndef VF_EXACT_CALL_MINWIN
+#define VF_EXACT_CALL_MINWIN 99
+#endif
+#if !VF_EXACT_LIBM
+static __device__ __noinline__ float vf_expm1f_call(float x) {   // x = -z
+  VF_ASSUME_RANGE(x <= 0.0f && x >= -0.75f);
+  return expm1f(x);
+}
+static __device__ __noinline__ float vf_log1pf_call(float x) {   // x = -u
+  VF_ASSUME_RANGE(x <= 0.0f && x >= -0.64f);
+  return log1pf(x);
+}
+#endif
+
+template <int CRIT, int VAR, bool CALL = false>
 __device__ __forceinline__ void crit_accumulate(float zu, float& Ri, float& Rj) {
   if (VAR == MINIMAX) {
     // exp: Delta(z) / Q(z) = 1 - N/Q;  log: -Ntilde(u) / Qtilde(u) = -ENT(1 - u)
@@ -220,7 +241,7 @@ __device__ __forceinline__ void crit_accumulate(float zu, float& Ri, float& Rj) 
 #if VF_EXACT_LIBM
     const float v = __fadd_rn(1.0f, -expf(-zu));
 #else
-    const float v = -expm1f(-zu);
+    const float v = CALL ? -vf_expm1f_call(-zu) : -expm1f(-zu);
 #endif
     Ri = __fadd_rn(Ri, v);
     Rj = __fadd_rn(Rj, v);
@@ -231,7 +252,7 @@ __device__ __forceinline__ void crit_accumulate(float zu, float& Ri, float& Rj) 
     const float l = logf(-ms);
 #else
     VF_ASSUME_RANGE(zu >= 0.0f && zu <= 0.64f);      // u in [0, 1 - 1/e] (reading R3)
-    const float l = log1pf(-zu);
+    const float l = CALL ? vf_log1pf_call(-zu) : log1pf(-zu);
 #endif
     Ri = fmaf(ms, l, Ri);
     Rj = fmaf(ms, l, Rj);

@@ -131,7 +131,7 @@ __device__ __forceinline__ void el_window(const Launch& L, int b, int ox, int oy
     static_for<NPR>([&](auto pc) {
       constexpr int p = decltype(pc)::value;
       const float zu = fmaf(sc, __uint_as_float(keep[p]), bias);   // c * d1, one rounding
-      crit_accumulate<CRIT, VAR>(zu, Ra[pair_i<N>(p)], Ra[pair_j<N>(p)]);
+      crit_accumulate<CRIT, VAR, (VAR == EXACT && WIN >= VF_EXACT_CALL_MINWIN)>(zu, Ra[pair_i<N>(p)], Ra[pair_j<N>(p)]);
     });
   }
   uint32_t ww[N];
@@ -201,7 +201,7 @@ __device__ __forceinline__ void el_window_s1(const Launch& L, int b, int ox, int
       constexpr int i = pair_i<N>(decltype(pc)::value), j = pair_j<N>(decltype(pc)::value);
       const float fb = __uint_as_float(sad4(w[i], w[j], F2P23_BITS));   // 2^23 + d1
       const float zu = fmaf(sc, fb, bias);                               // c * d1, one rounding
-      crit_accumulate<CRIT, VAR>(zu, Ra[i], Ra[j]);
+      crit_accumulate<CRIT, VAR, (WIN >= VF_EXACT_CALL_MINWIN)>(zu, Ra[i], Ra[j]);
     });
   } else {
     // polynomial variants: pairs 2q and 2q + 1 together in packed FP32

@@ -63,7 +63,7 @@ def main():
     sys.path.insert(0, ROOT)
     import bench
     h = bench.lib_sha256(lib)
-    out = {"libvf_sha256": h, "command": "ncu --metrics <tools/ncu_exec.py --metrics> python tools/prof_kernels.py",
+    out = {"libvf_sha256": h, "src_sha256": bench.src_sha256(), "command": "ncu --metrics <tools/ncu_exec.py --metrics> python tools/prof_kernels.py",
            "note": "ncu replays each kernel (serialised, cold caches); pipe percentages are of the kernel's own "
                    "active cycles", "kernels": recs}
     with open(os.path.join(ROOT, "profiles", "ncu_exec.json"), "w") as fh:
