@@ -36,6 +36,32 @@ def test_reference_arm_other_ranks_exit_quietly():
     assert r.returncode == 0 and r.stdout.strip() == "", (r.stdout, r.stderr[-1000:])
 
 
+def test_ncu_exec_attach_rule(tmp_path, monkeypatch):
+    """profiles/ncu_exec.json is attached only if it was captured from this
+    library's device code, or from a library built from these same kernel
+    sources and flags (src_sha256); anything else is reported as stale."""
+    sys.path.insert(0, ROOT)
+    import bench
+    src = bench.src_sha256()
+    assert src == bench.src_sha256() and len(src) == 64
+    os.makedirs(tmp_path / "profiles")
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+
+    def put(d):
+        with open(tmp_path / "profiles" / "ncu_exec.json", "w") as fh:
+            json.dump(d, fh)
+    assert bench.load_ncu_exec("a" * 64)[0] is None                      # absent
+    put({"libvf_sha256": "a" * 64, "kernels": {}})
+    assert bench.load_ncu_exec("a" * 64)[0] is not None                  # same device code
+    d, why = bench.load_ncu_exec("b" * 64)
+    assert d is None and "stale" in why                                  # other device code, no source hash
+    put({"libvf_sha256": "a" * 64, "src_sha256": src, "kernels": {}})
+    d, why = bench.load_ncu_exec("b" * 64)
+    assert d is not None and "src_sha256" in why                         # rebuilt from the same sources
+    put({"libvf_sha256": "a" * 64, "src_sha256": "c" * 64, "kernels": {}})
+    assert bench.load_ncu_exec("b" * 64)[0] is None                      # other sources
+
+
 import pytest  # noqa: E402
 
 
