@@ -209,6 +209,18 @@ __device__ __forceinline__ float angular_pair(float ri, float gi, float bi, floa
 #ifndef VF_EXACT_CALL_MINWIN
 #define VF_EXACT_CALL_MINWIN 99
 #endif
+// VF_EXACT_ROLL_MINWIN: windows of at least this width evaluate the exact
+// variants' pairs in a rolled loop over the cyclic pair offsets (vf_window.cuh,
+// el_window_s1): the libm routine stays inlined, in N copies instead of
+// N (N - 1) / 2.  The aggregates' summation order differs from the unrolled form.
+// Default: the 5x5 kernels, where the unrolled form is ~10 K instructions and
+// ncu shows 37-42% of the stall samples on no_instructions
+// (profiles/r02_ncu_full_c3.md); measured on C3: exp exact 11.80 -> 11.15 ms,
+// log exact 11.55 -> 10.37 ms (123-128 registers instead of 71-76).  The 3x3
+// kernels (36 pairs) keep the unrolled form.
+#ifndef VF_EXACT_ROLL_MINWIN
+#define VF_EXACT_ROLL_MINWIN 5
+#endif
 #if !VF_EXACT_LIBM
 static __device__ __noinline__ float vf_expm1f_call(float x) {   // x = -z
   VF_ASSUME_RANGE(x <= 0.0f && x >= -0.75f);

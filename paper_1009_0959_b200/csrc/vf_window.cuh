@@ -196,7 +196,34 @@ __device__ __forceinline__ void el_window_s1(const Launch& L, int b, int ox, int
   float Ra[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) Ra[k] = -0.0f;   // -0 + v == v: the first add folds away
-  if constexpr (VAR == EXACT) {
+  if constexpr (VAR == EXACT && WIN >= VF_EXACT_ROLL_MINWIN) {
+    // Rolled form (knob): N is odd, so the pairs {k, (k + d) mod N},
+    // d = 1 .. (N - 1) / 2, k = 0 .. N - 1, are every unordered pair once.  One
+    // loop iteration per d with the second sample and its partial aggregate in
+    // registers that rotate by one position per iteration: N inlined libm
+    // calls of code instead of N (N - 1) / 2.
+    uint32_t wb[N];
+    float Rb[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) { wb[k] = w[k]; Rb[k] = -0.0f; }
+#pragma unroll 1
+    for (int d = 1; d <= (N - 1) / 2; ++d) {
+      const uint32_t w0 = wb[0];
+      const float r0 = Rb[0];
+#pragma unroll
+      for (int k = 0; k + 1 < N; ++k) { wb[k] = wb[k + 1]; Rb[k] = Rb[k + 1]; }
+      wb[N - 1] = w0;                                                    // wb[k] = w[(k + d) mod N]
+      Rb[N - 1] = r0;                                                    // Rb[k]: partial aggregate of that sample
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const float fb = __uint_as_float(sad4(w[k], wb[k], F2P23_BITS));   // 2^23 + d1
+        const float zu = fmaf(sc, fb, bias);                               // c * d1, one rounding
+        crit_accumulate<CRIT, VAR>(zu, Ra[k], Rb[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) Ra[(k + (N - 1) / 2) % N] = __fadd_rn(Ra[(k + (N - 1) / 2) % N], Rb[k]);
+  } else if constexpr (VAR == EXACT) {
     static_for<N * (N - 1) / 2>([&](auto pc) {
       constexpr int i = pair_i<N>(decltype(pc)::value), j = pair_j<N>(decltype(pc)::value);
       const float fb = __uint_as_float(sad4(w[i], w[j], F2P23_BITS));   // 2^23 + d1
